@@ -1,0 +1,142 @@
+/*
+ * bfly.h — C ABI of the B200-native butterfly merge (IOTA data-parallel merge step).
+ *
+ * The reference has no FFI: its boundary is the Python module API of
+ * `iota_sim.butterfly` (pkg/src/iota_sim/butterfly.py:22-35).  Each entry point
+ * below replaces one stage of that module; the Python mirror in
+ * paper_2507_17766_b200/butterfly.py binds them with ctypes exactly as a
+ * maintainer of the reference would.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; "d_" = device pointer, "h_" = host pointer;
+ *   - every call returns an int status (BFLY_OK or one of the BFLY_E* codes,
+ *     mapped 1:1 to the reference exception classes in errors.py:4-45) and
+ *     leaves a message in bfly_last_error() (thread-local);
+ *   - device work is stream-ordered on the `stream` argument (a cudaStream_t,
+ *     passed as void* so this header needs no CUDA include); no call
+ *     synchronises the device unless its comment says so.
+ */
+#ifndef BFLY_H_
+#define BFLY_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py) ------------------------------------------ */
+#define BFLY_OK 0
+#define BFLY_E_TOO_FEW_MINERS 1   /* TooFewMinersError       errors.py:28 */
+#define BFLY_E_DEGENERATE 2       /* DegenerateShardsError   errors.py:32 */
+#define BFLY_E_SHAPE 3            /* ShapeError              errors.py:12 */
+#define BFLY_E_INVALID_ARG 4      /* InvalidArgumentError    errors.py:36 */
+#define BFLY_E_CUDA 5             /* CUDA runtime failure (no reference analogue) */
+#define BFLY_E_UNSUPPORTED 6      /* NotImplementedError (e.g. custom reducer) */
+
+/* ---- element types of the miner replicas ------------------------------- */
+#define BFLY_F32 0      /* fp32 wire values ("<f4", butterfly.py:213) */
+#define BFLY_BF16 1     /* bf16 replicas, fp32 accumulation (C4 extension) */
+#define BFLY_F64WIRE 2  /* fp64 payloads rounded to the fp32 wire on load (butterfly.py:213,230) */
+
+/* ---- per-shard status (butterfly.py:151) ------------------------------- */
+#define BFLY_MERGED 0
+#define BFLY_LOST 1
+#define BFLY_DISAGREEMENT 2
+
+/* ---- corruption descriptors (GPU-native form of butterfly.py:168,232-233) */
+#define BFLY_CORR_NONE 0
+#define BFLY_CORR_ADD 1           /* copy = mean + a                              */
+#define BFLY_CORR_SCALE 2         /* copy = mean * a                              */
+#define BFLY_CORR_NOISE 3         /* copy = a * (2u - 1), u = Philox(key, elem)   */
+#define BFLY_CORR_NOISE_ADD 4     /* copy = mean + a * (2u - 1)                   */
+#define BFLY_CORR_HOST 5          /* copy supplied by the caller (Python callable) */
+
+typedef struct bfly_corruption {
+  int32_t kind;   /* BFLY_CORR_* */
+  int32_t pad;
+  double a;       /* constant, scale or noise amplitude */
+  uint64_t key0;  /* Philox4x64-10 key of the noise stream (colluders share it) */
+  uint64_t key1;
+} bfly_corruption_t;
+
+/* ---- merge phases ------------------------------------------------------ */
+#define BFLY_PHASE_ALL 0       /* reduce + compare + decide + adopt/scatter-back */
+#define BFLY_PHASE_REDUCE 1    /* reduce only: means of every element -> d_merged/d_ws */
+#define BFLY_PHASE_FINISH 2    /* compare + decide + adopt, after PHASE_REDUCE and host copies */
+
+typedef struct bfly_merge_args {
+  int32_t n_miners;      /* N = plan.pair_set.n_miners                    (butterfly.py:188) */
+  int32_t redundancy;    /* r: 2 = reference pairs; 3 = triple extension              */
+  int64_t payload_len;   /* P elements                                    (butterfly.py:195) */
+  int64_t n_shards;      /* S = C(N, r)                                   (butterfly.py:57)  */
+  int32_t dtype;         /* BFLY_F32 / BFLY_BF16 / BFLY_F64WIRE                       */
+  int32_t n_alive;       /* number of miners not in `failures`           (butterfly.py:203) */
+  const int32_t* d_assign;        /* [S*r] ascending miner indices of shard s        */
+  const void* const* d_src;       /* [n_alive] replicas of the alive miners, ascending index */
+  const uint8_t* d_failed;        /* [N] 1 = dropped before upload                  */
+  const bfly_corruption_t* d_corr;/* [N] per-miner corruption (kind NONE if honest) */
+  void* const* d_dst;             /* [n_dst] scatter-back targets (in place), or NULL */
+  int32_t n_dst;
+  int32_t pad0;
+  const double* d_fallback;       /* [P] fallback weights, or NULL (butterfly.py:169,268-273) */
+  double* d_merged;               /* [P] fp64 merged vector, or NULL                */
+  double* d_ws;                   /* [P] fp64 workspace, needed when d_merged is NULL
+                                     and some shard is special (lost / corrupted)     */
+  const double* d_host_copies;    /* [r*P] copies for BFLY_CORR_HOST survivors: slot k of
+                                     shard s at d_host_copies[k*P + e]                */
+  uint8_t* d_status;              /* [S] out: BFLY_MERGED / LOST / DISAGREEMENT     */
+  double* d_entries;              /* [N*N] out: agreement matrix, NaN where undefined */
+  uint8_t* d_flagged;             /* [N] out: 1 = flagged miner                     */
+  int32_t* d_source;              /* [S] out: adopted assignee, -1 if fallback; may be NULL */
+  void* d_scratch;                /* scratch, >= bfly_merge_scratch_bytes()         */
+  size_t scratch_bytes;
+  double tolerance;               /* agreement_tolerance (butterfly.py:171)         */
+  int32_t phase;                  /* BFLY_PHASE_*                                   */
+  int32_t pad1;
+} bfly_merge_args_t;
+
+/* ---- library ----------------------------------------------------------- */
+const char* bfly_version(void);
+const char* bfly_last_error(void);
+
+/* C(n, r) shard count; -1 on overflow.  enumerate_pairs  butterfly.py:76-81 */
+int64_t bfly_n_shards(int32_t n_miners, int32_t redundancy);
+
+/* Philox key of RngStream(seed, stream_id): first 16 bytes of
+ * SHA-256(f"{seed}\x1f{stream_id}") as two little-endian u64.
+ * `seed_decimal` is str(int(seed)).   simkernel.py:203-205,216-219 */
+int bfly_philox_key(const char* seed_decimal, const char* stream_id, uint64_t out_key[2]);
+
+/* Shard plan on the host: h_assign[S*r] (ascending members of the combination
+ * assigned to shard s) and h_bounds[S+1] element offsets.
+ * plan_shards  butterfly.py:84-114 (permutation simkernel.py:237-238). */
+int bfly_plan_host(int32_t n_miners, int32_t redundancy, int64_t payload_len, uint64_t key0,
+                   uint64_t key1, int32_t* h_assign, int64_t* h_bounds);
+
+/* Same plan computed on the device (GPU index map).  d_perm[S] receives the
+ * shard -> combination-rank permutation; d_assign[S*r] the members. */
+int bfly_plan_device(int32_t n_miners, int32_t redundancy, int64_t payload_len, uint64_t key0,
+                     uint64_t key1, int64_t* d_perm, int32_t* d_assign, void* stream);
+
+/* Scratch bytes bfly_merge needs for these sizes. */
+size_t bfly_merge_scratch_bytes(int32_t n_miners, int32_t redundancy, int64_t payload_len);
+
+/* One merge round: run_all_reduce  butterfly.py:161-295, device-resident. */
+int bfly_merge(const bfly_merge_args_t* args, void* stream);
+
+/* Pairwise agreement of two device vectors into *d_out (fp64).
+ * agreement  butterfly.py:117-133. */
+int bfly_agreement(const double* d_a, const double* d_b, int64_t len, double tolerance,
+                   double* d_out, void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* Element-wise mean over the rows of a (n_rows, width) fp64 stack, in the
+ * reference's order.  mean_reducer  butterfly.py:156-158. */
+int bfly_mean_rows(const double* d_stack, int32_t n_rows, int64_t width, double* d_out,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFLY_H_ */
