@@ -1,0 +1,23 @@
+# Builds the B200 product library (libbfly.so, in-tree so it travels with gpurun)
+# and the CPU oracle (test infrastructure).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O2,-Wall -Xptxas -v --expt-relaxed-constexpr
+PKG := paper_2507_17766_b200
+SRCS := $(PKG)/csrc/bfly_plan.cu $(PKG)/csrc/bfly_merge.cu
+HDRS := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/bfly.h
+LIB := $(PKG)/libbfly.so
+
+all: $(LIB) oracle
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -f $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

@@ -82,8 +82,8 @@ typedef struct bfly_merge_args {
   int32_t pad0;
   const double* d_fallback;       /* [P] fallback weights, or NULL (butterfly.py:169,268-273) */
   double* d_merged;               /* [P] fp64 merged vector, or NULL                */
-  double* d_ws;                   /* [P] fp64 workspace, needed when d_merged is NULL
-                                     and some shard is special (lost / corrupted)     */
+  double* d_ws;                   /* [P] fp64 means of special (corrupted) shards; may be
+                                     NULL when d_merged is given (then reused in place) */
   const double* d_host_copies;    /* [r*P] copies for BFLY_CORR_HOST survivors: slot k of
                                      shard s at d_host_copies[k*P + e]                */
   uint8_t* d_status;              /* [S] out: BFLY_MERGED / LOST / DISAGREEMENT     */
@@ -130,6 +130,11 @@ int bfly_merge(const bfly_merge_args_t* args, void* stream);
  * agreement  butterfly.py:117-133. */
 int bfly_agreement(const double* d_a, const double* d_b, int64_t len, double tolerance,
                    double* d_out, void* d_scratch, size_t scratch_bytes, void* stream);
+
+/* Copy of one assignee under a corruption descriptor: d_out[i] = corrupt(d_in[i])
+ * for global elements start_elem + i (the GPU form of butterfly.py:232-233). */
+int bfly_apply_corruption(const bfly_corruption_t* h_desc, const double* d_in, int64_t start_elem,
+                          int64_t len, double* d_out, void* stream);
 
 /* Element-wise mean over the rows of a (n_rows, width) fp64 stack, in the
  * reference's order.  mean_reducer  butterfly.py:156-158. */

@@ -1,0 +1,136 @@
+"""ctypes binding of libbfly.so (the C ABI declared in include/bfly.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``).  There
+is no fallback: if the shared object is missing, importing the product raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from . import errors
+
+_SO = Path(__file__).resolve().parent / "libbfly.so"
+
+OK = 0
+E_TOO_FEW_MINERS, E_DEGENERATE, E_SHAPE, E_INVALID_ARG, E_CUDA, E_UNSUPPORTED = 1, 2, 3, 4, 5, 6
+F32, BF16, F64WIRE = 0, 1, 2
+MERGED, LOST, DISAGREEMENT = 0, 1, 2
+STATUS_NAMES = ("merged", "lost", "disagreement")
+CORR_NONE, CORR_ADD, CORR_SCALE, CORR_NOISE, CORR_NOISE_ADD, CORR_HOST = 0, 1, 2, 3, 4, 5
+PHASE_ALL, PHASE_REDUCE, PHASE_FINISH = 0, 1, 2
+
+# every symbol include/bfly.h declares (tests/test_capi.py checks the export table)
+EXPORTS = (
+    "bfly_version",
+    "bfly_last_error",
+    "bfly_n_shards",
+    "bfly_philox_key",
+    "bfly_plan_host",
+    "bfly_plan_device",
+    "bfly_merge_scratch_bytes",
+    "bfly_merge",
+    "bfly_agreement",
+    "bfly_apply_corruption",
+    "bfly_mean_rows",
+)
+
+
+class Corruption(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+        ("a", ctypes.c_double),
+        ("key0", ctypes.c_uint64),
+        ("key1", ctypes.c_uint64),
+    ]
+
+
+class MergeArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_miners", ctypes.c_int32),
+        ("redundancy", ctypes.c_int32),
+        ("payload_len", ctypes.c_int64),
+        ("n_shards", ctypes.c_int64),
+        ("dtype", ctypes.c_int32),
+        ("n_alive", ctypes.c_int32),
+        ("d_assign", ctypes.c_void_p),
+        ("d_src", ctypes.c_void_p),
+        ("d_failed", ctypes.c_void_p),
+        ("d_corr", ctypes.c_void_p),
+        ("d_dst", ctypes.c_void_p),
+        ("n_dst", ctypes.c_int32),
+        ("pad0", ctypes.c_int32),
+        ("d_fallback", ctypes.c_void_p),
+        ("d_merged", ctypes.c_void_p),
+        ("d_ws", ctypes.c_void_p),
+        ("d_host_copies", ctypes.c_void_p),
+        ("d_status", ctypes.c_void_p),
+        ("d_entries", ctypes.c_void_p),
+        ("d_flagged", ctypes.c_void_p),
+        ("d_source", ctypes.c_void_p),
+        ("d_scratch", ctypes.c_void_p),
+        ("scratch_bytes", ctypes.c_size_t),
+        ("tolerance", ctypes.c_double),
+        ("phase", ctypes.c_int32),
+        ("pad1", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libbfly.so once; raise loudly when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _SO.exists():
+        raise ImportError(f"{_SO} is missing: build the CUDA library first (`make` or __graft_entry__.build())")
+    L = ctypes.CDLL(str(_SO))
+    i32, i64, u64, dbl, vp, sz = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                                  ctypes.c_void_p, ctypes.c_size_t)
+    L.bfly_version.restype = ctypes.c_char_p
+    L.bfly_last_error.restype = ctypes.c_char_p
+    L.bfly_n_shards.argtypes = [i32, i32]
+    L.bfly_n_shards.restype = i64
+    L.bfly_philox_key.argtypes = [ctypes.c_char_p, ctypes.c_char_p, vp]
+    L.bfly_plan_host.argtypes = [i32, i32, i64, u64, u64, vp, vp]
+    L.bfly_plan_device.argtypes = [i32, i32, i64, u64, u64, vp, vp, vp]
+    L.bfly_merge_scratch_bytes.argtypes = [i32, i32, i64]
+    L.bfly_merge_scratch_bytes.restype = sz
+    L.bfly_merge.argtypes = [ctypes.POINTER(MergeArgs), vp]
+    L.bfly_agreement.argtypes = [vp, vp, i64, dbl, vp, vp, sz, vp]
+    L.bfly_apply_corruption.argtypes = [ctypes.POINTER(Corruption), vp, i64, i64, vp, vp]
+    L.bfly_mean_rows.argtypes = [vp, i32, i64, vp, vp]
+    for name in EXPORTS:  # fail at load time if the export table is incomplete
+        getattr(L, name)
+    _lib = L
+    return L
+
+
+_ERRORS = {
+    E_TOO_FEW_MINERS: errors.TooFewMinersError,
+    E_DEGENERATE: errors.DegenerateShardsError,
+    E_SHAPE: errors.ShapeError,
+    E_INVALID_ARG: errors.InvalidArgumentError,
+    E_UNSUPPORTED: NotImplementedError,
+}
+
+
+def check(rc: int) -> None:
+    """Map a BFLY_E* status to the reference exception class (errors.py:4-45)."""
+    if rc == OK:
+        return
+    msg = lib().bfly_last_error().decode(errors="replace")
+    if rc == E_CUDA:
+        raise RuntimeError(f"CUDA error in libbfly: {msg}")
+    raise _ERRORS.get(rc, RuntimeError)(msg)
+
+
+def philox_key(seed: int, stream_id: str) -> tuple[int, int]:
+    """Key of RngStream(seed, stream_id) (simkernel.py:203-205), via the library's SHA-256."""
+    out = (ctypes.c_uint64 * 2)()
+    check(lib().bfly_philox_key(str(int(seed)).encode(), stream_id.encode(), out))
+    return int(out[0]), int(out[1])

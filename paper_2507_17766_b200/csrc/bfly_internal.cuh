@@ -1,0 +1,61 @@
+// bfly_internal.cuh — shared internals of libbfly (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/bfly.h"
+#include "bfly_index.cuh"
+
+namespace bfly {
+
+// thread-local error text behind bfly_last_error()
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+int sm_count();
+
+// Per-shard class computed by the classify kernel.
+enum ShardClass : uint8_t {
+  kFast = 0,     // >= 1 survivor, all survivors honest: mean is final (status merged)
+  kSpecial = 1,  // >= 1 corrupted survivor: compare copies, adopt or fall back
+  kLost = 2,     // no survivor: fallback (butterfly.py:264-273)
+};
+
+constexpr int kMaxR = 3;            // device path supports r = 2 (reference) and 3 (extension)
+constexpr int kThreads = 256;       // CTA size of the streaming kernels
+constexpr int kChunk = 16384;       // elements per CTA in the per-shard special kernels
+
+struct ScratchLayout {
+  int64_t S = 0, cps = 0;
+  int npairs = 0;
+  size_t off_cls = 0, off_source = 0, off_stats = 0, off_scores = 0, off_has = 0, off_inv = 0;
+  size_t total = 0;
+  void init(int32_t n, int32_t r, int64_t P) {
+    S = binom(n, r);
+    npairs = r * (r - 1) / 2;
+    Bounds b;
+    b.init(P, S > 0 ? S : 1);
+    const int64_t maxlen = b.base + (b.rem ? 1 : 0);
+    cps = (maxlen + kChunk - 1) / kChunk;
+    if (cps < 1) cps = 1;
+    auto align = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    size_t o = 0;
+    off_cls = o;
+    o = align(o + (size_t)S);
+    off_source = o;
+    o = align(o + sizeof(int32_t) * (size_t)S);
+    off_stats = o;
+    o = align(o + sizeof(double) * 4 * (size_t)S * (size_t)cps * (size_t)npairs);
+    off_scores = o;
+    o = align(o + sizeof(double) * (size_t)S * (size_t)npairs);
+    off_has = o;
+    o = align(o + (size_t)S * (size_t)npairs);
+    off_inv = o;
+    o = align(o + sizeof(int32_t) * (size_t)S);
+    total = o;
+  }
+};
+
+}  // namespace bfly

@@ -1,0 +1,822 @@
+// bfly_merge.cu — one butterfly merge round on the device (run_all_reduce,
+// butterfly.py:161-295), for r = 2 (reference) and r = 3 (extension).
+//
+// Kernels, in launch order (all on the caller's stream, no host sync):
+//   k_fill_nan      entries[N*N] = NaN                         (butterfly.py:243)
+//   k_classify      per shard: survivors, class fast/special/lost, status and
+//                   entry 1.0 for all-honest shards               (:219-224,:248-263)
+//   k_reduce  ★     the HBM stream: per element, fp64 sequential mean over the
+//                   alive replicas in ascending miner order (numpy's order,
+//                   :225-231,:156-158), scatter-back in place into every miner
+//                   replica for fast shards, fp64 merged / workspace otherwise
+//   k_stats         special shards: per-assignee copies (corruption descriptors
+//                   or host-supplied copies, :232-233), per chunk max|a-b|, a.b,
+//                   a.a, b.b for every surviving assignee pair     (:117-133)
+//   k_decide        one warp per special shard: fixed-order combine, agreement
+//                   score, adopt / disagreement / flags            (:248-273)
+//   k_entries3      r = 3 only: entry = min over the shards a pair shares
+//   k_apply         special + lost shards: adopted copy or fallback into the
+//                   merged vector and every replica               (:259-273)
+//
+// Determinism: no floating-point atomics; every reduction has a fixed order.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "bfly_internal.cuh"
+
+namespace bfly {
+
+// ---------------------------------------------------------------------------
+// element types
+// ---------------------------------------------------------------------------
+
+// 256-bit (32-byte) global accesses — new on sm_100: one LDG.256 / STG.256 per
+// thread per replica halves the load/store instruction count of 128-bit code.
+struct V8 {
+  uint32_t w[8];
+};
+
+__device__ __forceinline__ V8 ld_stream(const void* p) {
+  V8 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                 "=r"(r.w[6]), "=r"(r.w[7])
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, const V8& v) {
+  asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v.w[0]),
+               "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+               : "memory");
+}
+__device__ __forceinline__ void st_f64x4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// fp32 wire values, fp64 accumulation (the reference path).
+struct DF32 {
+  static constexpr int K = 8;  // elements per 32-byte vector
+  using Acc = double;
+  __device__ static Acc zero() { return 0.0; }
+  __device__ static Acc load(const void* p, int64_t e) { return (double)__ldg((const float*)p + e); }
+  __device__ static double raw(const void* p, int64_t e) { return (double)((const float*)p)[e]; }
+  __device__ static void unpack(const V8& v, Acc* x) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (double)__uint_as_float(v.w[k]);
+  }
+  __device__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ static Acc mean(Acc s, int n) { return __ddiv_rn(s, (double)n); }
+  __device__ static double widen(Acc m) { return m; }
+  __device__ static void store(void* p, int64_t e, double v) { ((float*)p)[e] = __double2float_rn(v); }
+  __device__ static V8 pack(const Acc* m) {
+    V8 v;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v.w[k] = __float_as_uint(__double2float_rn(m[k]));
+    return v;
+  }
+};
+
+// bf16 replicas, fp32 accumulation (extension, BASELINE config 4).
+struct DBF16 {
+  static constexpr int K = 16;
+  using Acc = float;
+  __device__ static Acc zero() { return 0.0f; }
+  __device__ static float bf(uint32_t bits16) { return __uint_as_float(bits16 << 16); }
+  __device__ static Acc load(const void* p, int64_t e) {
+    return bf(((const unsigned short*)p)[e]);
+  }
+  __device__ static double raw(const void* p, int64_t e) { return (double)load(p, e); }
+  __device__ static void unpack(const V8& v, Acc* x) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x[2 * k] = __uint_as_float(v.w[k] << 16);
+      x[2 * k + 1] = __uint_as_float(v.w[k] & 0xffff0000u);
+    }
+  }
+  __device__ static Acc add(Acc a, Acc b) { return __fadd_rn(a, b); }
+  __device__ static Acc mean(Acc s, int n) { return __fdiv_rn(s, (float)n); }
+  __device__ static double widen(Acc m) { return (double)m; }
+  __device__ static unsigned short to_bits(float f) {
+    __nv_bfloat16 h = __float2bfloat16_rn(f);
+    return *reinterpret_cast<unsigned short*>(&h);
+  }
+  __device__ static void store(void* p, int64_t e, double v) {
+    ((unsigned short*)p)[e] = to_bits(__double2float_rn(v));
+  }
+  __device__ static V8 pack(const Acc* m) {
+    V8 v;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v.w[k] = (uint32_t)to_bits(m[2 * k]) | ((uint32_t)to_bits(m[2 * k + 1]) << 16);
+    return v;
+  }
+};
+
+// fp64 payloads rounded to the fp32 wire on load (astype("<f4"), butterfly.py:213,230).
+struct DF64W {
+  static constexpr int K = 4;
+  using Acc = double;
+  __device__ static Acc zero() { return 0.0; }
+  __device__ static Acc load(const void* p, int64_t e) {
+    return (double)__double2float_rn(__ldg((const double*)p + e));
+  }
+  __device__ static double raw(const void* p, int64_t e) { return ((const double*)p)[e]; }
+  __device__ static void unpack(const V8& v, Acc* x) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      x[k] = (double)__double2float_rn(__hiloint2double((int)v.w[2 * k + 1], (int)v.w[2 * k]));
+  }
+  __device__ static Acc add(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ static Acc mean(Acc s, int n) { return __ddiv_rn(s, (double)n); }
+  __device__ static double widen(Acc m) { return m; }
+  __device__ static void store(void* p, int64_t e, double v) { ((double*)p)[e] = v; }
+  __device__ static V8 pack(const Acc* m) {
+    V8 v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v.w[2 * k] = (uint32_t)__double2loint(m[k]);
+      v.w[2 * k + 1] = (uint32_t)__double2hiint(m[k]);
+    }
+    return v;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// parameters
+// ---------------------------------------------------------------------------
+
+struct Params {
+  int32_t n, r, n_alive, n_dst, npairs;
+  int64_t P, S, cps;
+  Bounds bnd;
+  const int32_t* assign;
+  const void* const* src;
+  const uint8_t* failed;
+  const bfly_corruption_t* corr;
+  void* const* dst;
+  const double* fallback;
+  double* merged;
+  double* ws;  // means of special shards (aliases merged when no separate workspace)
+  const double* host_copies;
+  uint8_t* status;
+  double* entries;
+  uint8_t* flagged;
+  int32_t* source;
+  uint8_t* cls;
+  double* stats;
+  double* scores;
+  uint8_t* has_score;
+  int32_t* inv;
+  double tol;
+};
+
+__device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000LL); }
+
+// numpy DOUBLE_pairwise_sum over the alive replicas at element e (width-1 shards).
+template <class D>
+__device__ double pairwise_alive(const void* const* src, int lo, int n, int64_t e) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, D::load(src[lo + i], e));
+    return res;
+  } else if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = D::load(src[lo + k], e);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], D::load(src[lo + i + k], e));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, D::load(src[lo + i], e));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_alive<D>(src, lo, n2, e), pairwise_alive<D>(src, lo + n2, n - n2, e));
+}
+
+template <class D>
+__device__ __forceinline__ typename D::Acc mean_at(const void* const* src, int n_alive, int64_t e,
+                                                   bool width1) {
+  if constexpr (sizeof(typename D::Acc) == 8) {
+    if (width1) return D::mean(__dadd_rn(0.0, pairwise_alive<D>(src, 0, n_alive, e)), n_alive);
+  }
+  typename D::Acc acc = D::zero();
+  for (int q = 0; q < n_alive; ++q) acc = D::add(acc, D::load(src[q], e));
+  return D::mean(acc, n_alive);
+}
+
+// ---------------------------------------------------------------------------
+// k_fill_nan / k_classify
+// ---------------------------------------------------------------------------
+
+__global__ void k_fill_nan(double* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = nan64();
+}
+
+__device__ __forceinline__ int pair_index(int r, int a, int b) {  // slot pair (a<b) -> 0..npairs-1
+  int idx = 0;
+  for (int x = 0; x < a; ++x) idx += r - 1 - x;
+  return idx + (b - a - 1);
+}
+
+__global__ void k_classify(Params p) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= p.S) return;
+  const int32_t* mem = p.assign + s * p.r;
+  int ns = 0, first = -1;
+  bool corrupted = false;
+  for (int k = 0; k < p.r; ++k) {
+    const int m = mem[k];
+    if (p.failed[m]) continue;
+    if (first < 0) first = m;
+    ++ns;
+    if (p.corr[m].kind != BFLY_CORR_NONE) corrupted = true;
+  }
+  if (p.inv) p.inv[rank_combination(p.n, p.r, mem)] = (int32_t)s;
+  uint8_t c;
+  if (ns == 0 || p.n_alive == 0) {
+    c = kLost;
+    p.status[s] = BFLY_LOST;
+    p.source[s] = -1;
+  } else if (corrupted) {
+    c = kSpecial;
+  } else {
+    c = kFast;
+    if (p.r > 2)
+      for (int q = 0; q < p.npairs; ++q) p.has_score[s * p.npairs + q] = 0;
+    p.status[s] = BFLY_MERGED;
+    p.source[s] = first;
+    // every surviving pair agrees exactly (identical reductions, max|a-b| = 0)
+    for (int a = 0; a < p.r; ++a)
+      for (int b = a + 1; b < p.r; ++b) {
+        const int i = mem[a], j = mem[b];
+        if (p.failed[i] || p.failed[j]) continue;
+        if (p.r == 2) {
+          p.entries[(int64_t)i * p.n + j] = 1.0;
+          p.entries[(int64_t)j * p.n + i] = 1.0;
+        } else {
+          p.scores[s * p.npairs + pair_index(p.r, a, b)] = 1.0;
+          p.has_score[s * p.npairs + pair_index(p.r, a, b)] = 1;
+        }
+      }
+  }
+  if (c != kFast && p.r > 2)
+    for (int q = 0; q < p.npairs; ++q) p.has_score[s * p.npairs + q] = 0;
+  p.cls[s] = c;
+}
+
+// ---------------------------------------------------------------------------
+// k_reduce — the streaming mean + scatter-back
+// ---------------------------------------------------------------------------
+
+constexpr int kVecPerThread = 1;
+
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
+  extern __shared__ __align__(16) const void* s_ptr[];  // [n_alive] src, then [n_dst] dst
+  const void** s_src = s_ptr;
+  void** s_dst = const_cast<void**>(s_ptr + p.n_alive);
+  uintptr_t mis = 0;
+  for (int q = threadIdx.x; q < p.n_alive; q += blockDim.x) {
+    s_src[q] = p.src[q];
+    mis |= (uintptr_t)p.src[q];
+  }
+  for (int q = threadIdx.x; q < p.n_dst; q += blockDim.x) {
+    s_dst[q] = p.dst[q];
+    mis |= (uintptr_t)p.dst[q];
+  }
+  if (threadIdx.x == 0) mis |= (uintptr_t)p.merged;
+  const bool aligned = __syncthreads_or((int)(mis & 31)) == 0;
+
+  constexpr int K = D::K;
+  constexpr int TILE = kThreads * kVecPerThread * K;
+  const int64_t ntiles = (p.P + TILE - 1) / TILE;
+  const bool may_width1 = p.bnd.base == 1;
+  using Acc = typename D::Acc;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = tile * TILE;
+    const int64_t t1 = t0 + TILE < p.P ? t0 + TILE : p.P;
+    // uniform per tile: are all covered shards fast (and not width-1)?
+    const int64_t s_lo = p.bnd.shard_of(t0), s_hi = p.bnd.shard_of(t1 - 1);
+    bool fast = aligned && (t1 - t0 == TILE);
+    for (int64_t s = s_lo; fast && s <= s_hi; ++s)
+      fast = p.cls[s] == kFast && !(may_width1 && s >= p.bnd.rem);
+
+    if (fast) {
+      Acc acc[kVecPerThread][K];
+#pragma unroll
+      for (int v = 0; v < kVecPerThread; ++v)
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[v][k] = D::zero();
+      const int64_t vbase = t0 / K + threadIdx.x;  // 32-byte vector index
+      int q = 0;
+      constexpr int U = 4;  // replicas in flight per thread
+      for (; q + U <= p.n_alive; q += U) {
+        V8 raw[U][kVecPerThread];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < kVecPerThread; ++v)
+            raw[u][v] = ld_stream(reinterpret_cast<const V8*>(s_src[q + u]) + vbase + v * kThreads);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int v = 0; v < kVecPerThread; ++v) {
+            Acc x[K];
+            D::unpack(raw[u][v], x);
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[v][k] = D::add(acc[v][k], x[k]);
+          }
+      }
+      for (; q < p.n_alive; ++q) {
+#pragma unroll
+        for (int v = 0; v < kVecPerThread; ++v) {
+          Acc x[K];
+          D::unpack(ld_stream(reinterpret_cast<const V8*>(s_src[q]) + vbase + v * kThreads), x);
+#pragma unroll
+          for (int k = 0; k < K; ++k) acc[v][k] = D::add(acc[v][k], x[k]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < kVecPerThread; ++v) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[v][k] = D::mean(acc[v][k], p.n_alive);
+        const int64_t e0 = (vbase + v * kThreads) * K;
+        if (p.merged) {
+#pragma unroll
+          for (int k = 0; k < K; k += 4)
+            st_f64x4(p.merged + e0 + k, D::widen(acc[v][k]), D::widen(acc[v][k + 1]), D::widen(acc[v][k + 2]),
+                     D::widen(acc[v][k + 3]));
+        }
+        const V8 out = D::pack(acc[v]);
+        for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vbase + v * kThreads, out);
+      }
+    } else {
+      for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
+        const int64_t s = p.bnd.shard_of(e);
+        const uint8_t c = p.cls[s];
+        if (c == kLost) continue;
+        const bool w1 = p.bnd.len(s) == 1;
+        const Acc m = mean_at<D>(s_src, p.n_alive, e, w1);
+        if (c == kFast) {
+          if (p.merged) p.merged[e] = D::widen(m);
+          for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(m));
+        } else {
+          p.ws[e] = D::widen(m);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// special shards: copies, statistics, decision, adoption
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double corrupt_value(const bfly_corruption_t& c, double mean, int64_t e,
+                                                const double* host_copies, int slot, int64_t P) {
+  switch (c.kind) {
+    case BFLY_CORR_ADD: return __dadd_rn(mean, c.a);
+    case BFLY_CORR_SCALE: return __dmul_rn(mean, c.a);
+    case BFLY_CORR_NOISE:
+    case BFLY_CORR_NOISE_ADD: {
+      const double noise = __dmul_rn(c.a, noise_unit(philox_word(c.key0, c.key1, (uint64_t)e)));
+      return c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(mean, noise);
+    }
+    case BFLY_CORR_HOST: return host_copies[(int64_t)slot * P + e];
+    default: return mean;
+  }
+}
+
+__device__ __forceinline__ double max_nan(double a, double b) {
+  return (isnan(a) || isnan(b)) ? nan64() : fmax(a, b);
+}
+
+struct PairStat {
+  double mx, ab, aa, bb;
+};
+
+__device__ __forceinline__ PairStat warp_combine(PairStat s) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    s.mx = max_nan(s.mx, __shfl_xor_sync(0xffffffffu, s.mx, off));
+    s.ab = __dadd_rn(s.ab, __shfl_xor_sync(0xffffffffu, s.ab, off));
+    s.aa = __dadd_rn(s.aa, __shfl_xor_sync(0xffffffffu, s.aa, off));
+    s.bb = __dadd_rn(s.bb, __shfl_xor_sync(0xffffffffu, s.bb, off));
+  }
+  return s;
+}
+
+// CTA-wide fixed-order combine; result valid in thread 0.
+__device__ PairStat block_combine(PairStat s) {
+  __shared__ PairStat part[kThreads / 32];
+  s = warp_combine(s);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) part[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    s = lane < kThreads / 32 ? part[lane] : PairStat{0.0, 0.0, 0.0, 0.0};
+    s = warp_combine(s);
+  }
+  return s;
+}
+
+// agreement decision from combined statistics (butterfly.py:127-133)
+__device__ __forceinline__ double score_of(const PairStat& s, double tol) {
+  if (!isnan(s.mx) && s.mx <= tol) return 1.0;
+  const double na = sqrt(s.aa), nb = sqrt(s.bb);
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  const double c = __ddiv_rn(s.ab, __dmul_rn(na, nb));
+  if (isnan(c)) return c;
+  return c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+}
+
+__global__ void __launch_bounds__(kThreads) k_stats(Params p) {
+  const int64_t s = blockIdx.x;
+  if (p.cls[s] != kSpecial) return;
+  const int64_t lo = p.bnd.start(s) + (int64_t)blockIdx.y * kChunk;
+  const int64_t hi_s = p.bnd.start(s) + p.bnd.len(s);
+  const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
+  const int32_t* mem = p.assign + s * p.r;
+  bool alive[kMaxR];
+  bfly_corruption_t c[kMaxR];
+  for (int k = 0; k < p.r; ++k) {
+    alive[k] = !p.failed[mem[k]];
+    c[k] = p.corr[mem[k]];
+  }
+  for (int a = 0; a < p.r; ++a)
+    for (int b = a + 1; b < p.r; ++b) {
+      if (!alive[a] || !alive[b]) continue;
+      PairStat st{0.0, 0.0, 0.0, 0.0};
+      for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+        const double m = p.ws[e];
+        const double x = corrupt_value(c[a], m, e, p.host_copies, a, p.P);
+        const double y = corrupt_value(c[b], m, e, p.host_copies, b, p.P);
+        st.mx = max_nan(st.mx, fabs(__dsub_rn(x, y)));
+        st.ab = fma(x, y, st.ab);
+        st.aa = fma(x, x, st.aa);
+        st.bb = fma(y, y, st.bb);
+      }
+      st = block_combine(st);
+      if (threadIdx.x == 0) {
+        double* o = p.stats + ((s * p.cps + blockIdx.y) * p.npairs + pair_index(p.r, a, b)) * 4;
+        o[0] = st.mx;
+        o[1] = st.ab;
+        o[2] = st.aa;
+        o[3] = st.bb;
+      }
+    }
+}
+
+// One warp per shard.
+__global__ void k_decide(Params p) {
+  const int64_t s = blockIdx.x;
+  if (p.cls[s] != kSpecial) return;
+  const int lane = threadIdx.x;
+  const int32_t* mem = p.assign + s * p.r;
+  const int64_t len = p.bnd.len(s);
+  const int64_t nchunks = (len + kChunk - 1) / kChunk;
+  int surv[kMaxR], ns = 0;
+  for (int k = 0; k < p.r; ++k)
+    if (!p.failed[mem[k]]) surv[ns++] = k;
+  bool agree[kMaxR][kMaxR] = {};
+  for (int x = 0; x < ns; ++x)
+    for (int y = x + 1; y < ns; ++y) {
+      const int pi = pair_index(p.r, surv[x], surv[y]);
+      PairStat st{0.0, 0.0, 0.0, 0.0};
+      for (int64_t ch = lane; ch < nchunks; ch += 32) {
+        const double* o = p.stats + ((s * p.cps + ch) * p.npairs + pi) * 4;
+        st.mx = max_nan(st.mx, o[0]);
+        st.ab = __dadd_rn(st.ab, o[1]);
+        st.aa = __dadd_rn(st.aa, o[2]);
+        st.bb = __dadd_rn(st.bb, o[3]);
+      }
+      st = warp_combine(st);
+      const double sc = score_of(st, p.tol);
+      agree[x][y] = agree[y][x] = sc == 1.0;
+      if (lane == 0) {
+        const int i = mem[surv[x]], j = mem[surv[y]];
+        if (p.r == 2) {
+          p.entries[(int64_t)i * p.n + j] = sc;
+          p.entries[(int64_t)j * p.n + i] = sc;
+        } else {
+          p.scores[s * p.npairs + pi] = sc;
+          p.has_score[s * p.npairs + pi] = 1;
+        }
+      }
+    }
+  if (lane != 0) return;
+  // adopt the lowest survivor backed by a strict majority of the survivors
+  // (r = 2: both agree, or a lone survivor — butterfly.py:255-263)
+  int src = -1;
+  for (int x = 0; x < ns && src < 0; ++x) {
+    int cnt = 1;
+    for (int y = 0; y < ns; ++y)
+      if (y != x && agree[x][y]) ++cnt;
+    if (2 * cnt > ns) src = x;
+  }
+  if (src >= 0) {
+    p.status[s] = BFLY_MERGED;
+    p.source[s] = mem[surv[src]];
+    for (int y = 0; y < ns; ++y)
+      if (y != src && !agree[src][y]) p.flagged[mem[surv[y]]] = 1;
+  } else {
+    p.status[s] = ns >= 2 ? BFLY_DISAGREEMENT : BFLY_LOST;
+    p.source[s] = -1;
+    if (ns >= 2)
+      for (int y = 0; y < ns; ++y) p.flagged[mem[surv[y]]] = 1;
+  }
+}
+
+// r = 3: entries[i][j] = min over the N-2 shards sharing {i, j} (NaN poisons).
+__global__ void k_entries3(Params p) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)p.n * p.n) return;
+  const int i = (int)(t / p.n), j = (int)(t % p.n);
+  if (i >= j) return;
+  double best = nan64();
+  bool any = false, poisoned = false;
+  for (int x = 0; x < p.n && !poisoned; ++x) {
+    if (x == i || x == j) continue;
+    int32_t m[3];
+    int a, b;  // slots of i and j
+    if (x < i) { m[0] = x; m[1] = i; m[2] = j; a = 1; b = 2; }
+    else if (x < j) { m[0] = i; m[1] = x; m[2] = j; a = 0; b = 2; }
+    else { m[0] = i; m[1] = j; m[2] = x; a = 0; b = 1; }
+    const int32_t s = p.inv[rank_combination(p.n, 3, m)];
+    const int pi = pair_index(3, a, b);
+    if (!p.has_score[(int64_t)s * 3 + pi]) continue;
+    const double sc = p.scores[(int64_t)s * 3 + pi];
+    if (isnan(sc)) { poisoned = true; best = sc; }
+    else if (!any || sc < best) best = sc;
+    any = true;
+  }
+  if (any) {
+    p.entries[(int64_t)i * p.n + j] = best;
+    p.entries[(int64_t)j * p.n + i] = best;
+  }
+}
+
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_apply(Params p) {
+  const int64_t s = blockIdx.x;
+  const uint8_t c = p.cls[s];
+  if (c == kFast) return;
+  const int64_t lo = p.bnd.start(s) + (int64_t)blockIdx.y * kChunk;
+  const int64_t hi_s = p.bnd.start(s) + p.bnd.len(s);
+  const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
+  const int32_t src_m = p.source[s];
+  int slot = -1;
+  bfly_corruption_t cd{};
+  if (src_m >= 0) {
+    for (int k = 0; k < p.r; ++k)
+      if (p.assign[s * p.r + k] == src_m) slot = k;
+    cd = p.corr[src_m];
+  }
+  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+    double v;
+    if (slot >= 0) v = corrupt_value(cd, p.ws[e], e, p.host_copies, slot, p.P);
+    else if (p.fallback) v = p.fallback[e];
+    else if (p.n_alive > 0) v = D::raw(p.src[0], e);  // lowest alive upload (butterfly.py:270-271)
+    else v = nan64();
+    if (p.merged) p.merged[e] = v;
+    for (int d = 0; d < p.n_dst; ++d) D::store(p.dst[d], e, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// standalone agreement and mean_reducer
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(kThreads) k_agree_partial(const double* a, const double* b, int64_t len,
+                                                            double* part) {
+  const int64_t lo = (int64_t)blockIdx.x * kChunk;
+  const int64_t hi = lo + kChunk < len ? lo + kChunk : len;
+  PairStat st{0.0, 0.0, 0.0, 0.0};
+  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+    const double x = a[e], y = b[e];
+    st.mx = max_nan(st.mx, fabs(__dsub_rn(x, y)));
+    st.ab = fma(x, y, st.ab);
+    st.aa = fma(x, x, st.aa);
+    st.bb = fma(y, y, st.bb);
+  }
+  st = block_combine(st);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x * 4 + 0] = st.mx;
+    part[blockIdx.x * 4 + 1] = st.ab;
+    part[blockIdx.x * 4 + 2] = st.aa;
+    part[blockIdx.x * 4 + 3] = st.bb;
+  }
+}
+
+__global__ void k_agree_final(const double* part, int64_t nchunks, double tol, double* out) {
+  PairStat st{0.0, 0.0, 0.0, 0.0};
+  for (int64_t ch = threadIdx.x; ch < nchunks; ch += 32) {
+    st.mx = max_nan(st.mx, part[ch * 4]);
+    st.ab = __dadd_rn(st.ab, part[ch * 4 + 1]);
+    st.aa = __dadd_rn(st.aa, part[ch * 4 + 2]);
+    st.bb = __dadd_rn(st.bb, part[ch * 4 + 3]);
+  }
+  st = warp_combine(st);
+  if (threadIdx.x == 0) *out = score_of(st, tol);
+}
+
+// numpy DOUBLE_pairwise_sum over a contiguous column (width-1 stacks).
+__device__ double pairwise_contig(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  } else if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_contig(a, n2), pairwise_contig(a + n2, n - n2));
+}
+
+__global__ void k_corrupt(bfly_corruption_t c, const double* in, int64_t start, int64_t len, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = corrupt_value(c, in[i], start + i, nullptr, 0, 0);
+}
+
+__global__ void k_mean_rows(const double* stack, int32_t rows, int64_t width, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < width;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    if (width == 1) {
+      acc = __dadd_rn(0.0, pairwise_contig(stack, rows));
+    } else {
+      for (int q = 0; q < rows; ++q) acc = __dadd_rn(acc, stack[(int64_t)q * width + e]);
+    }
+    out[e] = __ddiv_rn(acc, (double)rows);
+  }
+}
+
+}  // namespace bfly
+
+using namespace bfly;
+
+template <class D>
+static void launch_reduce(const Params& p, cudaStream_t st) {
+  const int64_t tile = (int64_t)kThreads * kVecPerThread * D::K;
+  const int64_t ntiles = (p.P + tile - 1) / tile;
+  int64_t grid = (int64_t)sm_count() * 8;
+  if (grid > ntiles) grid = ntiles;
+  const size_t smem = sizeof(void*) * (size_t)(p.n_alive + p.n_dst);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_reduce<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_reduce<D><<<(unsigned)grid, kThreads, smem, st>>>(p);
+}
+
+template <class D>
+static void launch_apply(const Params& p, cudaStream_t st) {
+  k_apply<D><<<dim3((unsigned)p.S, (unsigned)p.cps), kThreads, 0, st>>>(p);
+}
+
+extern "C" {
+
+size_t bfly_merge_scratch_bytes(int32_t n_miners, int32_t redundancy, int64_t payload_len) {
+  ScratchLayout L;
+  L.init(n_miners, redundancy, payload_len);
+  return L.total;
+}
+
+int bfly_merge(const bfly_merge_args_t* a, void* stream) {
+  if (!a) return fail(BFLY_E_INVALID_ARG, "null args");
+  if (a->n_miners < 2) return fail(BFLY_E_TOO_FEW_MINERS, "need at least 2 miners");
+  if (a->redundancy < 2 || a->redundancy > kMaxR)
+    return fail(BFLY_E_UNSUPPORTED, "device merge supports redundancy 2 or 3");
+  const int64_t S = binom(a->n_miners, a->redundancy);
+  if (S != a->n_shards) return fail(BFLY_E_SHAPE, "n_shards != C(n_miners, redundancy)");
+  if (a->payload_len < S) return fail(BFLY_E_DEGENERATE, "payload cannot fill every shard");
+  if (a->n_alive < 0 || a->n_alive > a->n_miners) return fail(BFLY_E_INVALID_ARG, "bad n_alive");
+  if (a->dtype != BFLY_F32 && a->dtype != BFLY_BF16 && a->dtype != BFLY_F64WIRE)
+    return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  if (!a->d_assign || !a->d_failed || !a->d_corr || !a->d_status || !a->d_entries || !a->d_flagged)
+    return fail(BFLY_E_INVALID_ARG, "missing required device array");
+  if (a->n_alive > 0 && !a->d_src) return fail(BFLY_E_INVALID_ARG, "missing replicas");
+  if (a->n_dst > 0 && !a->d_dst) return fail(BFLY_E_INVALID_ARG, "missing scatter-back targets");
+  if (!a->d_merged && !a->d_ws) return fail(BFLY_E_INVALID_ARG, "need d_merged or d_ws");
+  ScratchLayout L;
+  L.init(a->n_miners, a->redundancy, a->payload_len);
+  if (!a->d_scratch || a->scratch_bytes < L.total)
+    return fail(BFLY_E_INVALID_ARG, "scratch too small: need " + std::to_string(L.total) + " bytes");
+  if ((int64_t)(a->n_alive + a->n_dst) * 8 > 200 * 1024) return fail(BFLY_E_UNSUPPORTED, "too many replicas");
+  if (L.cps > 65535) return fail(BFLY_E_UNSUPPORTED, "shards longer than 65535 chunks");
+
+  Params p{};
+  p.n = a->n_miners;
+  p.r = a->redundancy;
+  p.n_alive = a->n_alive;
+  p.n_dst = a->n_dst;
+  p.npairs = L.npairs;
+  p.P = a->payload_len;
+  p.S = S;
+  p.cps = L.cps;
+  p.bnd.init(a->payload_len, S);
+  p.assign = a->d_assign;
+  p.src = a->d_src;
+  p.failed = a->d_failed;
+  p.corr = a->d_corr;
+  p.dst = a->d_dst;
+  p.fallback = a->d_fallback;
+  p.merged = a->d_merged;
+  p.ws = a->d_ws ? a->d_ws : a->d_merged;  // keep special-shard means apart when given
+  p.host_copies = a->d_host_copies;
+  p.status = a->d_status;
+  p.entries = a->d_entries;
+  p.flagged = a->d_flagged;
+  unsigned char* sc = (unsigned char*)a->d_scratch;
+  p.cls = sc + L.off_cls;
+  p.source = a->d_source ? a->d_source : (int32_t*)(sc + L.off_source);
+  p.stats = (double*)(sc + L.off_stats);
+  p.scores = (double*)(sc + L.off_scores);
+  p.has_score = sc + L.off_has;
+  p.inv = p.r > 2 ? (int32_t*)(sc + L.off_inv) : nullptr;
+  p.tol = a->tolerance;
+  cudaStream_t st = (cudaStream_t)stream;
+
+  const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
+  const bool do_finish = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH;
+  if (do_reduce) {
+    const int64_t nn = (int64_t)p.n * p.n;
+    k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
+    cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
+    k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
+    if (p.n_alive > 0) {
+      switch (a->dtype) {
+        case BFLY_F32: launch_reduce<DF32>(p, st); break;
+        case BFLY_BF16: launch_reduce<DBF16>(p, st); break;
+        default: launch_reduce<DF64W>(p, st); break;
+      }
+    }
+  }
+  if (do_finish) {
+    k_stats<<<dim3((unsigned)S, (unsigned)p.cps), kThreads, 0, st>>>(p);
+    k_decide<<<(unsigned)S, 32, 0, st>>>(p);
+    if (p.r > 2) {
+      const int64_t nn = (int64_t)p.n * p.n;
+      k_entries3<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p);
+    }
+    switch (a->dtype) {
+      case BFLY_F32: launch_apply<DF32>(p, st); break;
+      case BFLY_BF16: launch_apply<DBF16>(p, st); break;
+      default: launch_apply<DF64W>(p, st); break;
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_merge launch");
+  return BFLY_OK;
+}
+
+int bfly_agreement(const double* d_a, const double* d_b, int64_t len, double tol, double* d_out,
+                   void* d_scratch, size_t scratch_bytes, void* stream) {
+  const int64_t nchunks = len > 0 ? (len + kChunk - 1) / kChunk : 0;
+  if (nchunks > 0 && (!d_scratch || scratch_bytes < sizeof(double) * 4 * (size_t)nchunks))
+    return fail(BFLY_E_INVALID_ARG, "scratch too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nchunks > 0) k_agree_partial<<<(unsigned)nchunks, kThreads, 0, st>>>(d_a, d_b, len, (double*)d_scratch);
+  k_agree_final<<<1, 32, 0, st>>>((const double*)d_scratch, nchunks, tol, d_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_agreement launch");
+  return BFLY_OK;
+}
+
+int bfly_apply_corruption(const bfly_corruption_t* h_desc, const double* d_in, int64_t start_elem, int64_t len,
+                          double* d_out, void* stream) {
+  if (!h_desc || len < 0) return fail(BFLY_E_INVALID_ARG, "bad corruption arguments");
+  if (h_desc->kind == BFLY_CORR_HOST) return fail(BFLY_E_INVALID_ARG, "host copies are not device-computable");
+  if (len == 0) return BFLY_OK;
+  int64_t grid = (len + 255) / 256;
+  if (grid > 65535) grid = 65535;
+  k_corrupt<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(*h_desc, d_in, start_elem, len, d_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_apply_corruption launch");
+  return BFLY_OK;
+}
+
+int bfly_mean_rows(const double* d_stack, int32_t n_rows, int64_t width, double* d_out, void* stream) {
+  if (n_rows <= 0 || width < 0) return fail(BFLY_E_INVALID_ARG, "bad stack shape");
+  if (width == 0) return BFLY_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t grid = (width + 255) / 256;
+  if (grid > 65535) grid = 65535;
+  k_mean_rows<<<(unsigned)grid, 256, 0, st>>>(d_stack, n_rows, width, d_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_mean_rows launch");
+  return BFLY_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+"""The C ABI (include/bfly.h): library loads, exports every declared symbol,
+struct layouts agree with ctypes, and the host-side entry points (no GPU
+needed) match the reference: SHA-256 keys, the host index map, error codes."""
+
+import ctypes
+import hashlib
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from _golden import lex_pairs, plans
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "bfly.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"\b(bfly_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2507_17766_b200 import _lib
+
+    L = _lib.lib()
+    declared = _declared()
+    assert set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.bfly_version().decode().startswith("bfly ")
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(_lib._SO)], capture_output=True, text=True).stdout
+    for name in declared:
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_struct_layout_matches_header(tmp_path):
+    from paper_2507_17766_b200 import _lib
+
+    src = tmp_path / "layout.c"
+    fields = [f for f, _ in _lib.MergeArgs._fields_]
+    body = "\n".join(f'  printf("{f} %zu\\n", offsetof(bfly_merge_args_t, {f}));' for f in fields)
+    src.write_text(f"""#include <stdio.h>
+#include <stddef.h>
+#include "bfly.h"
+int main(void) {{
+  printf("size %zu\\n", sizeof(bfly_merge_args_t));
+  printf("csize %zu\\n", sizeof(bfly_corruption_t));
+{body}
+  return 0;
+}}
+""")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    assert int(out["size"]) == ctypes.sizeof(_lib.MergeArgs)
+    assert int(out["csize"]) == ctypes.sizeof(_lib.Corruption)
+    for f in fields:
+        assert int(out[f]) == getattr(_lib.MergeArgs, f).offset, f
+
+
+@pytest.mark.parametrize("seed", [0, 1, 24, 2**63 - 1, 2**64 + 5, -7, 10**30])
+def test_philox_key_matches_hashlib(seed):
+    from paper_2507_17766_b200 import _lib
+
+    for stream in ("shard-plan", "root/epoch0/plan/sync/L0", "resilience"):
+        d = hashlib.sha256(f"{seed}\x1f{stream}".encode()).digest()
+        want = (int.from_bytes(d[:8], "little"), int.from_bytes(d[8:16], "little"))
+        assert _lib.philox_key(seed, stream) == want
+
+
+def test_host_plan_matches_reference_goldens():
+    from paper_2507_17766_b200 import butterfly as bf
+
+    g = plans()
+    for n in (2, 3, 4, 5, 7, 8, 10, 16, 32, 50, 64):
+        pairs = lex_pairs(n)
+        for seed in [int(s) for s in g["seeds"]]:
+            plan = bf.plan_shards(bf.enumerate_pairs(n), len(pairs) + 3, 4, seed)
+            assert list(plan.assignment) == [pairs[k] for k in g[f"n{n}_s{seed}"]]
+
+
+@pytest.mark.parametrize("n,r", [(6, 3), (32, 3), (200, 2), (400, 2)])
+def test_host_plan_matches_oracle_r3_and_large(n, r):
+    from paper_2507_17766_b200 import butterfly as bf
+
+    S = orc.n_shards(n, r)
+    assign, bounds = bf._host_plan(n, r, S * 3 + 1, 99)
+    want, wb = orc.plan(n, S * 3 + 1, 99, r=r)
+    assert np.array_equal(assign, want) and np.array_equal(bounds, wb)
+
+
+def test_error_mapping():
+    from paper_2507_17766_b200 import butterfly as bf
+    from paper_2507_17766_b200 import errors
+
+    with pytest.raises(errors.TooFewMinersError):
+        bf.enumerate_pairs(1)
+    with pytest.raises(errors.DegenerateShardsError):
+        bf.plan_shards(bf.enumerate_pairs(3), 2, 4, 0)
+    with pytest.raises(errors.TooFewMinersError):
+        bf._host_plan(1, 2, 10, 0)
+    with pytest.raises(errors.DegenerateShardsError):
+        bf._host_plan(4, 2, 5, 0)
+    assert bf.valid_shard_fraction(50, 5) == pytest.approx(1.0 - 20.0 / 2450.0)
+    with pytest.raises(errors.InvalidArgumentError):
+        bf.valid_shard_fraction(10, 11)
+
+
+def test_plan_metadata_and_helpers():
+    from paper_2507_17766_b200 import butterfly as bf
+
+    plan = bf.plan_shards(bf.enumerate_pairs(3), 10, 4, 0)
+    assert [e - s for s, e in plan.bounds] == [4, 3, 3]
+    assert plan.byte_bounds(1) == (16, 28)
+    assert plan.metadata() == b"[[0, 0, 16], [1, 16, 12], [2, 28, 12]]"
+    assert sorted(s for m in range(3) for s in plan.shards_of(m)) == [0, 0, 1, 1, 2, 2]
