@@ -1,17 +1,22 @@
 #!/usr/bin/env python
-"""Benchmark of the butterfly merge (BASELINE.json metric: params merged/sec).
+"""Benchmark of the butterfly merge (BASELINE.json metric: params merged/sec (GB/s)).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
 
-N=1 workload: BASELINE config 2 — one 1B-parameter pipeline stage, 16 miners,
-fp32 wire values, redundancy 2, on one B200 (the largest single-GPU config; the
-reference's own CPU-runnable config 1 is a parity-test case).  A "step" is one
-merge round: reduce every shard over the alive replicas (fp64 sequential
-accumulation), compare redundant copies, adopt, scatter back in place into all
-16 replicas.  Inputs are 64 GB of replicas, far larger than the 126 MB L2, so
-no flush is needed between steps.
+Workload (weak scaling, 16 miners per GPU): each GPU holds 16 miner replicas of
+one 1B-parameter pipeline stage (fp32 wire values), redundancy 2.  N=1 is
+BASELINE config 2 (16 miners on one B200); N=4 is config 3's 64 miners of a 1B
+stage; N GPUs merge 16*N miners.  A "step" is one merge round: every shard is
+reduced over the alive replicas (fp64 sequential accumulation in miner order,
+bit-identical to the reference), redundant copies are compared, and the
+adopted slices are scattered back in place into every replica.  Inputs are
+64 GB per GPU, far larger than the 126 MB L2, so no flush is needed.
 
-One JSON line on rank 0 (see DESIGN.md §Measurement for every field).
+``value`` is the whole-job merge bandwidth in GB/s: sum over GPUs of the
+algorithmic bytes (every alive replica read once + every replica written once,
+4 B per parameter) divided by the round time (max over ranks).  The same
+round's params merged/s (P / t) is reported beside it.
 """
 
 from __future__ import annotations
@@ -30,23 +35,22 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "params merged/sec (GB/s) at 1/2/4/8 B200 vs HBM/NVLink roofline and CPU ref"
-UNIT = "params/s"
+UNIT = "GB/s"
 
 CONFIGS = {
-    # name: (miners, params, dtype, redundancy, deceptive)
+    # name: (miners per GPU, params, dtype, redundancy, deceptive miners)
     "c1": (8, 10_000_000, "fp32", 2, 0),
     "c2": (16, 1_000_000_000, "fp32", 2, 0),
-    "c3": (64, 1_000_000_000, "fp32", 2, 0),
     "c4": (32, 1_750_000_000, "bf16", 3, 0),
-    "c5": (64, 1_000_000_000, "fp32", 2, 6),
+    "c5": (16, 1_000_000_000, "fp32", 2, 6),
 }
 WORKLOAD = {
-    "c1": "reference default: butterfly merge 8 miners x 10M fp32, r=2",
-    "c2": "1B-param stage, 16 miners fp32, r=2, 1 B200 (BASELINE config 2)",
-    "c3": "1B-param stage, 64 miners across the GPUs, r=2 (BASELINE config 3)",
-    "c4": "14B model / 8 stages: 1.75B-param stage, 32 miners bf16 (fp32 acc), r=3 (BASELINE config 4)",
-    "c5": "1B-param stage, 64 miners, 6 deceptive (noise), r=2 (BASELINE config 5)",
+    "c1": "reference default: 8 miners x 10M fp32, r=2 (BASELINE config 1)",
+    "c2": "1B-param stage, 16 miners per B200 fp32, r=2 (config 2 at N=1, config 3's 64 miners at N=4)",
+    "c4": "14B model / 8 stages: one 1.75B-param stage per GPU, 32 miners bf16 (fp32 acc), r=3 (BASELINE config 4)",
+    "c5": "1B-param stage, 16 miners per GPU, 6 deceptive (noise), r=2 (BASELINE config 5 at N=4)",
 }
+BYTES = {"fp32": 4, "bf16": 2}
 
 
 def _peaks():
@@ -61,26 +65,23 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t = threading.Thread(target=lambda: self.lines.extend(ln.strip() for ln in self.proc.stdout),
+                                       daemon=True)
             self._t.start()
+            time.sleep(0.2)
         except FileNotFoundError:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -93,7 +94,6 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) != 6:
@@ -103,9 +103,7 @@ class ClockSampler:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+            reasons.update(nm for nm, v in zip(self.NAMES, parts[2:]) if v.lower() == "active")
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
@@ -124,29 +122,37 @@ def _oracle():
     return orc
 
 
-def cpu_sample(cfg, p_cpu: int, reps: int = 2):
-    """Time the C oracle (restatement of run_all_reduce) with all host threads."""
+def cpu_sample(n, p_cpu, dtype, r, fp64_payloads: bool, reps: int = 1):
+    """Time the C oracle (restatement of run_all_reduce) with all host threads.
+    Returns (seconds per merge, threads)."""
     import numpy as np
 
     orc = _oracle()
-    n, _, dtype, r, _ = cfg
     threads = orc.threads_available()
     rng = np.random.default_rng(0)
     if dtype == "bf16":
         replicas = [(rng.uniform(-1, 1, p_cpu).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
                     for _ in range(n)]
         odt = orc.BF16
+    elif fp64_payloads:
+        replicas = [rng.uniform(-1, 1, p_cpu) for _ in range(n)]
+        odt = orc.F64WIRE
     else:
         replicas = [rng.uniform(-1, 1, p_cpu).astype(np.float32) for _ in range(n)]
         odt = orc.F32
     assign, bounds = orc.plan(n, p_cpu, 0, r=r)
     orc.merge(replicas, assign, bounds, dtype=odt, threads=threads)  # warm
-    best = float("inf")
+    times = []
     for _ in range(reps):
         t = time.perf_counter()
         orc.merge(replicas, assign, bounds, dtype=odt, threads=threads)
-        best = min(best, time.perf_counter() - t)
-    return p_cpu / best, threads, best
+        times.append(time.perf_counter() - t)
+    return times, threads
+
+
+def merge_bytes(n_miners, params, esize):
+    """Algorithmic bytes of one round: each replica read once and written once."""
+    return 2 * n_miners * params * esize
 
 
 # ---------------------------------------------------------------------------
@@ -173,7 +179,29 @@ def deceptive_set(n, k, seed=0):
     return sorted(int(x) for x in np.random.default_rng(seed).choice(n, k, replace=False)) if k else []
 
 
-def run_device(cfg, args, dev):
+def timed_rounds(step, args, dev):
+    """W untimed rounds, then K rounds between CUDA events on the current stream."""
+    import torch
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index or 0) as clk:
+        if torch.distributed.is_initialized():
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        kernel_ms = [step(timed=True) for _ in range(args.steps)]
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if torch.distributed.is_initialized():
+            torch.distributed.barrier()
+    return t0.elapsed_time(t1), kernel_ms, clk.summary()
+
+
+def run_single(cfg, args, dev):
     import torch
 
     from paper_2507_17766_b200 import _lib as L
@@ -184,52 +212,66 @@ def run_device(cfg, args, dev):
     plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
     corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in deceptive_set(n, k_bad)}
     job = ButterflyMerge(reps, plan, corruptions=corr, scatter_back=True, want_merged=False)
-    stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
+    events = []
+
+    def step(timed=False):
+        if not timed:
+            job.run()
+            return None
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         job.run(L.PHASE_REDUCE)
+        b.record()
         job.run(L.PHASE_FINISH)
+        events.append((a, b))
+        return None
+
+    total_ms, _, clocks = timed_rounds(step, args, dev)
     torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps)]
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index or 0) as clk:
-        torch.cuda.synchronize()
-        t0.record(stream)
-        for k in range(args.steps):
-            ev[3 * k].record(stream)
-            job.run(L.PHASE_REDUCE)
-            ev[3 * k + 1].record(stream)
-            job.run(L.PHASE_FINISH)
-            ev[3 * k + 2].record(stream)
-        t1.record(stream)
-        torch.cuda.synchronize()
-    total_ms = t0.elapsed_time(t1)
-    reduce_ms = [ev[3 * k].elapsed_time(ev[3 * k + 1]) for k in range(args.steps)]
-    finish_ms = [ev[3 * k + 1].elapsed_time(ev[3 * k + 2]) for k in range(args.steps)]
+    reduce_ms = statistics.mean(a.elapsed_time(b) for a, b in events)
     status = job.status.cpu()
-    info = {
-        "total_ms": total_ms,
-        "reduce_ms": statistics.mean(reduce_ms),
-        "finish_ms": statistics.mean(finish_ms),
-        "launches": job.launches_per_run() * args.steps,
-        "clocks": clk.summary(),
-        "n_alive": len(job.alive),
-        "disagreement_shards": int((status == L.DISAGREEMENT).sum()),
-        "flagged": int(job.flagged.sum().item()),
-    }
+    info = dict(total_ms=total_ms, reduce_ms=reduce_ms, launches=job.launches_per_run() * args.steps,
+                clocks=clocks, n_alive=len(job.alive), disagreement=int((status == L.DISAGREEMENT).sum()),
+                flagged=int(job.flagged.sum().item()))
+    resident = run_e2e_resident(job, args)
     del job, reps
     torch.cuda.empty_cache()
-    return info
+    return info, resident
 
 
-def run_e2e(cfg, args, dev, p_e2e):
-    """Same metric through the drop-in API (butterfly.run_all_reduce) from pinned host fp64 payloads."""
-    import numpy as np
+def run_e2e_resident(job, args):
+    """Device-resident API end to end: per round the host sends the round's control
+    inputs (failure mask, corruption table; pinned -> device) and reads back the
+    round's result (status, flags, agreement matrix) — weights stay in HBM."""
+    import torch
+
+    failed_h = job._failed.cpu().pin_memory()
+    corr_h = job._corr.cpu().pin_memory()
+    outs = [torch.empty_like(t, device="cpu").pin_memory() for t in (job.status, job.flagged, job.entries)]
+    steps = max(1, min(args.steps, 10))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(steps):
+        job._failed.copy_(failed_h, non_blocking=True)
+        job._corr.copy_(corr_h, non_blocking=True)
+        job.run()
+        for o, d in zip(outs, (job.status, job.flagged, job.entries)):
+            o.copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+    dt = (time.perf_counter() - t) / steps
+    h2d = failed_h.numel() + corr_h.numel()
+    d2h = sum(o.numel() * o.element_size() for o in outs)
+    return dt, h2d, d2h
+
+
+def run_e2e(n, r, args, dev, p_e2e):
+    """The drop-in API (butterfly.run_all_reduce) on fp64 payloads in pinned host memory:
+    H2D of every payload and D2H of the merged vector inside every step."""
     import torch
 
     from paper_2507_17766_b200 import butterfly as bf
     from paper_2507_17766_b200.simkernel import BlobStore
 
-    n, _, _, r, _ = cfg
     if r != 2:
         return None
     payloads = {}
@@ -242,31 +284,123 @@ def run_e2e(cfg, args, dev, p_e2e):
     plan = bf.plan_shards(bf.enumerate_pairs(n), p_e2e, bf.BYTES_PER_WEIGHT, 0)
     for _ in range(max(1, min(args.warmup, 2))):
         res = bf.run_all_reduce(BlobStore(), payloads, plan)
+    del res
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 5))
     t = time.perf_counter()
     for _ in range(steps):
         res = bf.run_all_reduce(BlobStore(), payloads, plan)
+        del res
     dt = (time.perf_counter() - t) / steps
-    assert res.merged.shape == (p_e2e,)
     S = plan.n_shards
     return {
-        "value": p_e2e / dt,
+        "value": merge_bytes(n, p_e2e, 4) / dt / 1e9,
         "unit": UNIT,
-        "h2d_bytes_per_step": n * p_e2e * 8 + S * 2 * 4 + n,
+        "h2d_bytes_per_step": n * p_e2e * 8 + S * 2 * 4 + n + n * 32,
         "d2h_bytes_per_step": p_e2e * 8 + S + n * n * 8 + n + S * 4,
         "params": p_e2e,
+        "params_merged_per_s": p_e2e / dt,
         "ms_per_step": dt * 1e3,
-        "path": "paper_2507_17766_b200.butterfly.run_all_reduce(BlobStore(), fp64 pinned host payloads, plan)",
+        "path": "paper_2507_17766_b200.butterfly.run_all_reduce(BlobStore(), {miner: fp64 payload in pinned "
+                "host memory}, plan) -> MergeResult (merged fp64 copied back)",
+        "bound": "PCIe: %.1f GB of fp64 payloads H2D per step" % (n * p_e2e * 8 / 1e9),
     }
 
 
-def traffic_from_profiles(config_name):
-    f = ROOT / "profiles" / "ncu_traffic.json"
-    try:
-        return json.loads(f.read_text()).get(config_name)
-    except Exception:
+def run_multi(cfg, args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_17766_b200.device import Corruption, DevicePlan
+    from paper_2507_17766_b200.multigpu import ShardedButterflyMerge
+
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    n_local, P, dtype, r, k_bad = cfg
+    n = n_local * world
+    reps = make_replicas(n_local, P, dtype, dev, seed=rank * n_local)
+    plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
+    bad = deceptive_set(n, k_bad)
+    corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in bad}
+    job = ShardedButterflyMerge(reps, plan, corruptions=corr, chunk=args.chunk)
+
+    def step(timed=False):
+        job.run()
         return None
+
+    total_ms, _, clocks = timed_rounds(step, args, dev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    t_step = total_ms / args.steps / 1e3
+    esize = BYTES[dtype]
+    nb = job.bytes_per_round()
+    nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
+    dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
+    launches = job.launches_per_run() * args.steps
+    if rank == 0:
+        peaks = _peaks()
+        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        alg = merge_bytes(n, P, esize)
+        value = alg / t_step / 1e9
+        per_gpu_hbm = merge_bytes(n_local, P, esize)
+        nvl_peak = 770.0
+        t_roof = max(per_gpu_hbm / (hbm_peak * 1e9), float(nvl.item()) / (nvl_peak * 1e9))
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if dtype == "fp32" else "f32",
+            "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
+            "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "miners_per_gpu": n_local,
+                       "params": P, "replica_dtype": dtype, "redundancy": r, "deceptive": len(bad),
+                       "parallelism": f"miners in contiguous blocks over {world} GPUs; fp64 running-sum chain "
+                                      f"(NCCL send/recv, {args.chunk}-element chunks) + broadcast of the result",
+                       "l2": "inputs %.0f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
+            "params_merged_per_s": P / t_step,
+            "roofline": {"bound": "hbm" if per_gpu_hbm / hbm_peak > float(nvl.item()) / nvl_peak else "nvlink",
+                         "achieved": t_roof / t_step, "peak": 1.0, "unit": "fraction of t_roof",
+                         "frac": t_roof / t_step, "traffic": None,
+                         "t_roof_ms": t_roof * 1e3, "hbm_bytes_per_gpu": per_gpu_hbm,
+                         "nvlink_bytes_in_per_gpu": float(nvl.item()),
+                         "peaks": {"hbm_GBps": hbm_peak, "nvlink_GBps_per_direction": nvl_peak}},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def run_reference(cfg, args, rank, world):
+    """--impl reference: the CPU restatement of the reference's run_all_reduce
+    (oracle/bfly_oracle.c, all host threads) on fp64 payloads — the reference API's
+    input — for a bounded sample of the same workload, one merge per step."""
+    if rank != 0:
+        return
+    n_local, P, dtype, r, _ = cfg
+    n = n_local * world
+    p_cpu = args.cpu_params
+    for _ in range(args.warmup):
+        cpu_sample(n, p_cpu, dtype, r, dtype == "fp32")
+    times, threads = cpu_sample(n, p_cpu, dtype, r, dtype == "fp32", reps=args.steps)
+    t_step = statistics.mean(times)
+    value = merge_bytes(n, p_cpu, BYTES[dtype]) / t_step / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if dtype == "fp32" else "f32",
+        "data": "synthetic uniform(-1,1) payloads",
+        "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "params": p_cpu,
+                   "sampled_from_params": P, "redundancy": r},
+        "params_merged_per_s": p_cpu / t_step,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"oracle/bfly_oracle.c restatement of run_all_reduce (OpenMP, {threads} threads), "
+                                   f"{n} miners x {p_cpu} params as fp64 payloads -> fp32 wire -> fp64 mean, "
+                                   f"one merge per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
 
 
 def main():
@@ -276,6 +410,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--params", type=int, default=None, help="override the stage size")
+    ap.add_argument("--chunk", type=int, default=1 << 24)
     ap.add_argument("--e2e-params", type=int, default=1 << 27)
     ap.add_argument("--cpu-params", type=int, default=1 << 25)
     ap.add_argument("--no-e2e", action="store_true")
@@ -283,58 +419,40 @@ def main():
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
-        from paper_2507_17766_b200 import multigpu
-
-        return multigpu.bench_main(args, rank, world)
     name = args.config or "c2"
-    cfg = CONFIGS[name]
-    n, P, dtype, r, k_bad = cfg
-
+    cfg = list(CONFIGS[name])
+    if args.params:
+        cfg[1] = args.params
+    cfg = tuple(cfg)
     if args.impl == "reference":
-        per_step = []
-        threads = None
-        for _ in range(args.warmup):
-            cpu_sample(cfg, args.cpu_params, reps=1)
-        for _ in range(args.steps):
-            v, threads, secs = cpu_sample(cfg, args.cpu_params, reps=1)
-            per_step.append(secs)
-        value = args.cpu_params / statistics.mean(per_step)
-        line = {
-            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(per_step) * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64" if dtype == "fp32" else "f32",
-            "data": "synthetic uniform(-1,1) replicas",
-            "config": {"workload": WORKLOAD[name], "miners": n, "params": args.cpu_params, "redundancy": r,
-                       "sampled_from_params": P},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"oracle/bfly_oracle.c run_all_reduce restatement, {n} miners x "
-                                       f"{args.cpu_params} params {dtype}, one merge per step"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line))
-        return
+        return run_reference(cfg, args, rank, world)
+    if world > 1:
+        return run_multi(cfg, args, rank, world)
 
     import torch
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    info = run_device(cfg, args, dev)
+    n, P, dtype, r, k_bad = cfg
+    info, resident = run_single(cfg, args, dev)
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     t_step = info["total_ms"] / args.steps / 1e3
-    value = P / t_step
-    esize = 2 if dtype == "bf16" else 4
-    alg_bytes = (info["n_alive"] + n) * P * esize  # read every alive replica once, write every replica once
-    achieved = alg_bytes / (info["reduce_ms"] / 1e3) / 1e9
-    e2e = None if args.no_e2e else run_e2e(cfg, args, dev, args.e2e_params)
+    esize = BYTES[dtype]
+    alg = (info["n_alive"] + n) * P * esize  # read every alive replica once, write every replica once
+    value = alg / t_step / 1e9
+    achieved = alg / (info["reduce_ms"] / 1e3) / 1e9
+    e2e = None if args.no_e2e else run_e2e(n, r, args, dev, args.e2e_params)
     cpu = None
     if not args.no_cpu:
-        v, threads, secs = cpu_sample(cfg, args.cpu_params)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"oracle/bfly_oracle.c (C restatement of run_all_reduce, OpenMP), {n} miners x "
-                         f"{args.cpu_params} params {dtype}, best of 2 ({secs:.3f} s)"}
+        times, threads = cpu_sample(n, args.cpu_params, dtype, r, False, reps=2)
+        secs = min(times)
+        cpu = {"value": merge_bytes(n, args.cpu_params, esize) / secs / 1e9, "unit": UNIT, "cores": threads,
+               "kind": "port", "params_merged_per_s": args.cpu_params / secs,
+               "sample": f"oracle/bfly_oracle.c (C restatement of run_all_reduce, OpenMP {threads} threads) on "
+                         f"host-resident {dtype} replicas, {n} miners x {args.cpu_params} params, best of 2 "
+                         f"({secs * 1e3:.1f} ms per merge)"}
+    rt, h2d, d2h = resident
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -342,21 +460,32 @@ def main():
         "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
         "config": {"workload": WORKLOAD[name], "miners": n, "params": P, "replica_dtype": dtype,
                    "redundancy": r, "deceptive": k_bad, "parallelism": "single GPU",
-                   "l2": "inputs (%.0f GB) >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
-        "GBps": alg_bytes / t_step / 1e9,
+                   "l2": "inputs %.0f GB >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
+        "params_merged_per_s": P / t_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_from_profiles(name),
-                     "kernel": "k_reduce (+k_fill_nan, k_classify in the same event window)",
-                     "algorithmic_bytes": alg_bytes, "kernel_ms": info["reduce_ms"],
+                     "kernel": "k_reduce (event window also holds k_fill_nan + k_classify, < 10 us)",
+                     "algorithmic_bytes_per_launch": alg, "kernel_ms": info["reduce_ms"],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-        "finish_ms": info["finish_ms"],
         "e2e": e2e,
+        "e2e_resident": {"value": alg / rt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                         "ms_per_step": rt * 1e3,
+                         "path": "device.ButterflyMerge.run() on HBM-resident replicas; per step H2D of the "
+                                 "failure mask + corruption table, D2H of status/flags/agreement matrix"},
         "cpu_baseline": cpu,
         "gpu_launches": info["launches"],
         "clocks": info["clocks"],
-        "disagreement_shards": info["disagreement_shards"],
+        "disagreement_shards": info["disagreement"],
     }
     print(json.dumps(line))
+
+
+def traffic_from_profiles(config_name):
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(f.read_text()).get(config_name)
+    except Exception:
+        return None
 
 
 if __name__ == "__main__":

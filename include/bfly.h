@@ -95,6 +95,15 @@ typedef struct bfly_merge_args {
   double tolerance;               /* agreement_tolerance (butterfly.py:171)         */
   int32_t phase;                  /* BFLY_PHASE_*                                   */
   int32_t pad1;
+  /* multi-GPU (one process per GPU, miners in contiguous blocks per GPU): the
+   * last GPU of the chain finishes the reduction from the running sums */
+  const double* d_acc_in;         /* [elem_end-elem_begin] fp64 running sums from the previous GPUs, or NULL */
+  int32_t n_div;                  /* divisor of the mean = alive miners on all GPUs; 0 = n_alive */
+  int32_t pad2;
+  int64_t elem_begin;             /* REDUCE this element range only; 0,0 = all.  The per-round */
+  int64_t elem_end;               /* setup (NaN fill, classify) runs with the range starting at 0 */
+  const void* d_fallback_src;     /* replica supplying fallback values (lowest alive miner);
+                                     NULL = d_src[0]                                   */
 } bfly_merge_args_t;
 
 /* ---- library ----------------------------------------------------------- */
@@ -125,6 +134,25 @@ size_t bfly_merge_scratch_bytes(int32_t n_miners, int32_t redundancy, int64_t pa
 
 /* One merge round: run_all_reduce  butterfly.py:161-295, device-resident. */
 int bfly_merge(const bfly_merge_args_t* args, void* stream);
+
+/* One link of the cross-GPU reduction chain (multi-GPU merge): for elements
+ * e in [begin, end), d_acc_out[e-begin] = (d_acc_in ? d_acc_in[e-begin] : +0.0)
+ * + x_0[e] + x_1[e] + ... over this GPU's alive replicas in ascending miner
+ * order — the reference's summation order continued across GPUs. */
+int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
+                    double* d_acc_out, int64_t begin, int64_t end, void* stream);
+
+/* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
+int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);
+
+/* Element ranges between a full-length vector and a packed buffer:
+ * scatter == 0: d_packed[off_r + i] = d_full[lo_r + i];
+ * scatter == 1: d_dst[k][lo_r + i] = d_packed[off_r + i] for every k.
+ * d_ranges = n_ranges x {lo, hi, off} (int64, device).  Multi-GPU redistribution
+ * of the shards decided after the chain (corrupted / lost shards). */
+int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int32_t n_dst,
+                     const int64_t* d_ranges, int32_t n_ranges, int32_t elem_size, int32_t scatter,
+                     void* stream);
 
 /* Pairwise agreement of two device vectors into *d_out (fp64).
  * agreement  butterfly.py:117-133. */

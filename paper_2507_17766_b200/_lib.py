@@ -34,6 +34,9 @@ EXPORTS = (
     "bfly_agreement",
     "bfly_apply_corruption",
     "bfly_mean_rows",
+    "bfly_chain_step",
+    "bfly_fanout",
+    "bfly_copy_ranges",
 )
 
 
@@ -75,6 +78,12 @@ class MergeArgs(ctypes.Structure):
         ("tolerance", ctypes.c_double),
         ("phase", ctypes.c_int32),
         ("pad1", ctypes.c_int32),
+        ("d_acc_in", ctypes.c_void_p),
+        ("n_div", ctypes.c_int32),
+        ("pad2", ctypes.c_int32),
+        ("elem_begin", ctypes.c_int64),
+        ("elem_end", ctypes.c_int64),
+        ("d_fallback_src", ctypes.c_void_p),
     ]
 
 
@@ -104,6 +113,9 @@ def lib() -> ctypes.CDLL:
     L.bfly_agreement.argtypes = [vp, vp, i64, dbl, vp, vp, sz, vp]
     L.bfly_apply_corruption.argtypes = [ctypes.POINTER(Corruption), vp, i64, i64, vp, vp]
     L.bfly_mean_rows.argtypes = [vp, i32, i64, vp, vp]
+    L.bfly_chain_step.argtypes = [vp, i32, i32, vp, vp, i64, i64, vp]
+    L.bfly_fanout.argtypes = [vp, vp, i32, i64, vp]
+    L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)
     _lib = L

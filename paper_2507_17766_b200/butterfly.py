@@ -296,8 +296,10 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     else:
         job.run(L.PHASE_ALL)
 
-    merged = job.merged.cpu().numpy()
+    merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
+    merged_host.copy_(job.merged, non_blocking=True)
     status_codes = job.status.cpu().numpy()
+    merged = merged_host.numpy()  # the array keeps the pinned tensor alive
     entries = job.entries.cpu().numpy()
     flagged_idx = np.flatnonzero(job.flagged.cpu().numpy())
     sources = job.source.cpu().numpy()

@@ -168,6 +168,10 @@ struct Params {
   uint8_t* has_score;
   int32_t* inv;
   double tol;
+  const double* acc_in;  // chain accumulator for [ebeg, eend) (multi-GPU), or null
+  int32_t n_div;         // divisor of the mean: all alive miners across GPUs
+  int64_t ebeg, eend;    // element range of this REDUCE call
+  const void* fb_src;    // replica supplying fallback values (the lowest alive miner's)
 };
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000LL); }
@@ -236,7 +240,7 @@ __global__ void k_classify(Params p) {
   }
   if (p.inv) p.inv[rank_combination(p.n, p.r, mem)] = (int32_t)s;
   uint8_t c;
-  if (ns == 0 || p.n_alive == 0) {
+  if (ns == 0 || p.n_div == 0) {
     c = kLost;
     p.status[s] = BFLY_LOST;
     p.source[s] = -1;
@@ -271,34 +275,83 @@ __global__ void k_classify(Params p) {
 // k_reduce — the streaming mean + scatter-back
 // ---------------------------------------------------------------------------
 
-constexpr int kVecPerThread = 1;
+// Sequential accumulation of one 32-byte vector per thread over the replica
+// table, U replicas' loads in flight before their adds (the add order stays
+// ascending, which is what parity needs).
+template <class D>
+__device__ __forceinline__ void accumulate_vec(typename D::Acc (&acc)[D::K], const void* const* s_src, int n,
+                                               int64_t vidx) {
+  constexpr int K = D::K;
+  constexpr int U = 4;
+  int q = 0;
+  for (; q + U <= n; q += U) {
+    V8 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) raw[u] = ld_stream(reinterpret_cast<const V8*>(s_src[q + u]) + vidx);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      typename D::Acc x[K];
+      D::unpack(raw[u], x);
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = D::add(acc[k], x[k]);
+    }
+  }
+  for (; q < n; ++q) {
+    typename D::Acc x[K];
+    D::unpack(ld_stream(reinterpret_cast<const V8*>(s_src[q]) + vidx), x);
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = D::add(acc[k], x[k]);
+  }
+}
+
+// acc[k] <- incoming chain accumulator (fp64 storage; fp32 value for bf16)
+template <class D>
+__device__ __forceinline__ void load_acc_in(typename D::Acc (&acc)[D::K], const double* a) {
+#pragma unroll
+  for (int k = 0; k < D::K; k += 4) {
+    double x0, x1, x2, x3;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3)
+                 : "l"(a + k));
+    acc[k] = (typename D::Acc)x0;
+    acc[k + 1] = (typename D::Acc)x1;
+    acc[k + 2] = (typename D::Acc)x2;
+    acc[k + 3] = (typename D::Acc)x3;
+  }
+}
+
+// Copies the pointer tables to shared memory; returns whether every pointer the
+// vector path touches is 32-byte aligned.
+__device__ __forceinline__ bool stage_pointers(const void** s_src, void** s_dst, const void* const* src, int n_src,
+                                               void* const* dst, int n_dst, uintptr_t extra) {
+  uintptr_t mis = threadIdx.x == 0 ? extra : 0;
+  for (int q = threadIdx.x; q < n_src; q += blockDim.x) {
+    s_src[q] = src[q];
+    mis |= (uintptr_t)src[q];
+  }
+  for (int q = threadIdx.x; q < n_dst; q += blockDim.x) {
+    s_dst[q] = dst[q];
+    mis |= (uintptr_t)dst[q];
+  }
+  return __syncthreads_or((int)(mis & 31)) == 0;
+}
 
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_alive] src, then [n_dst] dst
   const void** s_src = s_ptr;
   void** s_dst = const_cast<void**>(s_ptr + p.n_alive);
-  uintptr_t mis = 0;
-  for (int q = threadIdx.x; q < p.n_alive; q += blockDim.x) {
-    s_src[q] = p.src[q];
-    mis |= (uintptr_t)p.src[q];
-  }
-  for (int q = threadIdx.x; q < p.n_dst; q += blockDim.x) {
-    s_dst[q] = p.dst[q];
-    mis |= (uintptr_t)p.dst[q];
-  }
-  if (threadIdx.x == 0) mis |= (uintptr_t)p.merged;
-  const bool aligned = __syncthreads_or((int)(mis & 31)) == 0;
-
+  const bool aligned = stage_pointers(s_src, s_dst, p.src, p.n_alive, p.dst, p.n_dst,
+                                      (uintptr_t)p.merged | (uintptr_t)p.acc_in);
   constexpr int K = D::K;
-  constexpr int TILE = kThreads * kVecPerThread * K;
-  const int64_t ntiles = (p.P + TILE - 1) / TILE;
-  const bool may_width1 = p.bnd.base == 1;
+  constexpr int TILE = kThreads * K;
   using Acc = typename D::Acc;
+  const bool may_width1 = p.bnd.base == 1;
+  const int64_t tile_lo = p.ebeg / TILE, tile_hi = (p.eend + TILE - 1) / TILE;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t t0 = tile * TILE;
-    const int64_t t1 = t0 + TILE < p.P ? t0 + TILE : p.P;
+  for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
+    const int64_t t0 = max(tile * TILE, p.ebeg);
+    const int64_t t1 = min(tile * TILE + TILE, p.eend);
     // uniform per tile: are all covered shards fast (and not width-1)?
     const int64_t s_lo = p.bnd.shard_of(t0), s_hi = p.bnd.shard_of(t1 - 1);
     bool fast = aligned && (t1 - t0 == TILE);
@@ -306,61 +359,39 @@ __global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
       fast = p.cls[s] == kFast && !(may_width1 && s >= p.bnd.rem);
 
     if (fast) {
-      Acc acc[kVecPerThread][K];
+      Acc acc[K];
+      const int64_t vidx = t0 / K + threadIdx.x;  // 32-byte vector index
+      const int64_t e0 = vidx * K;
+      if (p.acc_in) {
+        load_acc_in<D>(acc, p.acc_in + (e0 - p.ebeg));
+      } else {
 #pragma unroll
-      for (int v = 0; v < kVecPerThread; ++v)
-#pragma unroll
-        for (int k = 0; k < K; ++k) acc[v][k] = D::zero();
-      const int64_t vbase = t0 / K + threadIdx.x;  // 32-byte vector index
-      int q = 0;
-      constexpr int U = 4;  // replicas in flight per thread
-      for (; q + U <= p.n_alive; q += U) {
-        V8 raw[U][kVecPerThread];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int v = 0; v < kVecPerThread; ++v)
-            raw[u][v] = ld_stream(reinterpret_cast<const V8*>(s_src[q + u]) + vbase + v * kThreads);
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int v = 0; v < kVecPerThread; ++v) {
-            Acc x[K];
-            D::unpack(raw[u][v], x);
-#pragma unroll
-            for (int k = 0; k < K; ++k) acc[v][k] = D::add(acc[v][k], x[k]);
-          }
+        for (int k = 0; k < K; ++k) acc[k] = D::zero();
       }
-      for (; q < p.n_alive; ++q) {
+      accumulate_vec<D>(acc, s_src, p.n_alive, vidx);
 #pragma unroll
-        for (int v = 0; v < kVecPerThread; ++v) {
-          Acc x[K];
-          D::unpack(ld_stream(reinterpret_cast<const V8*>(s_src[q]) + vbase + v * kThreads), x);
+      for (int k = 0; k < K; ++k) acc[k] = D::mean(acc[k], p.n_div);
+      if (p.merged) {
 #pragma unroll
-          for (int k = 0; k < K; ++k) acc[v][k] = D::add(acc[v][k], x[k]);
-        }
+        for (int k = 0; k < K; k += 4)
+          st_f64x4(p.merged + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
+                   D::widen(acc[k + 3]));
       }
-#pragma unroll
-      for (int v = 0; v < kVecPerThread; ++v) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) acc[v][k] = D::mean(acc[v][k], p.n_alive);
-        const int64_t e0 = (vbase + v * kThreads) * K;
-        if (p.merged) {
-#pragma unroll
-          for (int k = 0; k < K; k += 4)
-            st_f64x4(p.merged + e0 + k, D::widen(acc[v][k]), D::widen(acc[v][k + 1]), D::widen(acc[v][k + 2]),
-                     D::widen(acc[v][k + 3]));
-        }
-        const V8 out = D::pack(acc[v]);
-        for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vbase + v * kThreads, out);
-      }
+      const V8 out = D::pack(acc);
+      for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
     } else {
       for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
         const int64_t s = p.bnd.shard_of(e);
         const uint8_t c = p.cls[s];
         if (c == kLost) continue;
-        const bool w1 = p.bnd.len(s) == 1;
-        const Acc m = mean_at<D>(s_src, p.n_alive, e, w1);
+        Acc m;
+        if (p.acc_in) {  // chain continuation (width-1 shards are rejected on the host)
+          Acc acc = (Acc)p.acc_in[e - p.ebeg];
+          for (int q = 0; q < p.n_alive; ++q) acc = D::add(acc, D::load(s_src[q], e));
+          m = D::mean(acc, p.n_div);
+        } else {
+          m = mean_at<D>(s_src, p.n_alive, e, p.bnd.len(s) == 1);
+        }
         if (c == kFast) {
           if (p.merged) p.merged[e] = D::widen(m);
           for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(m));
@@ -369,6 +400,80 @@ __global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
         }
       }
     }
+  }
+}
+
+// One link of the cross-GPU chain: acc_out = acc_in (or +0.0) + x_0 + x_1 + ...
+// over this GPU's alive replicas, for elements [begin, end); the acc buffers are
+// chunk-local.  Carrying the running fp64 sum from GPU to GPU keeps the
+// reference's ascending-miner order, so the multi-GPU mean is bit-exact.
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_chain(const void* const* src, int n_src, const double* acc_in,
+                                                    double* acc_out, int64_t begin, int64_t end) {
+  extern __shared__ __align__(16) const void* s_ptr[];
+  const bool aligned = stage_pointers(s_ptr, nullptr, src, n_src, nullptr, 0,
+                                      (uintptr_t)acc_in | (uintptr_t)acc_out);
+  constexpr int K = D::K;
+  constexpr int TILE = kThreads * K;
+  using Acc = typename D::Acc;
+  const int64_t tile_lo = begin / TILE, tile_hi = (end + TILE - 1) / TILE;
+  for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
+    const int64_t t0 = max(tile * TILE, begin);
+    const int64_t t1 = min(tile * TILE + TILE, end);
+    if (aligned && t1 - t0 == TILE) {
+      Acc acc[K];
+      const int64_t vidx = t0 / K + threadIdx.x;
+      const int64_t e0 = vidx * K;
+      if (acc_in) {
+        load_acc_in<D>(acc, acc_in + (e0 - begin));
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = D::zero();
+      }
+      accumulate_vec<D>(acc, s_ptr, n_src, vidx);
+#pragma unroll
+      for (int k = 0; k < K; k += 4)
+        st_f64x4(acc_out + (e0 - begin) + k, (double)acc[k], (double)acc[k + 1], (double)acc[k + 2],
+                 (double)acc[k + 3]);
+    } else {
+      for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
+        Acc acc = acc_in ? (Acc)acc_in[e - begin] : D::zero();
+        for (int q = 0; q < n_src; ++q) acc = D::add(acc, D::load(s_ptr[q], e));
+        acc_out[e - begin] = (double)acc;
+      }
+    }
+  }
+}
+
+// Gather element ranges of `full` into `packed` (dir 0), or scatter `packed`
+// back into every `dst` (dir 1).  ranges[r] = {lo, hi, packed offset}.
+template <class T>
+__global__ void k_ranges(const T* full, T* packed, T* const* dst, int n_dst, const int64_t* ranges, int dir) {
+  const int64_t lo = ranges[3 * blockIdx.y], hi = ranges[3 * blockIdx.y + 1], off = ranges[3 * blockIdx.y + 2];
+  for (int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < hi; e += (int64_t)gridDim.x * blockDim.x) {
+    if (dir == 0) {
+      packed[off + (e - lo)] = full[e];
+    } else {
+      const T v = packed[off + (e - lo)];
+      for (int d = 0; d < n_dst; ++d) dst[d][e] = v;
+    }
+  }
+}
+
+// Scatter one final vector into several replicas (multi-GPU fan-out).
+__global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* const* dst, int n_dst, int64_t nbytes) {
+  extern __shared__ __align__(16) const void* s_ptr[];
+  void** s_dst = const_cast<void**>(s_ptr);
+  const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, dst, n_dst, (uintptr_t)src);
+  const int64_t nvec = aligned ? nbytes / 32 : 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const V8 x = ld_stream(reinterpret_cast<const V8*>(src) + v);
+    for (int d = 0; d < n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + v, x);
+  }
+  for (int64_t b = nvec * 32 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned char x = ((const unsigned char*)src)[b];
+    for (int d = 0; d < n_dst; ++d) ((unsigned char*)s_dst[d])[b] = x;
   }
 }
 
@@ -581,7 +686,8 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
     double v;
     if (slot >= 0) v = corrupt_value(cd, p.ws[e], e, p.host_copies, slot, p.P);
     else if (p.fallback) v = p.fallback[e];
-    else if (p.n_alive > 0) v = D::raw(p.src[0], e);  // lowest alive upload (butterfly.py:270-271)
+    else if (p.fb_src) v = D::raw(p.fb_src, e);  // lowest alive upload (butterfly.py:270-271)
+    else if (p.n_alive > 0) v = D::raw(p.src[0], e);
     else v = nan64();
     if (p.merged) p.merged[e] = v;
     for (int d = 0; d < p.n_dst; ++d) D::store(p.dst[d], e, v);
@@ -671,8 +777,8 @@ using namespace bfly;
 
 template <class D>
 static void launch_reduce(const Params& p, cudaStream_t st) {
-  const int64_t tile = (int64_t)kThreads * kVecPerThread * D::K;
-  const int64_t ntiles = (p.P + tile - 1) / tile;
+  const int64_t tile = (int64_t)kThreads * D::K;
+  const int64_t ntiles = (p.eend + tile - 1) / tile - p.ebeg / tile;
   int64_t grid = (int64_t)sm_count() * 8;
   if (grid > ntiles) grid = ntiles;
   const size_t smem = sizeof(void*) * (size_t)(p.n_alive + p.n_dst);
@@ -707,6 +813,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   if (!a->d_assign || !a->d_failed || !a->d_corr || !a->d_status || !a->d_entries || !a->d_flagged)
     return fail(BFLY_E_INVALID_ARG, "missing required device array");
   if (a->n_alive > 0 && !a->d_src) return fail(BFLY_E_INVALID_ARG, "missing replicas");
+  if (a->n_alive == 0 && a->n_div > 0 && !a->d_acc_in) return fail(BFLY_E_INVALID_ARG, "n_div without replicas");
   if (a->n_dst > 0 && !a->d_dst) return fail(BFLY_E_INVALID_ARG, "missing scatter-back targets");
   if (!a->d_merged && !a->d_ws) return fail(BFLY_E_INVALID_ARG, "need d_merged or d_ws");
   ScratchLayout L;
@@ -746,16 +853,25 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   p.has_score = sc + L.off_has;
   p.inv = p.r > 2 ? (int32_t*)(sc + L.off_inv) : nullptr;
   p.tol = a->tolerance;
+  p.acc_in = a->d_acc_in;
+  p.n_div = a->n_div > 0 ? a->n_div : a->n_alive;
+  p.ebeg = a->elem_begin;
+  p.eend = (a->elem_begin == 0 && a->elem_end == 0) ? a->payload_len : a->elem_end;
+  if (p.ebeg < 0 || p.eend > p.P || p.ebeg > p.eend) return fail(BFLY_E_INVALID_ARG, "bad element range");
+  if (p.acc_in && p.bnd.base == 1) return fail(BFLY_E_UNSUPPORTED, "chained reduction needs shards of >= 2 elements");
+  p.fb_src = a->d_fallback_src ? a->d_fallback_src : nullptr;
   cudaStream_t st = (cudaStream_t)stream;
 
   const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
   const bool do_finish = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH;
   if (do_reduce) {
-    const int64_t nn = (int64_t)p.n * p.n;
-    k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
-    cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
-    k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
-    if (p.n_alive > 0) {
+    if (p.ebeg == 0) {  // per-round setup runs with the first (or only) element range
+      const int64_t nn = (int64_t)p.n * p.n;
+      k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
+      cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
+      k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
+    }
+    if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
       switch (a->dtype) {
         case BFLY_F32: launch_reduce<DF32>(p, st); break;
         case BFLY_BF16: launch_reduce<DBF16>(p, st); break;
@@ -778,6 +894,70 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bfly_merge launch");
+  return BFLY_OK;
+}
+
+int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
+                    double* d_acc_out, int64_t begin, int64_t end, void* stream) {
+  if (n_src < 0 || (n_src > 0 && !d_src) || !d_acc_out || begin < 0 || end < begin)
+    return fail(BFLY_E_INVALID_ARG, "bad chain-step arguments");
+  if (end == begin) return BFLY_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = sizeof(void*) * (size_t)n_src;
+  auto go = [&](auto kern, int K) {
+    const int64_t tile = (int64_t)kThreads * K;
+    int64_t grid = (end + tile - 1) / tile - begin / tile;
+    if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)grid, kThreads, smem, st>>>(d_src, n_src, d_acc_in, d_acc_out, begin, end);
+  };
+  switch (dtype) {
+    case BFLY_F32: go(k_chain<DF32>, DF32::K); break;
+    case BFLY_BF16: go(k_chain<DBF16>, DBF16::K); break;
+    case BFLY_F64WIRE: go(k_chain<DF64W>, DF64W::K); break;
+    default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_chain_step launch");
+  return BFLY_OK;
+}
+
+int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int32_t n_dst, const int64_t* d_ranges,
+                     int32_t n_ranges, int32_t elem_size, int32_t scatter, void* stream) {
+  if (n_ranges < 0 || n_ranges > 65535 || (elem_size != 2 && elem_size != 4 && elem_size != 8) || !d_packed ||
+      (!scatter && !d_full) || (scatter && n_dst > 0 && !d_dst))
+    return fail(BFLY_E_INVALID_ARG, "bad copy-ranges arguments");
+  if (n_ranges == 0) return BFLY_OK;
+  const dim3 grid(64, (unsigned)n_ranges);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (elem_size) {
+    case 2:
+      k_ranges<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)d_full, (uint16_t*)d_packed, (uint16_t* const*)d_dst,
+                                               n_dst, d_ranges, scatter);
+      break;
+    case 4:
+      k_ranges<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)d_full, (uint32_t*)d_packed, (uint32_t* const*)d_dst,
+                                               n_dst, d_ranges, scatter);
+      break;
+    default:
+      k_ranges<uint64_t><<<grid, 256, 0, st>>>((const uint64_t*)d_full, (uint64_t*)d_packed, (uint64_t* const*)d_dst,
+                                               n_dst, d_ranges, scatter);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_copy_ranges launch");
+  return BFLY_OK;
+}
+
+int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream) {
+  if (!d_src || n_dst < 0 || (n_dst > 0 && !d_dst) || nbytes < 0) return fail(BFLY_E_INVALID_ARG, "bad fanout arguments");
+  if (n_dst == 0 || nbytes == 0) return BFLY_OK;
+  int64_t grid = (nbytes / 32 + kThreads - 1) / kThreads;
+  if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+  if (grid < 1) grid = 1;
+  k_fanout<<<(unsigned)grid, kThreads, sizeof(void*) * (size_t)n_dst, (cudaStream_t)stream>>>(d_src, d_dst, n_dst,
+                                                                                             nbytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_fanout launch");
   return BFLY_OK;
 }
 

@@ -142,31 +142,38 @@ def corruption_table(n: int, corruptions: dict | None, host_kinds=()) -> bytes:
 class ButterflyMerge:
     """One prepared merge round over device-resident replicas.
 
-    replicas     N contiguous 1-D CUDA tensors (float32 wire values, bfloat16, or
-                 float64 payloads that are rounded to the fp32 wire on load), in
-                 miner-index order (the reference's sorted(payloads), butterfly.py:189).
+    replicas     list of N entries in miner-index order (the reference's
+                 sorted(payloads), butterfly.py:189): contiguous 1-D CUDA tensors
+                 (float32 wire values, bfloat16, or float64 payloads rounded to the
+                 fp32 wire on load).  None marks a failed miner or — with
+                 ``remote_sum`` — a miner resident on another GPU.
     plan         DevicePlan (or any object with .assign [S, r] int32 CUDA tensor).
     failures     miner indices that dropped before upload (butterfly.py:167,203).
     corruptions  {miner index: Corruption}; ``host_miners`` lists miners whose
                  copies the caller supplies to ``run(host_copies=...)``.
     fallback     optional fp64 [P] CUDA tensor (butterfly.py:169,268-273).
-    scatter_back write the adopted slices into every replica in place.
+    fallback_src replica supplying fallback values when ``fallback`` is None
+                 (default: the lowest alive resident replica).
+    scatter_back write the adopted slices into every resident replica in place.
     want_merged  also produce the fp64 merged vector (MergeResult.merged).
     keep_means   keep special-shard means in a separate workspace (read back by
                  the drop-in shim for the store's lazy blobs).
+    remote_sum   multi-GPU chain: the running sums of the miners on earlier GPUs
+                 arrive through ``reduce_range(acc_in=...)`` and the mean divides
+                 by ``n_div`` = alive miners on all GPUs.
     """
 
     def __init__(self, replicas, plan, *, failures=(), corruptions=None, host_miners=(), fallback=None,
-                 scatter_back: bool = True, want_merged: bool = False, keep_means: bool = False,
-                 tolerance: float = 1e-6):
+                 fallback_src=None, scatter_back: bool = True, want_merged: bool = False,
+                 keep_means: bool = False, tolerance: float = 1e-6, remote_sum: bool = False,
+                 n_div: int | None = None):
         n = len(replicas)
         if n != plan.n_miners:
             raise errors.ShapeError(f"plan expects {plan.n_miners} payloads, got {n}")
         failures = set(int(m) for m in failures)
         present = [t for t in replicas if t is not None]
-        if any(t is None for m, t in enumerate(replicas) if m not in failures) or (
-                scatter_back and len(present) != n):
-            raise errors.InvalidArgumentError("only failed miners may be passed as None, and not with scatter_back")
+        if not remote_sum and any(t is None for m, t in enumerate(replicas) if m not in failures):
+            raise errors.InvalidArgumentError("only failed miners may be passed as None")
         if not present:
             raise errors.InvalidArgumentError("no replica tensors given")
         dev = present[0].device
@@ -190,12 +197,17 @@ class ButterflyMerge:
         self.r = plan.redundancy
         self.S = plan.n_shards
         self.dtype = _DTYPES[next(iter(dtypes))]
+        self.elem_size = next(iter(dtypes)).itemsize
         self.alive = [m for m in range(n) if m not in failures]
+        self.local_alive = [m for m in self.alive if replicas[m] is not None]
+        self.resident = [m for m in range(n) if replicas[m] is not None]
         self.replicas = list(replicas)
         self.plan = plan
+        self.remote_sum = remote_sum
+        self.n_div = int(n_div) if n_div is not None else len(self.alive)
 
-        self._src = _ptr_table([replicas[m] for m in self.alive], dev) if self.alive else None
-        self._dst = _ptr_table(replicas, dev) if scatter_back else None
+        self._src = _ptr_table([replicas[m] for m in self.local_alive], dev) if self.local_alive else None
+        self._dst = _ptr_table([replicas[m] for m in self.resident], dev) if scatter_back else None
         failed = np.zeros(n, dtype=np.uint8)
         for m in failures:
             failed[m] = 1
@@ -203,31 +215,33 @@ class ButterflyMerge:
         self._corr = torch.frombuffer(bytearray(corruption_table(n, corruptions, host_miners)),
                                       dtype=torch.uint8).to(dev)
         self.fallback = None if fallback is None else fallback.to(dev, torch.float64).contiguous()
+        self.fallback_src = fallback_src
         self.status = torch.empty(self.S, dtype=torch.uint8, device=dev)
         self.entries = torch.empty((n, n), dtype=torch.float64, device=dev)
         self.flagged = torch.empty(n, dtype=torch.uint8, device=dev)
         self.source = torch.empty(self.S, dtype=torch.int32, device=dev)
         self.merged = torch.empty(P, dtype=torch.float64, device=dev) if want_merged else None
-        special = bool(corruptions) or bool(host_miners)
+        self.special = bool({m for m in (corruptions or {}) if m not in failures}) or bool(host_miners)
+        # a shard is lost only if all of its r assignees failed
+        self.maybe_lost = len(failures) >= self.r
         self.means = (torch.empty(P, dtype=torch.float64, device=dev)
-                      if special and (keep_means or not want_merged) else None)
+                      if self.special and (keep_means or not want_merged) else None)
+        if self.means is None and self.merged is None:  # never written without special shards
+            self.means = torch.empty(1, dtype=torch.float64, device=dev)
         scratch_bytes = int(L.lib().bfly_merge_scratch_bytes(n, self.r, P))
         self._scratch = torch.empty(max(scratch_bytes, 1), dtype=torch.uint8, device=dev)
 
         a = L.MergeArgs()
         a.n_miners, a.redundancy, a.payload_len, a.n_shards = n, self.r, P, self.S
-        a.dtype, a.n_alive = self.dtype, len(self.alive)
+        a.dtype, a.n_alive = self.dtype, len(self.local_alive)
         a.d_assign = plan.assign.data_ptr()
         a.d_src = self._src.data_ptr() if self._src is not None else None
         a.d_failed = self._failed.data_ptr()
         a.d_corr = self._corr.data_ptr()
         a.d_dst = self._dst.data_ptr() if self._dst is not None else None
-        a.n_dst = n if scatter_back else 0
+        a.n_dst = len(self.resident) if scatter_back else 0
         a.d_fallback = self.fallback.data_ptr() if self.fallback is not None else None
         a.d_merged = self.merged.data_ptr() if self.merged is not None else None
-        # a scratch mean buffer is still needed when there is no merged output
-        if self.means is None and self.merged is None:
-            self.means = torch.empty(1, dtype=torch.float64, device=dev)
         a.d_ws = self.means.data_ptr() if self.means is not None else None
         a.d_status = self.status.data_ptr()
         a.d_entries = self.entries.data_ptr()
@@ -236,20 +250,48 @@ class ButterflyMerge:
         a.d_scratch = self._scratch.data_ptr()
         a.scratch_bytes = scratch_bytes
         a.tolerance = float(tolerance)
+        a.n_div = self.n_div
+        a.d_fallback_src = fallback_src.data_ptr() if fallback_src is not None else None
         self._args = a
         self._host_copies = None
+        self._acc_in = None
+
+    def _call(self, stream):
+        with torch.cuda.device(self.dev):
+            L.check(L.lib().bfly_merge(ctypes.byref(self._args), _stream_handle(stream)))
 
     def run(self, phase: int = L.PHASE_ALL, host_copies: torch.Tensor | None = None, stream=None) -> "ButterflyMerge":
         """Issue the merge kernels on ``stream`` (default: current stream). Asynchronous."""
+        if self.remote_sum and phase != L.PHASE_FINISH:
+            raise errors.InvalidArgumentError("a chained merge reduces through reduce_range(acc_in=...)")
         if host_copies is not None:
             self._host_copies = host_copies
             self._args.d_host_copies = host_copies.data_ptr()
+        if phase == L.PHASE_FINISH and not self.needs_finish():
+            return self  # every shard is fast: nothing to compare, adopt or fall back
         self._args.phase = phase
-        with torch.cuda.device(self.dev):
-            L.check(L.lib().bfly_merge(ctypes.byref(self._args), _stream_handle(stream)))
+        self._args.d_acc_in = None
+        self._args.elem_begin = self._args.elem_end = 0
+        self._call(stream)
         return self
+
+    def reduce_range(self, begin: int, end: int, acc_in: torch.Tensor | None = None, stream=None):
+        """REDUCE elements [begin, end) — call with begin == 0 first in every round.
+        ``acc_in`` holds the running fp64 sums of the miners on earlier GPUs."""
+        if acc_in is not None and (acc_in.dtype != torch.float64 or acc_in.numel() < end - begin):
+            raise errors.ShapeError("acc_in must be float64 covering [begin, end)")
+        self._acc_in = acc_in
+        self._args.phase = L.PHASE_REDUCE
+        self._args.d_acc_in = acc_in.data_ptr() if acc_in is not None else None
+        self._args.elem_begin, self._args.elem_end = int(begin), int(end)
+        self._call(stream)
+        return self
+
+    def needs_finish(self) -> bool:
+        return self.special or self.maybe_lost
 
     # number of our kernels one run() launches (reported by bench.py as gpu_launches)
     def launches_per_run(self) -> int:
-        # k_fill_nan, k_classify, [k_reduce], k_stats, k_decide, [k_entries3], k_apply
-        return 2 + (1 if self.alive else 0) + 3 + (1 if self.r > 2 else 0)
+        # k_fill_nan, k_classify, [k_reduce] + [k_stats, k_decide, [k_entries3], k_apply]
+        fin = (3 + (1 if self.r > 2 else 0)) if self.needs_finish() else 0
+        return 2 + (1 if self.local_alive or self.remote_sum else 0) + fin
