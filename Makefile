@@ -21,3 +21,9 @@ clean:
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean
+
+# tuning build (not the product): adds bfly_tune_reduce for tools/tune_reduce.py
+tune: build/libbfly_tune.so
+build/libbfly_tune.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DBFLY_TUNING -shared -o $@ $(SRCS) 2> build/ptxas_tune.log || (cat build/ptxas_tune.log; false)
+.PHONY: tune

@@ -320,6 +320,10 @@ def run_multi(cfg, args, rank, world):
     dist.init_process_group("nccl", device_id=dev)
     n_local, P, dtype, r, k_bad = cfg
     n = n_local * world
+    if args.max_ctas:
+        from paper_2507_17766_b200 import _lib as L
+
+        L.check(L.lib().bfly_set_max_ctas(args.max_ctas))
     reps = make_replicas(n_local, P, dtype, dev, seed=rank * n_local)
     plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
     bad = deceptive_set(n, k_bad)
@@ -372,6 +376,55 @@ def run_multi(cfg, args, rank, world):
     dist.destroy_process_group()
 
 
+def run_stages(cfg, args, rank, world):
+    """Config 4: one pipeline stage per GPU; stages merge independently
+    (orchestrator.py:596-597 loops over layers), so N GPUs run N independent
+    merges — replicas only, no exchange.  Timing is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
+
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    n, P, dtype, r, _ = cfg
+    reps = make_replicas(n, P, dtype, dev, seed=1000 * rank)
+    plan = DevicePlan(n, P, rank, redundancy=r, device=dev)
+    job = ButterflyMerge(reps, plan, scatter_back=True)
+
+    def step(timed=False):
+        job.run()
+
+    total_ms, _, clocks = timed_rounds(step, args, dev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item()) / args.steps / 1e3
+    if rank == 0:
+        esize = BYTES[dtype]
+        alg = world * merge_bytes(n, P, esize)
+        hbm_peak = _peaks().get("hbm_gbs", 6650.0)
+        line = {
+            "metric": METRIC, "value": alg / t_step / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic uniform(-1,1) bf16 replicas (torch Philox)",
+            "config": {"workload": WORKLOAD["c4"], "miners_per_stage": n, "params_per_stage": P, "stages": world,
+                       "replica_dtype": dtype, "redundancy": r, "parallelism": "one stage per GPU (replicas only)",
+                       "l2": "inputs %.0f GB per GPU >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
+            "params_merged_per_s": world * P / t_step,
+            "roofline": {"bound": "hbm", "achieved": merge_bytes(n, P, esize) / t_step / 1e9, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": merge_bytes(n, P, esize) / t_step / 1e9 / hbm_peak,
+                         "traffic": None, "kernel": "whole merge round per GPU"},
+            "e2e": None, "cpu_baseline": None, "gpu_launches": job.launches_per_run() * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def run_reference(cfg, args, rank, world):
     """--impl reference: the CPU restatement of the reference's run_all_reduce
     (oracle/bfly_oracle.c, all host threads) on fp64 payloads — the reference API's
@@ -412,6 +465,7 @@ def main():
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
     ap.add_argument("--params", type=int, default=None, help="override the stage size")
     ap.add_argument("--chunk", type=int, default=1 << 24)
+    ap.add_argument("--max-ctas", type=int, default=0, help="cap streaming-kernel CTAs (multi-GPU)")
     ap.add_argument("--e2e-params", type=int, default=1 << 27)
     ap.add_argument("--cpu-params", type=int, default=1 << 25)
     ap.add_argument("--no-e2e", action="store_true")
@@ -427,7 +481,7 @@ def main():
     if args.impl == "reference":
         return run_reference(cfg, args, rank, world)
     if world > 1:
-        return run_multi(cfg, args, rank, world)
+        return run_stages(cfg, args, rank, world) if name == "c4" else run_multi(cfg, args, rank, world)
 
     import torch
 

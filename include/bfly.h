@@ -142,6 +142,11 @@ int bfly_merge(const bfly_merge_args_t* args, void* stream);
 int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
                     double* d_acc_out, int64_t begin, int64_t end, void* stream);
 
+/* Cap the grid of the streaming kernels (k_reduce, k_chain, k_fanout) at max_ctas
+ * CTAs (0 = no cap, the default).  The multi-GPU merge leaves SMs to the NCCL
+ * kernels that move the running sums, so transfers overlap the HBM stream. */
+int bfly_set_max_ctas(int32_t max_ctas);
+
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);
 

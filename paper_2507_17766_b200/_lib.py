@@ -37,6 +37,7 @@ EXPORTS = (
     "bfly_chain_step",
     "bfly_fanout",
     "bfly_copy_ranges",
+    "bfly_set_max_ctas",
 )
 
 
@@ -115,6 +116,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_mean_rows.argtypes = [vp, i32, i64, vp, vp]
     L.bfly_chain_step.argtypes = [vp, i32, i32, vp, vp, i64, i64, vp]
     L.bfly_fanout.argtypes = [vp, vp, i32, i64, vp]
+    L.bfly_set_max_ctas.argtypes = [i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)

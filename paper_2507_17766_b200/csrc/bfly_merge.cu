@@ -278,12 +278,26 @@ __global__ void k_classify(Params p) {
 // Sequential accumulation of one 32-byte vector per thread over the replica
 // table, U replicas' loads in flight before their adds (the add order stays
 // ascending, which is what parity needs).
-template <class D>
+template <class D, int U = 4, bool NO_OUTER_UNROLL = false>
 __device__ __forceinline__ void accumulate_vec(typename D::Acc (&acc)[D::K], const void* const* s_src, int n,
                                                int64_t vidx) {
   constexpr int K = D::K;
-  constexpr int U = 4;
   int q = 0;
+  if constexpr (NO_OUTER_UNROLL) {
+#pragma unroll 1
+    for (; q + U <= n; q += U) {
+      V8 raw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) raw[u] = ld_stream(reinterpret_cast<const V8*>(s_src[q + u]) + vidx);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        typename D::Acc x[K];
+        D::unpack(raw[u], x);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = D::add(acc[k], x[k]);
+      }
+    }
+  }
   for (; q + U <= n; q += U) {
     V8 raw[U];
 #pragma unroll
@@ -336,8 +350,8 @@ __device__ __forceinline__ bool stage_pointers(const void** s_src, void** s_dst,
   return __syncthreads_or((int)(mis & 31)) == 0;
 }
 
-template <class D>
-__global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
+template <class D, int U = 4, int MINB = 1, bool NOU = false>
+__global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_alive] src, then [n_dst] dst
   const void** s_src = s_ptr;
   void** s_dst = const_cast<void**>(s_ptr + p.n_alive);
@@ -368,7 +382,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce(Params p) {
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = D::zero();
       }
-      accumulate_vec<D>(acc, s_src, p.n_alive, vidx);
+      accumulate_vec<D, U, NOU>(acc, s_src, p.n_alive, vidx);
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = D::mean(acc[k], p.n_div);
       if (p.merged) {
@@ -775,15 +789,26 @@ __global__ void k_mean_rows(const double* stack, int32_t rows, int64_t width, do
 
 using namespace bfly;
 
-template <class D>
-static void launch_reduce(const Params& p, cudaStream_t st) {
+// Optional cap on the CTAs of the streaming kernels (bfly_set_max_ctas): with one
+// resident CTA per SM it leaves SMs free for concurrent NCCL kernels.
+static int g_max_ctas = 0;
+static int64_t cap_grid(int64_t grid) {
+  if (g_max_ctas > 0 && grid > g_max_ctas) grid = g_max_ctas;
+  return grid < 1 ? 1 : grid;
+}
+
+template <class D, int U = 4, int MINB = 1, bool NOU = false>
+static void launch_reduce(const Params& p, cudaStream_t st, int grid_per_sm = 8) {
   const int64_t tile = (int64_t)kThreads * D::K;
   const int64_t ntiles = (p.eend + tile - 1) / tile - p.ebeg / tile;
-  int64_t grid = (int64_t)sm_count() * 8;
+  int64_t grid = (int64_t)sm_count() * grid_per_sm;
   if (grid > ntiles) grid = ntiles;
+  grid = cap_grid(grid);
+  if (grid < 1) grid = 1;
   const size_t smem = sizeof(void*) * (size_t)(p.n_alive + p.n_dst);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_reduce<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_reduce<D><<<(unsigned)grid, kThreads, smem, st>>>(p);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_reduce<D, U, MINB, NOU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_reduce<D, U, MINB, NOU><<<(unsigned)grid, kThreads, smem, st>>>(p);
 }
 
 template <class D>
@@ -799,7 +824,7 @@ size_t bfly_merge_scratch_bytes(int32_t n_miners, int32_t redundancy, int64_t pa
   return L.total;
 }
 
-int bfly_merge(const bfly_merge_args_t* a, void* stream) {
+static int build_params(const bfly_merge_args_t* a, Params& p) {
   if (!a) return fail(BFLY_E_INVALID_ARG, "null args");
   if (a->n_miners < 2) return fail(BFLY_E_TOO_FEW_MINERS, "need at least 2 miners");
   if (a->redundancy < 2 || a->redundancy > kMaxR)
@@ -823,7 +848,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   if ((int64_t)(a->n_alive + a->n_dst) * 8 > 200 * 1024) return fail(BFLY_E_UNSUPPORTED, "too many replicas");
   if (L.cps > 65535) return fail(BFLY_E_UNSUPPORTED, "shards longer than 65535 chunks");
 
-  Params p{};
+  p = Params{};
   p.n = a->n_miners;
   p.r = a->redundancy;
   p.n_alive = a->n_alive;
@@ -860,6 +885,14 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   if (p.ebeg < 0 || p.eend > p.P || p.ebeg > p.eend) return fail(BFLY_E_INVALID_ARG, "bad element range");
   if (p.acc_in && p.bnd.base == 1) return fail(BFLY_E_UNSUPPORTED, "chained reduction needs shards of >= 2 elements");
   p.fb_src = a->d_fallback_src ? a->d_fallback_src : nullptr;
+  return BFLY_OK;
+}
+
+int bfly_merge(const bfly_merge_args_t* a, void* stream) {
+  Params p;
+  int rc = build_params(a, p);
+  if (rc) return rc;
+  const int64_t S = p.S;
   cudaStream_t st = (cudaStream_t)stream;
 
   const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
@@ -873,7 +906,9 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
     }
     if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
       switch (a->dtype) {
-        case BFLY_F32: launch_reduce<DF32>(p, st); break;
+        case BFLY_F32:  // U=4, 3 CTAs/SM, 16 CTAs/SM grid: best of tools/tune_reduce.py (profiles/)
+          launch_reduce<DF32, 4, 3, true>(p, st, 16);
+          break;
         case BFLY_BF16: launch_reduce<DBF16>(p, st); break;
         default: launch_reduce<DF64W>(p, st); break;
       }
@@ -897,6 +932,33 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   return BFLY_OK;
 }
 
+#ifdef BFLY_TUNING
+// Tuning build only (build/libbfly_tune.so, tools/tune_reduce.py): launch k_reduce
+// alone with a chosen (replicas in flight, min CTAs/SM) variant and grid size, on
+// params whose per-round setup already ran through bfly_merge.
+int bfly_tune_reduce(const bfly_merge_args_t* a, int variant, int grid_per_sm, void* stream) {
+  Params p;
+  int rc = build_params(a, p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (a->dtype != BFLY_F32) return fail(BFLY_E_UNSUPPORTED, "tuning covers fp32");
+  switch (variant) {
+    case 0: launch_reduce<DF32, 4, 1, false>(p, st, grid_per_sm); break;
+    case 1: launch_reduce<DF32, 4, 2, true>(p, st, grid_per_sm); break;
+    case 2: launch_reduce<DF32, 8, 1, true>(p, st, grid_per_sm); break;
+    case 3: launch_reduce<DF32, 8, 2, true>(p, st, grid_per_sm); break;
+    case 4: launch_reduce<DF32, 4, 3, true>(p, st, grid_per_sm); break;
+    case 5: launch_reduce<DF32, 16, 1, true>(p, st, grid_per_sm); break;
+    case 6: launch_reduce<DF32, 2, 4, true>(p, st, grid_per_sm); break;
+    case 7: launch_reduce<DF32, 4, 1, true>(p, st, grid_per_sm); break;
+    default: return fail(BFLY_E_INVALID_ARG, "unknown variant");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_tune_reduce launch");
+  return BFLY_OK;
+}
+#endif
+
 int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
                     double* d_acc_out, int64_t begin, int64_t end, void* stream) {
   if (n_src < 0 || (n_src > 0 && !d_src) || !d_acc_out || begin < 0 || end < begin)
@@ -908,6 +970,7 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
     const int64_t tile = (int64_t)kThreads * K;
     int64_t grid = (end + tile - 1) / tile - begin / tile;
     if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+    grid = cap_grid(grid);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, kThreads, smem, st>>>(d_src, n_src, d_acc_in, d_acc_out, begin, end);
   };
@@ -948,11 +1011,18 @@ int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int
   return BFLY_OK;
 }
 
+int bfly_set_max_ctas(int32_t max_ctas) {
+  if (max_ctas < 0) return fail(BFLY_E_INVALID_ARG, "max_ctas must be >= 0");
+  g_max_ctas = max_ctas;
+  return BFLY_OK;
+}
+
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream) {
   if (!d_src || n_dst < 0 || (n_dst > 0 && !d_dst) || nbytes < 0) return fail(BFLY_E_INVALID_ARG, "bad fanout arguments");
   if (n_dst == 0 || nbytes == 0) return BFLY_OK;
   int64_t grid = (nbytes / 32 + kThreads - 1) / kThreads;
   if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+  grid = cap_grid(grid);
   if (grid < 1) grid = 1;
   k_fanout<<<(unsigned)grid, kThreads, sizeof(void*) * (size_t)n_dst, (cudaStream_t)stream>>>(d_src, d_dst, n_dst,
                                                                                              nbytes);

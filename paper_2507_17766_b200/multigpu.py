@@ -250,6 +250,15 @@ class ShardedButterflyMerge:
         K = len(self._chunks())
         nb = 3
         T = K + 3 * Z + 1 if G > 1 else K
+        # fallback values (the lowest alive miner's replica) for the late shards,
+        # moved before the fan-out below overwrites that replica
+        if self._needs_fb and self.fb_owner != Z:
+            if g == self.fb_owner:
+                self.ops.gather_ranges(self.local[self.alive[0] - self.offset], self._packed, self._ranges)
+                dist.send(self._packed, dst=Z)
+            elif self.is_last:
+                dist.recv(self._packed, src=self.fb_owner)
+                self.ops.scatter_ranges(self._packed, [self._fb_buf], self._ranges)
         pending = []
         for t in range(T):
             for w in pending:  # data received at step t-1 is needed now
@@ -272,12 +281,6 @@ class ShardedButterflyMerge:
             w.wait()
 
         last = Z
-        # fallback values from the lowest alive miner's replica, if it lives elsewhere
-        if self._needs_fb and self.fb_owner != last:
-            if g == self.fb_owner:
-                dist.send(self.local[self.alive[0] - self.offset], dst=last)
-            elif self.is_last:
-                dist.recv(self._fb_buf, src=self.fb_owner)
 
         # finish on the last rank, then the per-shard results and the late shards
         res = torch.empty(self._res_bytes, dtype=torch.uint8, device=self._comm_dev())

@@ -238,4 +238,6 @@ def test_store_contents_materialise_like_the_reference():
             mean = np.mean([_f32(payloads[m][lo:hi]) for m in range(n) if m != 1], axis=0)
             want = (mean + 0.5 if x == 2 else mean).astype("<f4").tobytes()
             assert store.get("x", f"ep/0/miner/{x}/merged/{s}") == want
-    assert res.flagged == {2}
+    # both members of every disagreeing pair are flagged (butterfly.py:266-267)
+    partners = {m for pair in plan.assignment if 2 in pair for m in pair if m != 1}
+    assert res.flagged == partners
