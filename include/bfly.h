@@ -147,6 +147,20 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
  * kernels that move the running sums, so transfers overlap the HBM stream. */
 int bfly_set_max_ctas(int32_t max_ctas);
 
+/* ---- peer memory for the multi-GPU merge (one process per GPU, one node) ---- */
+/* cudaMalloc a zero-filled region and export its CUDA IPC handle (64 bytes). */
+int bfly_ipc_alloc(size_t bytes, void** d_ptr, uint8_t handle[64]);
+/* Map a neighbour's region (peer access over NVLink enabled lazily). */
+int bfly_ipc_open(const uint8_t handle[64], void** d_ptr);
+int bfly_ipc_close(void* d_ptr);
+int bfly_ipc_free(void* d_ptr);
+/* Stream-ordered cross-GPU signalling (CUDA stream memory operations, no SM spin):
+ * the stream waits until (int32)(*d_flag - value) >= 0, flushing remote writes
+ * when the device supports it; or writes value to *d_flag (with a memory
+ * barrier) once all earlier work in the stream is done. */
+int bfly_stream_wait_value(const uint32_t* d_flag, uint32_t value, void* stream);
+int bfly_stream_write_value(uint32_t* d_flag, uint32_t value, void* stream);
+
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);
 

@@ -38,6 +38,12 @@ EXPORTS = (
     "bfly_fanout",
     "bfly_copy_ranges",
     "bfly_set_max_ctas",
+    "bfly_ipc_alloc",
+    "bfly_ipc_open",
+    "bfly_ipc_close",
+    "bfly_ipc_free",
+    "bfly_stream_wait_value",
+    "bfly_stream_write_value",
 )
 
 
@@ -117,6 +123,13 @@ def lib() -> ctypes.CDLL:
     L.bfly_chain_step.argtypes = [vp, i32, i32, vp, vp, i64, i64, vp]
     L.bfly_fanout.argtypes = [vp, vp, i32, i64, vp]
     L.bfly_set_max_ctas.argtypes = [i32]
+    u32 = ctypes.c_uint32
+    L.bfly_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
+    L.bfly_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+    L.bfly_ipc_close.argtypes = [vp]
+    L.bfly_ipc_free.argtypes = [vp]
+    L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
+    L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)

@@ -275,16 +275,29 @@ class ButterflyMerge:
         self._call(stream)
         return self
 
-    def reduce_range(self, begin: int, end: int, acc_in: torch.Tensor | None = None, stream=None):
+    def reduce_range(self, begin: int, end: int, acc_in=None, stream=None, dst_table: tuple | None = None):
         """REDUCE elements [begin, end) — call with begin == 0 first in every round.
-        ``acc_in`` holds the running fp64 sums of the miners on earlier GPUs."""
-        if acc_in is not None and (acc_in.dtype != torch.float64 or acc_in.numel() < end - begin):
-            raise errors.ShapeError("acc_in must be float64 covering [begin, end)")
-        self._acc_in = acc_in
+
+        ``acc_in`` holds the running fp64 sums of the miners on earlier GPUs (a
+        float64 tensor covering [begin, end), or a raw device pointer into peer
+        memory).  ``dst_table`` = (device pointer, count) overrides the
+        scatter-back targets for this call (the multi-GPU last rank adds the next
+        GPU's inbox, biased by -begin, so the final chunk is pushed over NVLink)."""
+        if isinstance(acc_in, torch.Tensor):
+            if acc_in.dtype != torch.float64 or acc_in.numel() < end - begin:
+                raise errors.ShapeError("acc_in must be float64 covering [begin, end)")
+            self._acc_in = acc_in
+            acc_in = acc_in.data_ptr()
         self._args.phase = L.PHASE_REDUCE
-        self._args.d_acc_in = acc_in.data_ptr() if acc_in is not None else None
+        self._args.d_acc_in = acc_in if acc_in else None
         self._args.elem_begin, self._args.elem_end = int(begin), int(end)
-        self._call(stream)
+        saved = (self._args.d_dst, self._args.n_dst)
+        if dst_table is not None:
+            self._args.d_dst, self._args.n_dst = dst_table
+        try:
+            self._call(stream)
+        finally:
+            self._args.d_dst, self._args.n_dst = saved
         return self
 
     def needs_finish(self) -> bool:
