@@ -47,6 +47,7 @@ from . import ringsched as rs
 from .device import ButterflyMerge, _DTYPES, _stream_handle
 
 NB = 3  # inbox slots per ring
+WINDOW = 4  # chunks the host may run ahead of the GPUs per stream
 
 
 def special_ranges(assign: np.ndarray, P: int, failures: set, corrupted: set) -> list:
@@ -154,6 +155,7 @@ class ShardedButterflyMerge:
         self.want_merged = want_merged
         self.is_last = self.rank == G - 1
         self._round = 0
+        self.debug = int(__import__("os").environ.get("BFLY_DEBUG_RING", "0"))
         self._tables = []  # keeps the device pointer tables alive
         self._peer = None
 
@@ -297,6 +299,39 @@ class ShardedButterflyMerge:
             L.check(lib.bfly_fanout(lay.fin_slot(self._base, s), tab.data_ptr(), tab.numel(), (e - b) * self.esize,
                                     stream))
 
+    def _host_wait(self, events, deadline: float = 120.0):
+        import time
+
+        t0 = time.time()
+        while not all(e.query() for e in events):
+            if time.time() - t0 > deadline:
+                raise RuntimeError("multi-GPU ring made no progress for %.0f s" % deadline)
+            time.sleep(20e-6)
+
+    def _watch(self, marks, deadline: float = 30.0):
+        """Debug aid (BFLY_DEBUG_RING=1): wait for every op with a deadline and report
+        the first op each stream is stuck at, with this rank's flag values."""
+        import sys
+        import time
+
+        t0 = time.time()
+        while not all(ev.query() for _, ev in marks):
+            if time.time() - t0 > deadline:
+                stuck = {}
+                for op, ev in marks:
+                    if not ev.query() and op[1] not in stuck:
+                        stuck[op[1]] = op
+                flags = torch.empty(4 * NB, dtype=torch.int32, device=self.dev)
+                side = torch.cuda.Stream(device=self.dev)
+                with torch.cuda.stream(side):
+                    L.lib().bfly_fanout(self._base + self.layout.flags,
+                                        self._table([flags]).data_ptr(), 1, 16 * NB, side.cuda_stream)
+                side.synchronize()
+                print(f"[rank {self.rank}] ring stuck after {deadline}s: {stuck}; flags "
+                      f"{dict(zip(rs.FLAGS, flags.view(4, NB).tolist()))}", file=sys.stderr, flush=True)
+                raise RuntimeError("multi-GPU ring did not complete")
+            time.sleep(0.005)
+
     def _copy_ranges(self, full, table, n_dst, scatter):
         L.check(L.lib().bfly_copy_ranges(full, self._packed.data_ptr(), table, n_dst, self._ranges.data_ptr(),
                                          self._ranges.shape[0], self.esize, scatter, _stream_handle()))
@@ -321,8 +356,24 @@ class ShardedButterflyMerge:
                     dist.recv(self._packed, src=self.fb_owner)
                     self._copy_ranges(None, self._fb_table.data_ptr(), 1, 1)
             self._relay.wait_stream(cur)
-            for op in rs.round_ops(g, G, self.K, NB, self._round):
-                self._issue(op)
+            marks, window = [], []
+            for k in range(self.K):
+                for op in rs.chunk_ops(g, G, self.K, NB, self._round, k):
+                    self._issue(op)
+                    if self.debug:
+                        ev = torch.cuda.Event()
+                        ev.record(cur if op[1] == "C" else self._relay)
+                        marks.append((op, ev))
+                # bounded run-ahead: never more than WINDOW chunks queued per stream
+                done = (torch.cuda.Event(), torch.cuda.Event())
+                done[0].record(cur)
+                done[1].record(self._relay)
+                window.append(done)
+                if len(window) > WINDOW:
+                    self._host_wait(window.pop(0))
+            if self.debug == 1:
+                self._watch(marks)
+            self._marks = marks
             cur.wait_stream(self._relay)
         self._round += 1
 
@@ -345,6 +396,8 @@ class ShardedButterflyMerge:
         elif self.want_merged:
             self.merged.copy_(self.job.merged)
         unpack_results(self._res, self.entries, self.source, self.status, self.flagged)
+        if self.debug == 2 and G > 1:
+            self._watch(self._marks)
         return self
 
     def launches_per_run(self) -> int:

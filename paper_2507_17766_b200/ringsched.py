@@ -53,8 +53,8 @@ def slot(round_index: int, K: int, k: int, NB: int) -> int:
     return (round_index * K + k) % NB
 
 
-def round_ops(g: int, G: int, K: int, NB: int, round_index: int) -> list:
-    """Ops of rank g for one round, in issue order.  Each op is a tuple:
+def chunk_ops(g: int, G: int, K: int, NB: int, round_index: int, k: int) -> list:
+    """Ops of rank g for chunk k of one round (stream "C" ops, then stream "R" ops):
     ("wait", stream, flag, slot, value)         wait on a flag in MY region
     ("write", stream, peer, flag, slot, value)   write a flag in peer's region
     ("chain", stream, k, slot, dst_rank)
@@ -66,41 +66,46 @@ def round_ops(g: int, G: int, K: int, NB: int, round_index: int) -> list:
     if NB < 2:
         raise ValueError("need at least 2 inbox slots")
     Z = G - 1
+    s = slot(round_index, K, k, NB)
+    v = value(round_index, K, k)
+    first_use = round_index * K + k < NB  # slot never filled before
+    prev = (v - NB) & 0xFFFFFFFF
     ops = []
-    for k in range(K):
-        s = slot(round_index, K, k, NB)
-        v = value(round_index, K, k)
-        first_use = round_index * K + k < NB  # slot never filled before
-        if g < Z:
-            if g > 0:
-                ops.append(("wait", "C", "acc_ready", s, v))
-            if not first_use:
-                ops.append(("wait", "C", "acc_free", s, (v - NB) & 0xFFFFFFFF))
-            ops.append(("chain", "C", k, s, g + 1))
-            ops.append(("write", "C", g + 1, "acc_ready", s, v))
-            if g > 0:
-                ops.append(("write", "C", g - 1, "acc_free", s, v))
-        else:
-            ops.append(("wait", "C", "acc_ready", s, v))
-            if not first_use:
-                ops.append(("wait", "C", "fin_free", s, (v - NB) & 0xFFFFFFFF))
-            ops.append(("reduce", "C", k, s, 0))
-            ops.append(("write", "C", 0, "fin_ready", s, v))
-            ops.append(("write", "C", Z - 1, "acc_free", s, v))
     if g < Z:
+        if g > 0:
+            ops.append(("wait", "C", "acc_ready", s, v))
+        if not first_use:
+            ops.append(("wait", "C", "acc_free", s, prev))
+        ops.append(("chain", "C", k, s, g + 1))
+        ops.append(("write", "C", g + 1, "acc_ready", s, v))
+        if g > 0:
+            ops.append(("write", "C", g - 1, "acc_free", s, v))
         succ, pred = relay_succ(g, Z), relay_pred(g, Z)
-        for k in range(K):
-            s = slot(round_index, K, k, NB)
-            v = value(round_index, K, k)
-            first_use = round_index * K + k < NB
-            ops.append(("wait", "R", "fin_ready", s, v))
-            if succ is not None and not first_use:
-                ops.append(("wait", "R", "fin_free", s, (v - NB) & 0xFFFFFFFF))
-            ops.append(("fanout", "R", k, s, succ))
-            if succ is not None:
-                ops.append(("write", "R", succ, "fin_ready", s, v))
-            ops.append(("write", "R", pred, "fin_free", s, v))
+        ops.append(("wait", "R", "fin_ready", s, v))
+        if succ is not None and not first_use:
+            ops.append(("wait", "R", "fin_free", s, prev))
+        ops.append(("fanout", "R", k, s, succ))
+        if succ is not None:
+            ops.append(("write", "R", succ, "fin_ready", s, v))
+        ops.append(("write", "R", pred, "fin_free", s, v))
+    else:
+        ops.append(("wait", "C", "acc_ready", s, v))
+        if not first_use:
+            ops.append(("wait", "C", "fin_free", s, prev))
+        ops.append(("reduce", "C", k, s, 0))
+        ops.append(("write", "C", 0, "fin_ready", s, v))
+        ops.append(("write", "C", Z - 1, "acc_free", s, v))
     return ops
+
+
+def round_ops(g: int, G: int, K: int, NB: int, round_index: int) -> list:
+    """All ops of rank g for one round, chunk by chunk (see chunk_ops).
+
+    The executor issues them chunk by chunk and keeps at most a few chunks in
+    flight per stream: a host that enqueued far ahead could block inside a
+    launch on a stream stalled at a wait, before issuing the other stream's ops
+    the wait depends on."""
+    return [op for k in range(K) for op in chunk_ops(g, G, K, NB, round_index, k)]
 
 
 def geq(flag_value: int, v: int) -> bool:
