@@ -147,6 +147,15 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
  * kernels that move the running sums, so transfers overlap the HBM stream. */
 int bfly_set_max_ctas(int32_t max_ctas);
 
+/* Upload n fp64 host payloads of P elements (pageable or pinned) as fp32 wire
+ * values ("<f4", butterfly.py:213) into the device buffers d_wire[i]: `threads`
+ * host threads (0 = all cores) convert into a pinned staging ring while earlier
+ * slots are copied, so conversion and PCIe overlap.  Returns when the last copy
+ * has been issued on `stream` (the host payloads may be reused after the
+ * stream reaches that point). */
+int bfly_upload_wire(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
+                     int32_t threads, void* stream);
+
 /* ---- peer memory for the multi-GPU merge (one process per GPU, one node) ---- */
 /* cudaMalloc a zero-filled region and export its CUDA IPC handle (64 bytes). */
 int bfly_ipc_alloc(size_t bytes, void** d_ptr, uint8_t handle[64]);

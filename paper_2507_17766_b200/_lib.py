@@ -44,6 +44,7 @@ EXPORTS = (
     "bfly_ipc_free",
     "bfly_stream_wait_value",
     "bfly_stream_write_value",
+    "bfly_upload_wire",
 )
 
 
@@ -130,6 +131,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_ipc_free.argtypes = [vp]
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
+    L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)

@@ -19,6 +19,7 @@ There is no CPU fallback: without a CUDA device these functions raise.
 
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 from dataclasses import dataclass, field
@@ -258,8 +259,24 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
 
     # -- device merge ------------------------------------------------------
     reps = [None] * n
-    for m in alive:
-        reps[m], _ = _payload_to_device(payloads[miners[m]], dev)
+    host_f64 = [m for m in alive if not isinstance(payloads[miners[m]], torch.Tensor)]
+    if host_f64 and len(host_f64) == len(alive):
+        # host payloads: the upload stage's "<f4" serialisation (butterfly.py:213) runs on
+        # host threads into pinned staging, overlapped with the H2D copies (bfly_upload_wire)
+        hosts = [np.ascontiguousarray(np.asarray(payloads[miners[m]], dtype=np.float64)).reshape(-1) for m in alive]
+        wire = [torch.empty(P, dtype=torch.float32, device=dev) for _ in alive]
+        h_ptrs = (ctypes.c_void_p * len(alive))(*[h.ctypes.data for h in hosts])
+        d_ptrs = (ctypes.c_void_p * len(alive))(*[t.data_ptr() for t in wire])
+        L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _stream_handle()))
+        for m, t in zip(alive, wire):
+            reps[m] = t
+        unmerged_possible = len(failed) >= 2 or bool(descriptors) or bool(callables)
+        if fallback is None and unmerged_possible:
+            # unmerged shards fall back to the lowest alive *fp64* payload (butterfly.py:270-271)
+            fallback = hosts[0]
+    else:
+        for m in alive:
+            reps[m], _ = _payload_to_device(payloads[miners[m]], dev)
     if alive:
         kinds = {reps[m].dtype for m in alive}
         if len(kinds) != 1:

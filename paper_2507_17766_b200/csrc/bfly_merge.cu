@@ -75,6 +75,12 @@ struct DF32 {
     for (int k = 0; k < 8; ++k) v.w[k] = __float_as_uint(__double2float_rn(m[k]));
     return v;
   }
+  __device__ static void store8(void* p, int64_t e0, const double* v) {  // 32 B, aligned
+    V8 w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w.w[k] = __float_as_uint(__double2float_rn(v[k]));
+    st_stream((float*)p + e0, w);
+  }
 };
 
 // bf16 replicas, fp32 accumulation (extension, BASELINE config 4).
@@ -110,6 +116,14 @@ struct DBF16 {
     for (int k = 0; k < 8; ++k) v.w[k] = (uint32_t)to_bits(m[2 * k]) | ((uint32_t)to_bits(m[2 * k + 1]) << 16);
     return v;
   }
+  __device__ static void store8(void* p, int64_t e0, const double* v) {  // 16 B, aligned
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = (uint32_t)to_bits(__double2float_rn(v[2 * k])) |
+             ((uint32_t)to_bits(__double2float_rn(v[2 * k + 1])) << 16);
+    *reinterpret_cast<uint4*>((unsigned short*)p + e0) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 };
 
 // fp64 payloads rounded to the fp32 wire on load (astype("<f4"), butterfly.py:213,230).
@@ -138,6 +152,10 @@ struct DF64W {
       v.w[2 * k + 1] = (uint32_t)__double2hiint(m[k]);
     }
     return v;
+  }
+  __device__ static void store8(void* p, int64_t e0, const double* v) {  // 64 B, aligned
+    st_f64x4((double*)p + e0, v[0], v[1], v[2], v[3]);
+    st_f64x4((double*)p + e0 + 4, v[4], v[5], v[6], v[7]);
   }
 };
 
@@ -554,6 +572,66 @@ __device__ __forceinline__ double score_of(const PairStat& s, double tol) {
   return c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
 }
 
+// Copies of eight consecutive elements e0..e0+7 (e0 % 8 == 0): one Philox4x64
+// call yields four noise words, so a group needs two calls per noisy assignee.
+__device__ __forceinline__ void corrupt8(const bfly_corruption_t& c, const double* m, int64_t e0, unsigned valid,
+                                         const double* host_copies, int slot, int64_t P, double* out) {
+  switch (c.kind) {
+    case BFLY_CORR_ADD:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = __dadd_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_SCALE:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = __dmul_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_NOISE:
+    case BFLY_CORR_NOISE_ADD: {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        Philox4x64 ctr;
+        ctr.v[0] = (uint64_t)(e0 >> 2) + h + 1;  // word e lives in block e/4 (+1: numpy pre-increment)
+        ctr.v[1] = ctr.v[2] = ctr.v[3] = 0;
+        const Philox4x64 o = philox4x64_10(ctr, c.key0, c.key1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double noise = __dmul_rn(c.a, noise_unit(o.v[j]));
+          out[4 * h + j] = c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(m[4 * h + j], noise);
+        }
+      }
+      return;
+    }
+    case BFLY_CORR_HOST:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = (valid >> i) & 1 ? host_copies[(int64_t)slot * P + e0 + i] : 0.0;
+      return;
+    default:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = m[i];
+  }
+}
+
+// ws[e0..e0+7]: one 64-byte vector when the group is whole, masked scalars otherwise
+__device__ __forceinline__ unsigned load_group(const double* ws, int64_t e0, int64_t lo, int64_t hi, double* m) {
+  unsigned valid = 0;
+  if (e0 >= lo && e0 + 8 <= hi) {
+    valid = 0xff;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(m[4 * h]), "=d"(m[4 * h + 1]), "=d"(m[4 * h + 2]), "=d"(m[4 * h + 3])
+                   : "l"(ws + e0 + 4 * h));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool in = e0 + i >= lo && e0 + i < hi;
+      m[i] = in ? ws[e0 + i] : 0.0;
+      valid |= (unsigned)in << i;
+    }
+  }
+  return valid;
+}
+
 __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
   const int64_t s = blockIdx.x;
   if (p.cls[s] != kSpecial) return;
@@ -567,18 +645,24 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
     alive[k] = !p.failed[mem[k]];
     c[k] = p.corr[mem[k]];
   }
+  const int64_t g_lo = lo & ~(int64_t)7;
   for (int a = 0; a < p.r; ++a)
     for (int b = a + 1; b < p.r; ++b) {
       if (!alive[a] || !alive[b]) continue;
       PairStat st{0.0, 0.0, 0.0, 0.0};
-      for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
-        const double m = p.ws[e];
-        const double x = corrupt_value(c[a], m, e, p.host_copies, a, p.P);
-        const double y = corrupt_value(c[b], m, e, p.host_copies, b, p.P);
-        st.mx = max_nan(st.mx, fabs(__dsub_rn(x, y)));
-        st.ab = fma(x, y, st.ab);
-        st.aa = fma(x, x, st.aa);
-        st.bb = fma(y, y, st.bb);
+      for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
+        double m[8], x[8], y[8];
+        const unsigned valid = load_group(p.ws, e0, lo, hi, m);
+        corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
+        corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (!((valid >> i) & 1)) continue;
+          st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
+          st.ab = fma(x[i], y[i], st.ab);
+          st.aa = fma(x[i], x[i], st.aa);
+          st.bb = fma(y[i], y[i], st.bb);
+        }
       }
       st = block_combine(st);
       if (threadIdx.x == 0) {
@@ -682,9 +766,12 @@ __global__ void k_entries3(Params p) {
 
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
+  extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
   const int64_t s = blockIdx.x;
   const uint8_t c = p.cls[s];
   if (c == kFast) return;
+  void** s_dst = const_cast<void**>(s_ptr);
+  const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, (uintptr_t)p.merged);
   const int64_t lo = p.bnd.start(s) + (int64_t)blockIdx.y * kChunk;
   const int64_t hi_s = p.bnd.start(s) + p.bnd.len(s);
   const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
@@ -696,15 +783,41 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
       if (p.assign[s * p.r + k] == src_m) slot = k;
     cd = p.corr[src_m];
   }
-  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
-    double v;
-    if (slot >= 0) v = corrupt_value(cd, p.ws[e], e, p.host_copies, slot, p.P);
-    else if (p.fallback) v = p.fallback[e];
-    else if (p.fb_src) v = D::raw(p.fb_src, e);  // lowest alive upload (butterfly.py:270-271)
-    else if (p.n_alive > 0) v = D::raw(p.src[0], e);
-    else v = nan64();
-    if (p.merged) p.merged[e] = v;
-    for (int d = 0; d < p.n_dst; ++d) D::store(p.dst[d], e, v);
+  const void* fb_raw = p.fb_src ? p.fb_src : (p.n_alive > 0 ? p.src[0] : nullptr);
+  for (int64_t e0 = (lo & ~(int64_t)7) + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
+    double v[8];
+    unsigned valid;
+    if (slot >= 0) {
+      double m[8];
+      valid = load_group(p.ws, e0, lo, hi, m);
+      corrupt8(cd, m, e0, valid, p.host_copies, slot, p.P, v);
+    } else {
+      valid = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t e = e0 + i;
+        const bool in = e >= lo && e < hi;
+        valid |= (unsigned)in << i;
+        if (!in) v[i] = 0.0;
+        else if (p.fallback) v[i] = p.fallback[e];
+        else if (fb_raw) v[i] = D::raw(fb_raw, e);  // lowest alive upload (butterfly.py:270-271)
+        else v[i] = nan64();
+      }
+    }
+    if (valid == 0xff && aligned) {
+      if (p.merged) {
+        st_f64x4(p.merged + e0, v[0], v[1], v[2], v[3]);
+        st_f64x4(p.merged + e0 + 4, v[4], v[5], v[6], v[7]);
+      }
+      for (int d = 0; d < p.n_dst; ++d) D::store8(s_dst[d], e0, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (!((valid >> i) & 1)) continue;
+        if (p.merged) p.merged[e0 + i] = v[i];
+        for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e0 + i, v[i]);
+      }
+    }
   }
 }
 
@@ -813,7 +926,9 @@ static void launch_reduce(const Params& p, cudaStream_t st, int grid_per_sm = 8)
 
 template <class D>
 static void launch_apply(const Params& p, cudaStream_t st) {
-  k_apply<D><<<dim3((unsigned)p.S, (unsigned)p.cps), kThreads, 0, st>>>(p);
+  const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_apply<D><<<dim3((unsigned)p.S, (unsigned)p.cps), kThreads, smem, st>>>(p);
 }
 
 extern "C" {
