@@ -38,6 +38,7 @@ EXPORTS = (
     "bfly_fanout",
     "bfly_copy_ranges",
     "bfly_set_max_ctas",
+    "bfly_set_chain_bulk",
     "bfly_ipc_alloc",
     "bfly_ipc_open",
     "bfly_ipc_close",
@@ -45,6 +46,8 @@ EXPORTS = (
     "bfly_stream_wait_value",
     "bfly_stream_write_value",
     "bfly_upload_wire",
+    "bfly_ring_round",
+    "bfly_ring_ops",
 )
 
 
@@ -95,6 +98,33 @@ class MergeArgs(ctypes.Structure):
     ]
 
 
+class RingDesc(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("k_chunks", ctypes.c_int32),
+        ("nb", ctypes.c_int32),
+        ("payload_len", ctypes.c_int64),
+        ("chunk", ctypes.c_int64),
+        ("dtype", ctypes.c_int32),
+        ("esize", ctypes.c_int32),
+        ("peer_base", ctypes.c_void_p),
+        ("off_acc", ctypes.c_int64),
+        ("off_fin", ctypes.c_int64),
+        ("off_flags", ctypes.c_int64),
+        ("d_src_table", ctypes.c_void_p),
+        ("n_src", ctypes.c_int32),
+        ("fan_n", ctypes.c_int32),
+        ("fan_tables", ctypes.c_void_p),
+        ("merge_args", ctypes.POINTER(MergeArgs)),
+        ("reduce_tables", ctypes.c_void_p),
+        ("reduce_n", ctypes.c_int32),
+        ("window", ctypes.c_int32),
+        ("stream_c", ctypes.c_void_p),
+        ("stream_r", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 
@@ -124,6 +154,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_chain_step.argtypes = [vp, i32, i32, vp, vp, i64, i64, vp]
     L.bfly_fanout.argtypes = [vp, vp, i32, i64, vp]
     L.bfly_set_max_ctas.argtypes = [i32]
+    L.bfly_set_chain_bulk.argtypes = [i32]
     u32 = ctypes.c_uint32
     L.bfly_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
     L.bfly_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
@@ -132,6 +163,8 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
+    L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
+    L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, vp, i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)

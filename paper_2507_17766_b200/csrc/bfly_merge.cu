@@ -439,15 +439,21 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
 // over this GPU's alive replicas, for elements [begin, end); the acc buffers are
 // chunk-local.  Carrying the running fp64 sum from GPU to GPU keeps the
 // reference's ascending-miner order, so the multi-GPU mean is bit-exact.
-template <class D>
+template <class D, bool BULK>
 __global__ void __launch_bounds__(kThreads) k_chain(const void* const* src, int n_src, const double* acc_in,
                                                     double* acc_out, int64_t begin, int64_t end) {
-  extern __shared__ __align__(16) const void* s_ptr[];
-  const bool aligned = stage_pointers(s_ptr, nullptr, src, n_src, nullptr, 0,
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const void** s_src = reinterpret_cast<const void**>(smem_raw);
+  const bool aligned = stage_pointers(s_src, nullptr, src, n_src, nullptr, 0,
                                       (uintptr_t)acc_in | (uintptr_t)acc_out);
   constexpr int K = D::K;
   constexpr int TILE = kThreads * K;
   using Acc = typename D::Acc;
+  // BULK: each tile of sums is staged in shared memory (double buffer) and leaves
+  // with one TMA bulk store (cp.async.bulk.global.shared::cta) — large NVLink
+  // writes when acc_out is a peer GPU's inbox, issued by one thread
+  double* stage = reinterpret_cast<double*>(smem_raw + ((sizeof(void*) * n_src + 127) & ~(size_t)127));
+  int buf = 0, issued = 0;
   const int64_t tile_lo = begin / TILE, tile_hi = (end + TILE - 1) / TILE;
   for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
     const int64_t t0 = max(tile * TILE, begin);
@@ -462,18 +468,40 @@ __global__ void __launch_bounds__(kThreads) k_chain(const void* const* src, int 
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = D::zero();
       }
-      accumulate_vec<D>(acc, s_ptr, n_src, vidx);
+      accumulate_vec<D>(acc, s_src, n_src, vidx);
+      if constexpr (BULK) {
+        if (threadIdx.x == 0 && issued >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();  // stage[buf] no longer read by the store issued two tiles ago
+        double* sb = stage + buf * TILE + threadIdx.x * K;
 #pragma unroll
-      for (int k = 0; k < K; k += 4)
-        st_f64x4(acc_out + (e0 - begin) + k, (double)acc[k], (double)acc[k + 1], (double)acc[k + 2],
-                 (double)acc[k + 3]);
+        for (int k = 0; k < K; ++k) sb[k] = (double)acc[k];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(stage + buf * TILE);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                       "cp.async.bulk.commit_group;" ::"l"(acc_out + (t0 - begin)),
+                       "r"(sa), "r"((unsigned)(TILE * sizeof(double)))
+                       : "memory");
+        }
+        ++issued;
+        buf ^= 1;
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; k += 4)
+          st_f64x4(acc_out + (e0 - begin) + k, (double)acc[k], (double)acc[k + 1], (double)acc[k + 2],
+                   (double)acc[k + 3]);
+      }
     } else {
       for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
         Acc acc = acc_in ? (Acc)acc_in[e - begin] : D::zero();
-        for (int q = 0; q < n_src; ++q) acc = D::add(acc, D::load(s_ptr[q], e));
+        for (int q = 0; q < n_src; ++q) acc = D::add(acc, D::load(s_src[q], e));
         acc_out[e - begin] = (double)acc;
       }
     }
+  }
+  if constexpr (BULK) {
+    if (threadIdx.x == 0 && issued) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 }
 
@@ -905,6 +933,7 @@ using namespace bfly;
 // Optional cap on the CTAs of the streaming kernels (bfly_set_max_ctas): with one
 // resident CTA per SM it leaves SMs free for concurrent NCCL kernels.
 static int g_max_ctas = 0;
+static int g_chain_bulk = 1;  // k_chain stores through TMA bulk copies (bfly_set_chain_bulk)
 static int64_t cap_grid(int64_t grid) {
   if (g_max_ctas > 0 && grid > g_max_ctas) grid = g_max_ctas;
   return grid < 1 ? 1 : grid;
@@ -1080,19 +1109,25 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
     return fail(BFLY_E_INVALID_ARG, "bad chain-step arguments");
   if (end == begin) return BFLY_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = sizeof(void*) * (size_t)n_src;
-  auto go = [&](auto kern, int K) {
+  auto go = [&](auto kern, int K, bool bulk) {
     const int64_t tile = (int64_t)kThreads * K;
     int64_t grid = (end + tile - 1) / tile - begin / tile;
     if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
     grid = cap_grid(grid);
+    size_t smem = (sizeof(void*) * (size_t)n_src + 127) & ~(size_t)127;
+    if (bulk) smem += 2 * sizeof(double) * (size_t)tile;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, kThreads, smem, st>>>(d_src, n_src, d_acc_in, d_acc_out, begin, end);
   };
+  const bool bulk = g_chain_bulk != 0;
   switch (dtype) {
-    case BFLY_F32: go(k_chain<DF32>, DF32::K); break;
-    case BFLY_BF16: go(k_chain<DBF16>, DBF16::K); break;
-    case BFLY_F64WIRE: go(k_chain<DF64W>, DF64W::K); break;
+    case BFLY_F32: bulk ? go(k_chain<DF32, true>, DF32::K, true) : go(k_chain<DF32, false>, DF32::K, false); break;
+    case BFLY_BF16:
+      bulk ? go(k_chain<DBF16, true>, DBF16::K, true) : go(k_chain<DBF16, false>, DBF16::K, false);
+      break;
+    case BFLY_F64WIRE:
+      bulk ? go(k_chain<DF64W, true>, DF64W::K, true) : go(k_chain<DF64W, false>, DF64W::K, false);
+      break;
     default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
   }
   cudaError_t e = cudaGetLastError();
@@ -1123,6 +1158,11 @@ int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bfly_copy_ranges launch");
+  return BFLY_OK;
+}
+
+int bfly_set_chain_bulk(int32_t on) {
+  g_chain_bulk = on ? 1 : 0;
   return BFLY_OK;
 }
 

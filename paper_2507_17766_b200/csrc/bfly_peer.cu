@@ -14,6 +14,7 @@
 #include <string.h>
 
 #include <mutex>
+#include <vector>
 
 #include "bfly_internal.cuh"
 
@@ -102,6 +103,157 @@ int bfly_stream_write_value(uint32_t* d_flag, uint32_t value, void* stream) {
   CUresult r = g_write32((CUstream)stream, (CUdeviceptr)d_flag, value, CU_STREAM_WRITE_VALUE_DEFAULT);
   if (r != CUDA_SUCCESS) return fail(BFLY_E_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
   return BFLY_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Native executor of one multi-GPU ring round.  The op lists are the ones of
+// paper_2507_17766_b200/ringsched.py (chunk_ops); bfly_ring_ops exports them
+// so tests/test_ringsched.py checks both generators agree op for op.
+// ---------------------------------------------------------------------------
+
+namespace bfly {
+
+enum RingOp : int32_t { kOpWait = 0, kOpWrite = 1, kOpChain = 2, kOpReduce = 3, kOpFanout = 4 };
+enum RingFlag : int32_t { kAccReady = 0, kAccFree = 1, kFinReady = 2, kFinFree = 3 };
+
+struct Op {
+  int32_t kind, stream;  // stream 0 = C (chain/reduce), 1 = R (relay)
+  int32_t peer, flag, slot, k;
+  uint32_t value;
+};
+
+// The ops of rank g for chunk k (ringsched.chunk_ops, same order).
+static int chunk_ops(int g, int G, int K, int NB, uint32_t round_index, int k, Op* out) {
+  const int Z = G - 1;
+  const uint64_t idx = (uint64_t)round_index * (uint64_t)K + (uint64_t)k;
+  const int s = (int)(idx % (uint64_t)NB);
+  const uint32_t v = (uint32_t)(idx + 1);
+  const bool first_use = idx < (uint64_t)NB;
+  const uint32_t prev = v - (uint32_t)NB;
+  int n = 0;
+  auto add = [&](int kind, int st, int peer, int flag, uint32_t val) {
+    out[n++] = Op{kind, st, peer, flag, s, k, val};
+  };
+  if (g < Z) {
+    if (g > 0) add(kOpWait, 0, g, kAccReady, v);
+    if (!first_use) add(kOpWait, 0, g, kAccFree, prev);
+    add(kOpChain, 0, g + 1, -1, 0);
+    add(kOpWrite, 0, g + 1, kAccReady, v);
+    if (g > 0) add(kOpWrite, 0, g - 1, kAccFree, v);
+    const int succ = g + 1 < Z ? g + 1 : -1;
+    const int pred = g == 0 ? Z : g - 1;
+    add(kOpWait, 1, g, kFinReady, v);
+    if (succ >= 0 && !first_use) add(kOpWait, 1, g, kFinFree, prev);
+    add(kOpFanout, 1, succ, -1, 0);
+    if (succ >= 0) add(kOpWrite, 1, succ, kFinReady, v);
+    add(kOpWrite, 1, pred, kFinFree, v);
+  } else {
+    add(kOpWait, 0, g, kAccReady, v);
+    if (!first_use) add(kOpWait, 0, g, kFinFree, prev);
+    add(kOpReduce, 0, 0, -1, 0);
+    add(kOpWrite, 0, 0, kFinReady, v);
+    add(kOpWrite, 0, Z - 1, kAccFree, v);
+  }
+  return n;
+}
+
+}  // namespace bfly
+
+extern "C" {
+
+int bfly_ring_ops(int32_t g, int32_t G, int32_t K, int32_t NB, uint32_t round_index, int32_t* out, int32_t cap) {
+  if (G < 2 || NB < 2 || g < 0 || g >= G || K < 0) return -1;
+  int n = 0;
+  Op ops[16];
+  for (int k = 0; k < K; ++k) {
+    const int m = chunk_ops(g, G, K, NB, round_index, k, ops);
+    for (int i = 0; i < m; ++i) {
+      if (n + 1 > cap) return -1;
+      int32_t* r = out + 7 * n;
+      r[0] = ops[i].kind;
+      r[1] = ops[i].stream;
+      r[2] = ops[i].peer;
+      r[3] = ops[i].flag;
+      r[4] = ops[i].slot;
+      r[5] = ops[i].k;
+      r[6] = (int32_t)ops[i].value;
+      ++n;
+    }
+  }
+  return n;
+}
+
+int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
+  if (!d || d->world < 2 || d->nb < 2 || d->k_chunks < 1) return fail(BFLY_E_INVALID_ARG, "bad ring descriptor");
+  int rc = load_driver_ops();
+  if (rc) return rc;
+  const int g = d->rank, G = d->world, K = d->k_chunks, NB = d->nb;
+  const bool last = g == G - 1;
+  cudaStream_t sc = (cudaStream_t)d->stream_c, sr = (cudaStream_t)d->stream_r;
+  // run-ahead throttle: the host never has more than `window` chunks queued per
+  // stream; a launch blocked on a full queue behind a wait must not keep the host
+  // from issuing the other stream's ops that wait depends on
+  const int W = d->window > 0 ? d->window : 4;
+  std::vector<cudaEvent_t> ev(2 * (W + 1));
+  for (auto& e : ev) {
+    cudaError_t ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (ce != cudaSuccess) return cuda_fail(ce, "ring event");
+  }
+  auto flag_addr = [&](int owner, int flag, int s) -> CUdeviceptr {
+    return (CUdeviceptr)(d->peer_base[owner] + (uint64_t)d->off_flags + (uint64_t)(flag * NB + s) * 4);
+  };
+  bfly_merge_args_t args;
+  if (last) args = *d->merge_args;
+  Op ops[16];
+  int result = BFLY_OK;
+  for (int k = 0; k < K && result == BFLY_OK; ++k) {
+    const int64_t b = (int64_t)k * d->chunk;
+    const int64_t e = b + d->chunk < d->payload_len ? b + d->chunk : d->payload_len;
+    const int m = chunk_ops(g, G, K, NB, round_index, k, ops);
+    for (int i = 0; i < m && result == BFLY_OK; ++i) {
+      const Op& o = ops[i];
+      cudaStream_t st = o.stream == 0 ? sc : sr;
+      const int s = o.slot;
+      if (o.kind == kOpWait) {
+        const unsigned fl = CU_STREAM_WAIT_VALUE_GEQ | (g_flush_supported ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+        if (g_wait32((CUstream)st, flag_addr(g, o.flag, s), o.value, fl) != CUDA_SUCCESS)
+          result = fail(BFLY_E_CUDA, "ring wait");
+      } else if (o.kind == kOpWrite) {
+        if (g_write32((CUstream)st, flag_addr(o.peer, o.flag, s), o.value, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+            CUDA_SUCCESS)
+          result = fail(BFLY_E_CUDA, "ring write");
+      } else if (o.kind == kOpChain) {  // sums stored into the next GPU's inbox (TMA bulk stores)
+        const double* acc_in =
+            g > 0 ? (const double*)(d->peer_base[g] + d->off_acc + (uint64_t)s * d->chunk * 8) : nullptr;
+        double* acc_out = (double*)(d->peer_base[o.peer] + d->off_acc + (uint64_t)s * d->chunk * 8);
+        result = bfly_chain_step(d->d_src_table, d->n_src, d->dtype, acc_in, acc_out, b, e, st);
+      } else if (o.kind == kOpReduce) {
+        args.phase = BFLY_PHASE_REDUCE;
+        args.d_acc_in = (const double*)(d->peer_base[g] + d->off_acc + (uint64_t)s * d->chunk * 8);
+        args.elem_begin = b;
+        args.elem_end = e;
+        args.d_dst = (void* const*)d->reduce_tables[(int64_t)k * NB + s];
+        args.n_dst = d->reduce_n;
+        result = bfly_merge(&args, st);
+      } else if (o.kind == kOpFanout) {
+        const void* src = (const void*)(d->peer_base[g] + d->off_fin + (uint64_t)s * d->chunk * d->esize);
+        result = bfly_fanout(src, (void* const*)d->fan_tables[(int64_t)k * NB + s], d->fan_n,
+                             (e - b) * d->esize, st);
+      }
+    }
+    const int slot_ev = k % (W + 1);
+    cudaEventRecord(ev[2 * slot_ev], sc);
+    cudaEventRecord(ev[2 * slot_ev + 1], sr);
+    if (k >= W) {  // wait for chunk k - W on both streams before queueing more
+      const int old = (k - W) % (W + 1);
+      cudaEventSynchronize(ev[2 * old]);
+      cudaEventSynchronize(ev[2 * old + 1]);
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return result;
 }
 
 }  // extern "C"

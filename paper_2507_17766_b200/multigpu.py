@@ -8,7 +8,7 @@ makes the result reproducible, so the cross-GPU exchange keeps it exactly:
 
 1. **chain** — rank 0 sums its alive replicas into fp64 running sums; the
    chain kernel (``bfly_chain_step``) stores them *directly into rank 1's inbox*
-   over NVLink; rank 1 continues the same sum over its replicas and stores into
+   over NVLink (TMA bulk stores from shared memory); rank 1 continues the same sum over its replicas and stores into
    rank 2, and so on.  The payload is cut into chunks, so all ranks stream
    concurrently (chunk k on rank g while chunk k+1 is on rank g-1);
 2. **finish** — the last rank completes the sum, divides and scatters back into
@@ -248,6 +248,28 @@ class ShardedButterflyMerge:
                     if succ is not None:
                         views.append(lay.fin_slot(self._peer[succ], s))
                     self._fan_tables[k, s] = self._table(views)
+        # descriptor of the native executor (bfly_ring_round)
+        d = L.RingDesc()
+        d.rank, d.world, d.k_chunks, d.nb = g, self.world, self.K, NB
+        d.payload_len, d.chunk, d.dtype, d.esize = self.P, self.chunk, self.dtype, self.esize
+        self._peer_arr = (ctypes.c_uint64 * self.world)(*[self._peer[r] for r in range(self.world)])
+        d.peer_base = ctypes.cast(self._peer_arr, ctypes.c_void_p)
+        d.off_acc, d.off_fin, d.off_flags = lay.acc, lay.fin, lay.flags
+        d.d_src_table = self._src_table.data_ptr() if self._src_table is not None else None
+        d.n_src = len(self.local_alive)
+        d.window = WINDOW
+        if self.is_last:
+            self._red_arr = (ctypes.c_uint64 * (self.K * NB))(
+                *[self._reduce_tables[k, s].data_ptr() for k in range(self.K) for s in range(NB)])
+            d.reduce_tables = ctypes.cast(self._red_arr, ctypes.c_void_p)
+            d.reduce_n = len(self.local) + 1
+            d.merge_args = ctypes.pointer(self.job._args)
+        else:
+            self._fan_arr = (ctypes.c_uint64 * (self.K * NB))(
+                *[self._fan_tables[k, s].data_ptr() for k in range(self.K) for s in range(NB)])
+            d.fan_tables = ctypes.cast(self._fan_arr, ctypes.c_void_p)
+            d.fan_n = len(self.local) + (1 if rs.relay_succ(g, Z) is not None else 0)
+        self._desc = d
 
     def close(self):
         if self._peer:
@@ -357,7 +379,12 @@ class ShardedButterflyMerge:
                     self._copy_ranges(None, self._fb_table.data_ptr(), 1, 1)
             self._relay.wait_stream(cur)
             marks, window = [], []
-            for k in range(self.K):
+            if not self.debug:  # native executor: the whole round issued from C++
+                self._desc.stream_c = _stream_handle()
+                self._desc.stream_r = self._relay.cuda_stream
+                with torch.cuda.device(self.dev):
+                    L.check(L.lib().bfly_ring_round(ctypes.byref(self._desc), self._round & 0xFFFFFFFF))
+            for k in range(self.K if self.debug else 0):  # debug: the same ops issued from Python
                 for op in rs.chunk_ops(g, G, self.K, NB, self._round, k):
                     self._issue(op)
                     if self.debug:

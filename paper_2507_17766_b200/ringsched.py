@@ -30,6 +30,12 @@ relay (stream "R"), ranks 0..Z-1, ring Z -> 0 -> 1 -> ... -> Z-1:
 
 Every wait names an event of the same or an earlier chunk further up the chain
 or the ring, so the lists cannot deadlock (checked exhaustively by the tests).
+
+The chain kernel writes the running sums into the next GPU's inbox through TMA
+bulk stores from shared memory: measured on B200 (16 replicas x 16M elements),
+plain SM stores into peer memory stretched the kernel from 0.19 to 0.32 ms, a
+local write + copy-engine push pipeline cost 0.23 ms per chunk, the bulk stores
+0.21 ms with no extra HBM traffic (tools/peer_bw.py, profiles/).
 """
 
 from __future__ import annotations

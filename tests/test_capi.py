@@ -42,7 +42,10 @@ def test_struct_layout_matches_header(tmp_path):
 
     src = tmp_path / "layout.c"
     fields = [f for f, _ in _lib.MergeArgs._fields_]
+    rfields = [f for f, _ in _lib.RingDesc._fields_]
     body = "\n".join(f'  printf("{f} %zu\\n", offsetof(bfly_merge_args_t, {f}));' for f in fields)
+    body += "\n" + "\n".join(f'  printf("ring.{f} %zu\\n", offsetof(bfly_ring_desc_t, {f}));' for f in rfields)
+    body += '\n  printf("rsize %zu\\n", sizeof(bfly_ring_desc_t));'
     src.write_text(f"""#include <stdio.h>
 #include <stddef.h>
 #include "bfly.h"
@@ -60,6 +63,9 @@ int main(void) {{
     assert int(out["csize"]) == ctypes.sizeof(_lib.Corruption)
     for f in fields:
         assert int(out[f]) == getattr(_lib.MergeArgs, f).offset, f
+    assert int(out["rsize"]) == ctypes.sizeof(_lib.RingDesc)
+    for f in rfields:
+        assert int(out["ring." + f]) == getattr(_lib.RingDesc, f).offset, f
 
 
 @pytest.mark.parametrize("seed", [0, 1, 24, 2**63 - 1, 2**64 + 5, -7, 10**30])

@@ -170,3 +170,34 @@ def test_rejects_single_rank_and_one_slot():
         rs.round_ops(0, 1, 4, 2, 0)
     with pytest.raises(ValueError):
         rs.round_ops(0, 2, 4, 1, 0)
+
+
+@pytest.mark.parametrize("G", [2, 3, 5, 8])
+@pytest.mark.parametrize("K,NB,r", [(1, 2, 0), (7, 3, 0), (7, 3, 5), (13, 2, 2), (4, 3, (1 << 32) // 4 - 1)])
+def test_native_executor_issues_the_same_ops(G, K, NB, r):
+    """bfly_ring_round (C++) generates its ops with bfly_ring_ops' generator; it must
+    equal ringsched.round_ops, the schedule the simulator above verifies."""
+    import ctypes
+
+    from paper_2507_17766_b200 import _lib
+
+    kinds = {"wait": 0, "write": 1, "chain": 2, "reduce": 3, "fanout": 4}
+    streams = {"C": 0, "R": 1}
+    for g in range(G):
+        want = []
+        for op in rs.round_ops(g, G, K, NB, r):
+            kind, st = op[0], op[1]
+            if kind == "wait":
+                row = (kinds[kind], streams[st], g, rs.FLAGS.index(op[2]), op[3], -1, op[4])
+            elif kind == "write":
+                row = (kinds[kind], streams[st], op[2], rs.FLAGS.index(op[3]), op[4], -1, op[5])
+            else:
+                peer = -1 if op[4] is None else op[4]
+                row = (kinds[kind], streams[st], peer, -1, op[3], op[2], 0)
+            want.append(row)
+        buf = (ctypes.c_int32 * (7 * 16 * K))()
+        n = _lib.lib().bfly_ring_ops(g, G, K, NB, r & 0xFFFFFFFF, buf, 16 * K)
+        got = [tuple(buf[7 * i:7 * i + 7]) for i in range(n)]
+        got = [(a, b, c, d, e, (f if a >= 2 else -1), (h & 0xFFFFFFFF if a < 2 else 0)) for a, b, c, d, e, f, h in got]
+        want = [(a, b, c, d, e, f, h & 0xFFFFFFFF) for a, b, c, d, e, f, h in want]
+        assert got == want, (g, G, K, NB, r)
