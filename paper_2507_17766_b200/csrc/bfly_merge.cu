@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   const void** s_src = s_ptr;
   void** s_dst = const_cast<void**>(s_ptr + p.n_alive);
   const bool aligned = stage_pointers(s_src, s_dst, p.src, p.n_alive, p.dst, p.n_dst,
-                                      (uintptr_t)p.merged | (uintptr_t)p.acc_in);
+                                      (uintptr_t)p.merged | (uintptr_t)p.acc_in | (uintptr_t)p.ws);
   constexpr int K = D::K;
   constexpr int TILE = kThreads * K;
   using Acc = typename D::Acc;
@@ -384,13 +384,17 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
     const int64_t t0 = max(tile * TILE, p.ebeg);
     const int64_t t1 = min(tile * TILE + TILE, p.eend);
-    // uniform per tile: are all covered shards fast (and not width-1)?
+    // per tile: vector path unless a width-1 shard needs numpy's pairwise order;
+    // all-fast tiles skip the per-vector class lookup
     const int64_t s_lo = p.bnd.shard_of(t0), s_hi = p.bnd.shard_of(t1 - 1);
-    bool fast = aligned && (t1 - t0 == TILE);
-    for (int64_t s = s_lo; fast && s <= s_hi; ++s)
-      fast = p.cls[s] == kFast && !(may_width1 && s >= p.bnd.rem);
+    bool vec = aligned && (t1 - t0 == TILE);
+    bool all_fast = vec;
+    for (int64_t s = s_lo; vec && s <= s_hi; ++s) {
+      vec = !(may_width1 && s >= p.bnd.rem);
+      all_fast = all_fast && p.cls[s] == kFast;
+    }
 
-    if (fast) {
+    if (vec) {
       Acc acc[K];
       const int64_t vidx = t0 / K + threadIdx.x;  // 32-byte vector index
       const int64_t e0 = vidx * K;
@@ -403,14 +407,35 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
       accumulate_vec<D, U, NOU>(acc, s_src, p.n_alive, vidx);
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = D::mean(acc[k], p.n_div);
-      if (p.merged) {
+      const int64_t sa = all_fast ? 0 : p.bnd.shard_of(e0), sb = all_fast ? 0 : p.bnd.shard_of(e0 + K - 1);
+      const uint8_t c = all_fast ? (uint8_t)kFast : (sa == sb ? p.cls[sa] : (uint8_t)0xff);
+      if (c == kFast) {
+        if (p.merged) {
+#pragma unroll
+          for (int k = 0; k < K; k += 4)
+            st_f64x4(p.merged + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
+                     D::widen(acc[k + 3]));
+        }
+        const V8 out = D::pack(acc);
+        for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
+      } else if (c == kSpecial) {  // the mean waits in the workspace for k_stats / k_apply
 #pragma unroll
         for (int k = 0; k < K; k += 4)
-          st_f64x4(p.merged + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
+          st_f64x4(p.ws + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
                    D::widen(acc[k + 3]));
-      }
-      const V8 out = D::pack(acc);
-      for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
+      } else if (c == 0xff) {  // the vector straddles shards of different classes
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int64_t e = e0 + k;
+          const uint8_t ce = p.cls[p.bnd.shard_of(e)];
+          if (ce == kFast) {
+            if (p.merged) p.merged[e] = D::widen(acc[k]);
+            for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(acc[k]));
+          } else if (ce == kSpecial) {
+            p.ws[e] = D::widen(acc[k]);
+          }
+        }
+      }  // kLost: nothing to write, k_apply falls back
     } else {
       for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
         const int64_t s = p.bnd.shard_of(e);
