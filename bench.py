@@ -342,6 +342,10 @@ def run_multi(cfg, args, rank, world):
     total_ms = float(t.item())
     t_step = total_ms / args.steps / 1e3
     esize = BYTES[dtype]
+    if job.timing:
+        job.run()
+        print(f"[rank {rank}] phases (ms): " + json.dumps({k: round(v, 3) for k, v in job.timings.items()}),
+              file=sys.stderr, flush=True)
     nb = job.bytes_per_round()
     nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
     dist.all_reduce(nvl, op=dist.ReduceOp.MAX)

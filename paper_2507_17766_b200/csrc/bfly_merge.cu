@@ -530,17 +530,42 @@ __global__ void __launch_bounds__(kThreads) k_chain(const void* const* src, int 
   }
 }
 
-// Gather element ranges of `full` into `packed` (dir 0), or scatter `packed`
-// back into every `dst` (dir 1).  ranges[r] = {lo, hi, packed offset}.
-template <class T>
-__global__ void k_ranges(const T* full, T* packed, T* const* dst, int n_dst, const int64_t* ranges, int dir) {
-  const int64_t lo = ranges[3 * blockIdx.y], hi = ranges[3 * blockIdx.y + 1], off = ranges[3 * blockIdx.y + 2];
-  for (int64_t e = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < hi; e += (int64_t)gridDim.x * blockDim.x) {
-    if (dir == 0) {
-      packed[off + (e - lo)] = full[e];
-    } else {
-      const T v = packed[off + (e - lo)];
-      for (int d = 0; d < n_dst; ++d) dst[d][e] = v;
+// Gather element ranges of `full` into `packed` (SCATTER = false), or scatter
+// `packed` back into every `dst` (SCATTER = true).  ranges[r] = {lo, hi, packed
+// offset} in elements; the host keeps off = lo (mod 16 elements) so both sides of a
+// range share their 32-byte alignment and the body moves with 256-bit accesses.
+template <bool SCATTER>
+__global__ void __launch_bounds__(kThreads) k_ranges(const unsigned char* full, unsigned char* packed,
+                                                     unsigned char* const* dst, int n_dst, const int64_t* ranges,
+                                                     int esize) {
+  extern __shared__ __align__(16) const void* s_ptr[];
+  unsigned char** s_dst = reinterpret_cast<unsigned char**>(const_cast<void**>(s_ptr));
+  for (int q = threadIdx.x; q < n_dst; q += blockDim.x) s_dst[q] = dst[q];
+  __syncthreads();
+  const int64_t lo = ranges[3 * blockIdx.y] * esize, hi = ranges[3 * blockIdx.y + 1] * esize;
+  const int64_t off = ranges[3 * blockIdx.y + 2] * esize;
+  const unsigned char* src = SCATTER ? packed + off : full + lo;
+  const int64_t n = hi - lo;
+  const int nd = SCATTER ? n_dst : 1;
+  auto dst_at = [&](int d) -> unsigned char* { return SCATTER ? s_dst[d] + lo : packed + off; };
+  bool vec = true;
+  for (int d = 0; d < nd; ++d) vec = vec && ((((uintptr_t)dst_at(d)) ^ (uintptr_t)src) & 31) == 0;
+  int64_t head = vec ? (int64_t)((32 - ((uintptr_t)src & 31)) & 31) : n;
+  if (head > n) head = n;
+  const int64_t body = vec ? ((n - head) / 32) * 32 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < body / 32; v += stride) {
+    const V8 x = ld_stream(src + head + 32 * v);
+    for (int d = 0; d < nd; ++d) st_stream(dst_at(d) + head + 32 * v, x);
+  }
+  if (blockIdx.x == 0) {  // unaligned head and tail bytes
+    for (int64_t i = threadIdx.x; i < head; i += blockDim.x) {
+      const unsigned char x = src[i];
+      for (int d = 0; d < nd; ++d) dst_at(d)[i] = x;
+    }
+    for (int64_t i = head + body + threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned char x = src[i];
+      for (int d = 0; d < nd; ++d) dst_at(d)[i] = x;
     }
   }
 }
@@ -1165,22 +1190,16 @@ int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int
   if (n_ranges < 0 || n_ranges > 65535 || (elem_size != 2 && elem_size != 4 && elem_size != 8) || !d_packed ||
       (!scatter && !d_full) || (scatter && n_dst > 0 && !d_dst))
     return fail(BFLY_E_INVALID_ARG, "bad copy-ranges arguments");
-  if (n_ranges == 0) return BFLY_OK;
-  const dim3 grid(64, (unsigned)n_ranges);
+  if (n_ranges == 0 || (scatter && n_dst == 0)) return BFLY_OK;
+  const dim3 grid(32, (unsigned)n_ranges);
   cudaStream_t st = (cudaStream_t)stream;
-  switch (elem_size) {
-    case 2:
-      k_ranges<uint16_t><<<grid, 256, 0, st>>>((const uint16_t*)d_full, (uint16_t*)d_packed, (uint16_t* const*)d_dst,
-                                               n_dst, d_ranges, scatter);
-      break;
-    case 4:
-      k_ranges<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)d_full, (uint32_t*)d_packed, (uint32_t* const*)d_dst,
-                                               n_dst, d_ranges, scatter);
-      break;
-    default:
-      k_ranges<uint64_t><<<grid, 256, 0, st>>>((const uint64_t*)d_full, (uint64_t*)d_packed, (uint64_t* const*)d_dst,
-                                               n_dst, d_ranges, scatter);
-  }
+  const size_t smem = sizeof(void*) * (size_t)(n_dst > 0 ? n_dst : 1);
+  if (scatter)
+    k_ranges<true><<<grid, kThreads, smem, st>>>((const unsigned char*)d_full, (unsigned char*)d_packed,
+                                                 (unsigned char* const*)d_dst, n_dst, d_ranges, elem_size);
+  else
+    k_ranges<false><<<grid, kThreads, smem, st>>>((const unsigned char*)d_full, (unsigned char*)d_packed,
+                                                  (unsigned char* const*)d_dst, n_dst, d_ranges, elem_size);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "bfly_copy_ranges launch");
   return BFLY_OK;

@@ -156,6 +156,8 @@ class ShardedButterflyMerge:
         self.is_last = self.rank == G - 1
         self._round = 0
         self.debug = int(__import__("os").environ.get("BFLY_DEBUG_RING", "0"))
+        self.timing = bool(int(__import__("os").environ.get("BFLY_RING_TIMING", "0")))  # per-phase ms in .timings
+        self.timings = {}
         self._tables = []  # keeps the device pointer tables alive
         self._peer = None
 
@@ -166,6 +168,7 @@ class ShardedButterflyMerge:
         if runs:
             tab, off = [], 0
             for lo, hi in runs:
+                off += (lo - off) % 16  # same 32-byte alignment on both sides (vector copies)
                 tab.append((lo, hi, off))
                 off += hi - lo
             self._ranges = torch.tensor(tab, dtype=torch.int64, device=self.dev)
@@ -363,20 +366,31 @@ class ShardedButterflyMerge:
         G, g = self.world, self.rank
         last = G - 1
         cur = torch.cuda.current_stream(self.dev)
+        tm = [] if self.timing else None
+
+        def mark(name):
+            if tm is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(cur)
+                tm.append((name, ev))
+
+        mark("start")
+        fb_work = None
         if G == 1:
             for k in range(self.K):
                 b, e = self._bounds(k)
                 self.job.reduce_range(b, e)
         else:
-            # fallback values (the lowest alive miner's replica) for the late shards,
-            # moved before the relay overwrites that replica
+            # fallback values (the lowest alive miner's replica) for the late shards: packed
+            # before the relay overwrites that replica, sent while the ring runs
+            fb_work = None
             if self._needs_fb and self.fb_owner != last:
                 if g == self.fb_owner:
                     self._copy_ranges(self.local[self.alive[0] - self.offset].data_ptr(), None, 0, 0)
-                    dist.send(self._packed, dst=last)
+                    fb_work = dist.isend(self._packed, dst=last)
                 elif self.is_last:
-                    dist.recv(self._packed, src=self.fb_owner)
-                    self._copy_ranges(None, self._fb_table.data_ptr(), 1, 1)
+                    fb_work = dist.irecv(self._packed, src=self.fb_owner)
+            mark("fallback")
             self._relay.wait_stream(cur)
             marks, window = [], []
             if not self.debug:  # native executor: the whole round issued from C++
@@ -403,19 +417,28 @@ class ShardedButterflyMerge:
             self._marks = marks
             cur.wait_stream(self._relay)
         self._round += 1
+        mark("ring")
 
         # finish on the last rank, then per-shard results and the late shards
+        if G > 1 and fb_work is not None:
+            fb_work.wait()
+            if self.is_last:
+                self._copy_ranges(None, self._fb_table.data_ptr(), 1, 1)
         if self.is_last:
             self.job.run(L.PHASE_FINISH)
             pack_results(self.job.entries, self.job.source, self.job.status, self.job.flagged, self._res)
             if self.special_runs:
                 self._copy_ranges(self.local[0].data_ptr(), None, 0, 0)
+        mark("finish")
         if G > 1:
             dist.broadcast(self._res, src=last)
+            mark("results")
             if self.special_runs:
                 dist.broadcast(self._packed, src=last)
+                mark("late_bcast")
                 if not self.is_last:
                     self._copy_ranges(None, self._local_table.data_ptr(), len(self.local), 1)
+                mark("late_scatter")
             if self.want_merged:
                 if self.is_last:
                     self.merged.copy_(self.job.merged)
@@ -423,6 +446,10 @@ class ShardedButterflyMerge:
         elif self.want_merged:
             self.merged.copy_(self.job.merged)
         unpack_results(self._res, self.entries, self.source, self.status, self.flagged)
+        mark("end")
+        if tm is not None:
+            torch.cuda.synchronize(self.dev)
+            self.timings = {b[0]: a[1].elapsed_time(b[1]) for a, b in zip(tm, tm[1:])}
         if self.debug == 2 and G > 1:
             self._watch(self._marks)
         return self
