@@ -350,6 +350,7 @@ def run_multi(cfg, args, rank, world):
     nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
     dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
     launches = job.launches_per_run() * args.steps
+    e2e = None if args.no_e2e else run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0)
     if rank == 0:
         peaks = _peaks()
         hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -375,11 +376,64 @@ def run_multi(cfg, args, rank, world):
                          "t_roof_ms": t_roof * 1e3, "hbm_bytes_per_gpu": per_gpu_hbm,
                          "nvlink_bytes_in_per_gpu": float(nvl.item()),
                          "peaks": {"hbm_GBps": hbm_peak, "nvlink_GBps_per_direction": nvl_peak}},
-            "e2e": None, "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks,
+            "e2e": e2e, "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0):
+    """Multi-GPU end to end through the public API: every step each rank uploads its
+    miners' fp64 payloads from pinned host memory (bfly_upload_wire: fp32 wire
+    conversion on host threads + H2D), runs ShardedButterflyMerge, and reads the
+    round's results (status, flags, agreement matrix) back to the host.  Time is the
+    max over ranks."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_17766_b200 import _lib as L
+    from paper_2507_17766_b200.device import DevicePlan, _stream_handle
+    from paper_2507_17766_b200.multigpu import ShardedButterflyMerge
+
+    P = min(args.e2e_params, 1 << 26)
+    host = []
+    g = torch.Generator()
+    for i in range(n_local):
+        g.manual_seed(1000 + rank * n_local + i)
+        host.append(torch.empty(P, dtype=torch.float64, pin_memory=True).uniform_(-1.0, 1.0, generator=g))
+    wire = [torch.empty(P, dtype=torch.float32, device=dev) for _ in range(n_local)]
+    h_ptrs = (ctypes.c_void_p * n_local)(*[t.data_ptr() for t in host])
+    d_ptrs = (ctypes.c_void_p * n_local)(*[t.data_ptr() for t in wire])
+    threads = max(1, (os.cpu_count() or world) // world)
+    plan = DevicePlan(n, P, plan_seed, redundancy=r, device=dev)
+    job = ShardedButterflyMerge(wire, plan, chunk=min(args.chunk, 1 << 24))
+    outs = [torch.empty_like(t, device="cpu").pin_memory() for t in (job.status, job.flagged, job.entries)]
+
+    def step():
+        L.check(L.lib().bfly_upload_wire(h_ptrs, n_local, P, d_ptrs, threads, _stream_handle()))
+        job.run()
+        for o, d in zip(outs, (job.status, job.flagged, job.entries)):
+            o.copy_(d, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    dist.barrier()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = torch.tensor([(time.perf_counter() - t0) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dt = float(dt.item())
+    job.close()
+    return {"value": merge_bytes(n, P, 4) / dt / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": n_local * P * 4, "d2h_bytes_per_step": sum(o.numel() * o.element_size() for o in outs),
+            "params": P, "ms_per_step": dt * 1e3,
+            "path": "per rank: bfly_upload_wire(fp64 pinned host payloads) + ShardedButterflyMerge.run() + results D2H",
+            "bound": "host memory / PCIe of each rank"}
 
 
 def run_stages(cfg, args, rank, world):
