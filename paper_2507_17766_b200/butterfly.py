@@ -225,7 +225,7 @@ def _payload_to_device(x, dev) -> tuple[torch.Tensor, int]:
 def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reducer,
                    failures: frozenset | set = frozenset(), corruptions: dict | None = None,
                    fallback: np.ndarray | None = None, key_prefix: str = "merge",
-                   agreement_tolerance: float = 1e-6) -> MergeResult:
+                   agreement_tolerance: float = 1e-6, _device_merged: bool = False) -> MergeResult:
     """One merge round for a layer (butterfly.py:161-295), executed on the GPU.
 
     ``payloads`` maps miner id -> 1-D float64 payload (numpy; torch tensors on
@@ -313,10 +313,13 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     else:
         job.run(L.PHASE_ALL)
 
-    merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
-    merged_host.copy_(job.merged, non_blocking=True)
+    if _device_merged:  # stage glue (stage.py): the merged weights stay in HBM
+        merged = job.merged
+    else:
+        merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
+        merged_host.copy_(job.merged, non_blocking=True)
+        merged = merged_host.numpy()  # the array keeps the pinned tensor alive
     status_codes = job.status.cpu().numpy()
-    merged = merged_host.numpy()  # the array keeps the pinned tensor alive
     entries = job.entries.cpu().numpy()
     flagged_idx = np.flatnonzero(job.flagged.cpu().numpy())
     sources = job.source.cpu().numpy()
@@ -386,6 +389,10 @@ def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, me
         mt.bytes_downloaded += down
 
 
+def _host(x) -> np.ndarray:
+    return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+
+
 def _wire_bytes(src) -> bytes:
     if isinstance(src, torch.Tensor):
         return src.detach().to("cpu", torch.float64).numpy().astype("<f4").tobytes()
@@ -395,7 +402,7 @@ def _wire_bytes(src) -> bytes:
 def _reduction_maker(job, x, lo, hi, merged, special, descriptors):
     """Bytes of assignee x's re-uploaded reduction ("<f4", butterfly.py:235-240)."""
     if not special:  # all survivors honest: every reduction equals the merged mean
-        return lambda: merged[lo:hi].astype("<f4").tobytes()
+        return lambda: _host(merged[lo:hi]).astype("<f4").tobytes()
 
     def make():
         mean = job.means[lo:hi]
