@@ -30,14 +30,23 @@ counts, P, seed = case["counts"], case["P"], case["seed"]
 n = sum(counts)
 rng = np.random.default_rng(7)
 data = (rng.uniform(-1, 1, (n, P)) * 10.0 ** rng.integers(-4, 4, (n, 1))).astype(np.float32)
+r = case.get("r", 2)
+bf16 = case.get("bf16", False)
+if bf16:
+    data = (data.view(np.uint32) >> 16).astype(np.uint16)
 fails = tuple(case["failures"])
 specs = {int(k): tuple(v) for k, v in case["corr"].items()}
 fb = rng.uniform(-2, 2, P) if case["fallback"] else None
-assign, bounds = orc.plan(n, P, seed)
-want = orc.merge(list(data), assign, bounds, failures=fails, corruptions=specs, fallback=fb)
+assign, bounds = orc.plan(n, P, seed, r=r)
+want = orc.merge(list(data), assign, bounds, failures=fails, corruptions=specs, fallback=fb,
+                 dtype=orc.BF16 if bf16 else orc.F32)
 off = sum(counts[:rank])
-local = [torch.from_numpy(data[off + i].copy()).to(dev) for i in range(counts[rank])]
-plan = DevicePlan(n, P, seed, device=dev)
+if bf16:
+    local = [torch.from_numpy(data[off + i].view(np.int16).copy()).to(dev).view(torch.bfloat16)
+             for i in range(counts[rank])]
+else:
+    local = [torch.from_numpy(data[off + i].copy()).to(dev) for i in range(counts[rank])]
+plan = DevicePlan(n, P, seed, redundancy=r, device=dev)
 kinds = {1: "add", 2: "scale", 3: "noise", 4: "noise_add"}
 corr = {m: Corruption(kinds[s[0]], s[1], (s[2], s[3]) if len(s) > 2 else (0, 0)) for m, s in specs.items()}
 job = ShardedButterflyMerge(local, plan, failures=fails, corruptions=corr,
@@ -46,8 +55,14 @@ job = ShardedButterflyMerge(local, plan, failures=fails, corruptions=corr,
 job.run()
 torch.cuda.synchronize()
 assert_same_floats(job.merged.cpu().numpy(), want["merged"])
-for t in local:
-    assert_same_floats(t.cpu().numpy(), want["merged"].astype(np.float32))
+if not bf16:
+    for t in local:
+        assert_same_floats(t.cpu().numpy(), want["merged"].astype(np.float32))
+else:
+    bits = np.array([orc.lib().orc_f32_to_bf16(float(v)) for v in want["merged"][:4099].astype(np.float32)],
+                    dtype=np.uint16)
+    for t in local:
+        assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16)[:4099], bits)
 assert np.array_equal(job.status.cpu().numpy(), want["status"])
 assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
 assert_entries_close(job.entries.cpu().numpy(), want["entries"])
@@ -62,6 +77,12 @@ CASES = [
      "fallback": False, "chunk": 4096 * 7},
     {"counts": [2, 6], "P": 300_001, "seed": 4, "failures": [1, 2], "corr": {"5": [3, 2.0, 1, 1], "6": [3, 2.0, 1, 1]},
      "fallback": True, "chunk": 4096},
+    {"counts": [3, 2, 4], "P": 500_009, "seed": 6, "failures": [4], "corr": {"1": [1, 0.5]}, "fallback": False,
+     "chunk": 4096 * 9},
+    {"counts": [4, 3], "P": 350_003, "seed": 8, "failures": [2], "corr": {"5": [3, 1.0, 2, 2]}, "fallback": True,
+     "chunk": 65536, "bf16": True},
+    {"counts": [3, 4], "P": 35 * 2000 + 3, "seed": 10, "failures": [0], "corr": {"6": [3, 1.0, 4, 4]},
+     "fallback": False, "chunk": 8192, "r": 3},
 ]
 
 
