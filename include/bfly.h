@@ -104,6 +104,8 @@ typedef struct bfly_merge_args {
   int64_t elem_end;               /* setup (NaN fill, classify) runs with the range starting at 0 */
   const void* d_fallback_src;     /* replica supplying fallback values (lowest alive miner);
                                      NULL = d_src[0]                                   */
+  int64_t shard_begin;            /* FINISH these shards only; 0,0 = all (the multi-GPU */
+  int64_t shard_end;              /* last rank finishes each chunk's shards early)      */
 } bfly_merge_args_t;
 
 /* ---- library ----------------------------------------------------------- */
@@ -194,12 +196,16 @@ typedef struct bfly_ring_desc {
   int32_t reduce_n, window;      /* pointers per reduce table; chunks of run-ahead   */
   void* stream_c;                /* chain / reduce stream                           */
   void* stream_r;                /* relay stream                                    */
+  const int64_t* finish_ranges;  /* last rank, optional: [k_chunks*2] shard range to FINISH
+                                    after reducing chunk k (shards inside the chunk), on
+                                    stream_f, before the chunk enters the relay          */
+  void* stream_f;                /* last rank: late-shard stream (with finish_ranges)  */
 } bfly_ring_desc_t;
 int bfly_ring_round(const bfly_ring_desc_t* desc, uint32_t round_index);
 /* The op list of one rank for one round as rows of 7 int32
  * {kind, stream, peer, flag, slot, chunk, value}; returns the row count or -1. */
 int bfly_ring_ops(int32_t rank, int32_t world, int32_t k_chunks, int32_t nb, uint32_t round_index,
-                  int32_t* out, int32_t cap);
+                  int32_t late, int32_t* out, int32_t cap);
 
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);

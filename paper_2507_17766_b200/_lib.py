@@ -95,6 +95,8 @@ class MergeArgs(ctypes.Structure):
         ("elem_begin", ctypes.c_int64),
         ("elem_end", ctypes.c_int64),
         ("d_fallback_src", ctypes.c_void_p),
+        ("shard_begin", ctypes.c_int64),
+        ("shard_end", ctypes.c_int64),
     ]
 
 
@@ -122,6 +124,8 @@ class RingDesc(ctypes.Structure):
         ("window", ctypes.c_int32),
         ("stream_c", ctypes.c_void_p),
         ("stream_r", ctypes.c_void_p),
+        ("finish_ranges", ctypes.c_void_p),
+        ("stream_f", ctypes.c_void_p),
     ]
 
 
@@ -164,7 +168,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
-    L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, vp, i32]
+    L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)

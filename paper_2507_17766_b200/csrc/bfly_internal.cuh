@@ -23,14 +23,27 @@ enum ShardClass : uint8_t {
   kLost = 2,     // no survivor: fallback (butterfly.py:264-273)
 };
 
+// Outcome of a special / lost shard as k_classify predicts it, assuming honest copies
+// agree and corrupted ones disagree with everything: k_reduce writes the predicted
+// final value straight away and k_apply only revisits shards that came out otherwise.
+enum ShardPred : uint8_t {
+  kPredNone = 0,      // no guess (lone corrupted survivor, or fallback source overwritten in place)
+  kPredMean = 1,      // an honest majority adopts the mean
+  kPredFallback = 2,  // no majority (or no survivor): fallback values
+  kPredMask = 3,
+  kPredFuse = 0x80,   // flag: two device-computable copies, k_reduce accumulates their statistics
+};
+
 constexpr int kMaxR = 3;            // device path supports r = 2 (reference) and 3 (extension)
 constexpr int kThreads = 256;       // CTA size of the streaming kernels
-constexpr int kChunk = 16384;       // elements per CTA in the per-shard special kernels
+constexpr int kChunk = 16384;       // elements per CTA in k_apply
+constexpr int kMinStatTile = kThreads * 4;  // smallest statistics tile (fp64 payloads)
 
 struct ScratchLayout {
   int64_t S = 0, cps = 0;
   int npairs = 0;
-  size_t off_cls = 0, off_source = 0, off_stats = 0, off_scores = 0, off_has = 0, off_inv = 0;
+  int64_t ntiles = 0;  // statistics tiles of the smallest size
+  size_t off_cls = 0, off_pred = 0, off_done = 0, off_source = 0, off_stats = 0, off_scores = 0, off_has = 0, off_inv = 0;
   size_t total = 0;
   void init(int32_t n, int32_t r, int64_t P) {
     S = binom(n, r);
@@ -44,10 +57,16 @@ struct ScratchLayout {
     size_t o = 0;
     off_cls = o;
     o = align(o + (size_t)S);
+    off_pred = o;
+    o = align(o + (size_t)S);
+    ntiles = P / kMinStatTile + 1;
+    off_done = o;
+    o = align(o + (size_t)ntiles);
     off_source = o;
     o = align(o + sizeof(int32_t) * (size_t)S);
     off_stats = o;
-    o = align(o + sizeof(double) * 4 * (size_t)S * (size_t)cps * (size_t)npairs);
+    // one partial per (shard, statistics tile it overlaps): slot = tile + shard
+    o = align(o + sizeof(double) * 4 * (size_t)(ntiles + S) * (size_t)npairs);
     off_scores = o;
     o = align(o + sizeof(double) * (size_t)S * (size_t)npairs);
     off_has = o;

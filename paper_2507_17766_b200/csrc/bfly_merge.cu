@@ -76,10 +76,17 @@ struct DF32 {
     return v;
   }
   __device__ static void store8(void* p, int64_t e0, const double* v) {  // 32 B, aligned
+    st_stream((float*)p + e0, pack_d(v));
+  }
+  __device__ static V8 pack_d(const double* v) {  // K doubles -> one vector, as store() rounds
     V8 w;
 #pragma unroll
     for (int k = 0; k < 8; ++k) w.w[k] = __float_as_uint(__double2float_rn(v[k]));
-    st_stream((float*)p + e0, w);
+    return w;
+  }
+  __device__ static void unpack_raw(const V8& v, double* x) {  // stored values, exactly
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = (double)__uint_as_float(v.w[k]);
   }
 };
 
@@ -124,6 +131,21 @@ struct DBF16 {
              ((uint32_t)to_bits(__double2float_rn(v[2 * k + 1])) << 16);
     *reinterpret_cast<uint4*>((unsigned short*)p + e0) = make_uint4(w[0], w[1], w[2], w[3]);
   }
+  __device__ static V8 pack_d(const double* v) {
+    V8 w;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      w.w[k] = (uint32_t)to_bits(__double2float_rn(v[2 * k])) |
+               ((uint32_t)to_bits(__double2float_rn(v[2 * k + 1])) << 16);
+    return w;
+  }
+  __device__ static void unpack_raw(const V8& v, double* x) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      x[2 * k] = (double)__uint_as_float(v.w[k] << 16);
+      x[2 * k + 1] = (double)__uint_as_float(v.w[k] & 0xffff0000u);
+    }
+  }
 };
 
 // fp64 payloads rounded to the fp32 wire on load (astype("<f4"), butterfly.py:213,230).
@@ -157,6 +179,11 @@ struct DF64W {
     st_f64x4((double*)p + e0, v[0], v[1], v[2], v[3]);
     st_f64x4((double*)p + e0 + 4, v[4], v[5], v[6], v[7]);
   }
+  __device__ static V8 pack_d(const double* v) { return pack(v); }
+  __device__ static void unpack_raw(const V8& v, double* x) {  // the fp64 payload, unrounded
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = __hiloint2double((int)v.w[2 * k + 1], (int)v.w[2 * k]);
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -181,6 +208,9 @@ struct Params {
   uint8_t* flagged;
   int32_t* source;
   uint8_t* cls;
+  uint8_t* pred;  // ShardPred per shard
+  uint8_t* done;  // per statistics tile: partial already written by k_reduce
+  int64_t stile;  // statistics tile = one k_reduce tile (kThreads vectors)
   double* stats;
   double* scores;
   uint8_t* has_score;
@@ -190,6 +220,7 @@ struct Params {
   int32_t n_div;         // divisor of the mean: all alive miners across GPUs
   int64_t ebeg, eend;    // element range of this REDUCE call
   const void* fb_src;    // replica supplying fallback values (the lowest alive miner's)
+  int64_t sbeg, send;    // shard range of this FINISH call
 };
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000LL); }
@@ -287,6 +318,247 @@ __global__ void k_classify(Params p) {
   if (c != kFast && p.r > 2)
     for (int q = 0; q < p.npairs; ++q) p.has_score[s * p.npairs + q] = 0;
   p.cls[s] = c;
+  // predicted outcome (k_reduce writes it, k_apply revisits the rest); only when
+  // k_reduce runs, and a predicted mean only when the fallback source is not one
+  // of the replicas the mean overwrites in place
+  uint8_t pr = kPredNone;
+  if (p.n_alive > 0 || p.acc_in) {
+    if (c == kLost) {
+      pr = kPredFallback;
+    } else if (c == kSpecial) {
+      int nh = 0;
+      for (int k = 0; k < p.r; ++k) nh += !p.failed[mem[k]] && p.corr[mem[k]].kind == BFLY_CORR_NONE;
+      if (2 * nh > ns) {
+        const void* fb_raw = p.fb_src ? p.fb_src : (p.n_alive > 0 ? p.src[0] : nullptr);
+        bool safe = p.fallback != nullptr || fb_raw == nullptr;
+        if (!safe) {
+          safe = true;
+          for (int d = 0; d < p.n_dst; ++d) safe = safe && p.dst[d] != fb_raw;
+        }
+        if (safe) pr = kPredMean;
+      } else if (ns >= 2) {
+        pr = kPredFallback;
+      }
+    }
+  }
+  if (c == kSpecial && p.r == 2 && ns == 2 && p.corr[mem[0]].kind != BFLY_CORR_HOST &&
+      p.corr[mem[1]].kind != BFLY_CORR_HOST)
+    pr |= kPredFuse;
+  p.pred[s] = pr;
+}
+
+// fallback value of element e: the caller's fp64 fallback, else the lowest alive
+// miner's upload (butterfly.py:264-273), else NaN
+template <class D>
+__device__ __forceinline__ double fallback_at(const Params& p, const void* fb_raw, int64_t e) {
+  if (p.fallback) return p.fallback[e];
+  if (fb_raw) return D::raw(fb_raw, e);
+  return __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// the same for the K elements of 32-byte vector vidx (pointers 32-byte aligned)
+template <class D>
+__device__ __forceinline__ void fallback_vec(const Params& p, const void* fb_raw, int64_t vidx, double* v) {
+  constexpr int K = D::K;
+  if (p.fallback) {
+#pragma unroll
+    for (int k = 0; k < K; k += 4)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(v[k]), "=d"(v[k + 1]), "=d"(v[k + 2]), "=d"(v[k + 3])
+                   : "l"(p.fallback + vidx * K + k));
+  } else if (fb_raw) {
+    V8 raw;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(raw.w[0]), "=r"(raw.w[1]), "=r"(raw.w[2]), "=r"(raw.w[3]), "=r"(raw.w[4]),
+                   "=r"(raw.w[5]), "=r"(raw.w[6]), "=r"(raw.w[7])
+                 : "l"(reinterpret_cast<const V8*>(fb_raw) + vidx));
+    D::unpack_raw(raw, v);
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// corrupted copies and pair statistics (k_reduce's fused path, k_stats)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double corrupt_value(const bfly_corruption_t& c, double mean, int64_t e,
+                                                const double* host_copies, int slot, int64_t P) {
+  switch (c.kind) {
+    case BFLY_CORR_ADD: return __dadd_rn(mean, c.a);
+    case BFLY_CORR_SCALE: return __dmul_rn(mean, c.a);
+    case BFLY_CORR_NOISE:
+    case BFLY_CORR_NOISE_ADD: {
+      const double noise = __dmul_rn(c.a, noise_unit(philox_word(c.key0, c.key1, (uint64_t)e)));
+      return c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(mean, noise);
+    }
+    case BFLY_CORR_HOST: return host_copies[(int64_t)slot * P + e];
+    default: return mean;
+  }
+}
+
+__device__ __forceinline__ double max_nan(double a, double b) {
+  return (isnan(a) || isnan(b)) ? nan64() : fmax(a, b);
+}
+
+struct PairStat {
+  double mx, ab, aa, bb;
+};
+
+__device__ __forceinline__ PairStat warp_combine(PairStat s) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    s.mx = max_nan(s.mx, __shfl_xor_sync(0xffffffffu, s.mx, off));
+    s.ab = __dadd_rn(s.ab, __shfl_xor_sync(0xffffffffu, s.ab, off));
+    s.aa = __dadd_rn(s.aa, __shfl_xor_sync(0xffffffffu, s.aa, off));
+    s.bb = __dadd_rn(s.bb, __shfl_xor_sync(0xffffffffu, s.bb, off));
+  }
+  return s;
+}
+
+// CTA-wide fixed-order combine; result valid in thread 0.
+__device__ PairStat block_combine(PairStat s) {
+  __shared__ PairStat part[kThreads / 32];
+  s = warp_combine(s);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) part[w] = s;
+  __syncthreads();
+  if (w == 0) {
+    s = lane < kThreads / 32 ? part[lane] : PairStat{0.0, 0.0, 0.0, 0.0};
+    s = warp_combine(s);
+  }
+  return s;
+}
+
+// agreement decision from combined statistics (butterfly.py:127-133)
+__device__ __forceinline__ double score_of(const PairStat& s, double tol) {
+  if (!isnan(s.mx) && s.mx <= tol) return 1.0;
+  const double na = sqrt(s.aa), nb = sqrt(s.bb);
+  if (na == 0.0 || nb == 0.0) return 0.0;
+  const double c = __ddiv_rn(s.ab, __dmul_rn(na, nb));
+  if (isnan(c)) return c;
+  return c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+}
+
+// Copies of eight consecutive elements e0..e0+7 (e0 % 8 == 0): one Philox4x64
+// call yields four noise words, so a group needs two calls per noisy assignee.
+__device__ __forceinline__ void corrupt8(const bfly_corruption_t& c, const double* m, int64_t e0, unsigned valid,
+                                         const double* host_copies, int slot, int64_t P, double* out) {
+  switch (c.kind) {
+    case BFLY_CORR_ADD:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = __dadd_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_SCALE:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = __dmul_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_NOISE:
+    case BFLY_CORR_NOISE_ADD: {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        Philox4x64 ctr;
+        ctr.v[0] = (uint64_t)(e0 >> 2) + h + 1;  // word e lives in block e/4 (+1: numpy pre-increment)
+        ctr.v[1] = ctr.v[2] = ctr.v[3] = 0;
+        const Philox4x64 o = philox4x64_10(ctr, c.key0, c.key1);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double noise = __dmul_rn(c.a, noise_unit(o.v[j]));
+          out[4 * h + j] = c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(m[4 * h + j], noise);
+        }
+      }
+      return;
+    }
+    case BFLY_CORR_HOST:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = (valid >> i) & 1 ? host_copies[(int64_t)slot * P + e0 + i] : 0.0;
+      return;
+    default:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = m[i];
+  }
+}
+
+// ws[e0..e0+7]: one 64-byte vector when the group is whole, masked scalars otherwise
+__device__ __forceinline__ unsigned load_group(const double* ws, int64_t e0, int64_t lo, int64_t hi, double* m) {
+  unsigned valid = 0;
+  if (e0 >= lo && e0 + 8 <= hi) {
+    valid = 0xff;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                   : "=d"(m[4 * h]), "=d"(m[4 * h + 1]), "=d"(m[4 * h + 2]), "=d"(m[4 * h + 3])
+                   : "l"(ws + e0 + 4 * h));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool in = e0 + i >= lo && e0 + i < hi;
+      m[i] = in ? ws[e0 + i] : 0.0;
+      valid |= (unsigned)in << i;
+    }
+  }
+  return valid;
+}
+
+// Copies of four consecutive elements e0..e0+3 (e0 % 4 == 0) of a device-computable
+// corruption: one Philox4x64 block of noise words.
+__device__ __forceinline__ void corrupt4(const bfly_corruption_t& c, const double* m, int64_t e0, double* out) {
+  switch (c.kind) {
+    case BFLY_CORR_ADD:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[i] = __dadd_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_SCALE:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[i] = __dmul_rn(m[i], c.a);
+      return;
+    case BFLY_CORR_NOISE:
+    case BFLY_CORR_NOISE_ADD: {
+      Philox4x64 ctr;
+      ctr.v[0] = (uint64_t)(e0 >> 2) + 1;
+      ctr.v[1] = ctr.v[2] = ctr.v[3] = 0;
+      const Philox4x64 o = philox4x64_10(ctr, c.key0, c.key1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double noise = __dmul_rn(c.a, noise_unit(o.v[j]));
+        out[j] = c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(m[j], noise);
+      }
+      return;
+    }
+    default:
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[i] = m[i];
+  }
+}
+
+// Statistics of one vector (K means at e0, e0 % 4 == 0) for the copy pair (ca, cb).
+template <class D>
+__device__ __forceinline__ PairStat pair_stats_vec(const typename D::Acc* acc, int64_t e0, const bfly_corruption_t& ca,
+                                                   const bfly_corruption_t& cb) {
+  PairStat st{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int h = 0; h < D::K / 4; ++h) {
+    double m[4], x[4], y[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = D::widen(acc[4 * h + j]);
+    corrupt4(ca, m, e0 + 4 * h, x);
+    corrupt4(cb, m, e0 + 4 * h, y);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      st.mx = max_nan(st.mx, fabs(__dsub_rn(x[j], y[j])));
+      st.ab = fma(x[j], y[j], st.ab);
+      st.aa = fma(x[j], x[j], st.aa);
+      st.bb = fma(y[j], y[j], st.bb);
+    }
+  }
+  return st;
+}
+
+// partial statistics of shard s over statistics tile t (slot = t + s, see ScratchLayout)
+__device__ __forceinline__ double* stat_slot(const Params& p, int64_t s, int64_t t, int pi) {
+  return p.stats + ((t + s) * p.npairs + pi) * 4;
 }
 
 // ---------------------------------------------------------------------------
@@ -368,13 +640,32 @@ __device__ __forceinline__ bool stage_pointers(const void** s_src, void** s_dst,
   return __syncthreads_or((int)(mis & 31)) == 0;
 }
 
+// One element of a special / lost shard: the mean into the workspace (special), then
+// the predicted final value into merged and the replicas.
+template <class D>
+__device__ __forceinline__ void emit_predicted(const Params& p, void* const* s_dst, const void* fb_raw,
+                                               bool merged_apart, int64_t e, uint8_t c, uint8_t pr, double mean) {
+  if (c == kSpecial) p.ws[e] = mean;
+  if (pr == kPredMean) {
+    if (merged_apart) p.merged[e] = mean;
+    for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, mean);
+  } else if (pr == kPredFallback) {
+    const double v = fallback_at<D>(p, fb_raw, e);  // read before the in-place stores
+    if (p.merged && (c == kLost || merged_apart)) p.merged[e] = v;
+    for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, v);
+  }
+}
+
 template <class D, int U = 4, int MINB = 1, bool NOU = false>
 __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_alive] src, then [n_dst] dst
   const void** s_src = s_ptr;
   void** s_dst = const_cast<void**>(s_ptr + p.n_alive);
+  const void* fb_raw = p.fb_src ? p.fb_src : (p.n_alive > 0 ? p.src[0] : nullptr);
   const bool aligned = stage_pointers(s_src, s_dst, p.src, p.n_alive, p.dst, p.n_dst,
-                                      (uintptr_t)p.merged | (uintptr_t)p.acc_in | (uintptr_t)p.ws);
+                                      (uintptr_t)p.merged | (uintptr_t)p.acc_in | (uintptr_t)p.ws |
+                                          (uintptr_t)p.fallback | (uintptr_t)fb_raw);
+  const bool merged_apart = p.merged && p.merged != p.ws;  // final values may go to merged early
   constexpr int K = D::K;
   constexpr int TILE = kThreads * K;
   using Acc = typename D::Acc;
@@ -418,29 +709,69 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
         }
         const V8 out = D::pack(acc);
         for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
-      } else if (c == kSpecial) {  // the mean waits in the workspace for k_stats / k_apply
+      } else if (c != 0xff) {  // one special or lost shard
+        if (c == kSpecial) {  // the mean waits in the workspace for k_stats / k_apply
 #pragma unroll
-        for (int k = 0; k < K; k += 4)
-          st_f64x4(p.ws + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
-                   D::widen(acc[k + 3]));
-      } else if (c == 0xff) {  // the vector straddles shards of different classes
+          for (int k = 0; k < K; k += 4)
+            st_f64x4(p.ws + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
+                     D::widen(acc[k + 3]));
+        }
+        const uint8_t pr = p.pred[sa] & kPredMask;
+        if (pr == kPredMean) {
+          if (merged_apart) {
+#pragma unroll
+            for (int k = 0; k < K; k += 4)
+              st_f64x4(p.merged + e0 + k, D::widen(acc[k]), D::widen(acc[k + 1]), D::widen(acc[k + 2]),
+                       D::widen(acc[k + 3]));
+          }
+          const V8 out = D::pack(acc);
+          for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
+        } else if (pr == kPredFallback) {
+          double v[K];
+          fallback_vec<D>(p, fb_raw, vidx, v);  // read before the in-place stores below
+          if (p.merged && (c == kLost || merged_apart)) {
+#pragma unroll
+            for (int k = 0; k < K; k += 4) st_f64x4(p.merged + e0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
+          }
+          const V8 out = D::pack_d(v);
+          for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
+        }
+      } else {  // the vector straddles shards of different classes
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int64_t e = e0 + k;
-          const uint8_t ce = p.cls[p.bnd.shard_of(e)];
+          const int64_t se = p.bnd.shard_of(e);
+          const uint8_t ce = p.cls[se];
           if (ce == kFast) {
             if (p.merged) p.merged[e] = D::widen(acc[k]);
             for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(acc[k]));
-          } else if (ce == kSpecial) {
-            p.ws[e] = D::widen(acc[k]);
+          } else {
+            emit_predicted<D>(p, s_dst, fb_raw, merged_apart, e, ce, p.pred[se] & kPredMask, D::widen(acc[k]));
           }
         }
-      }  // kLost: nothing to write, k_apply falls back
+      }
+      // a whole tile of one special shard with two device-computable copies: its
+      // pair statistics now, from the means in registers (k_stats skips the tile)
+      if (!all_fast && s_lo == s_hi && (p.pred[s_lo] & kPredFuse)) {
+        const int32_t* mem = p.assign + s_lo * 2;
+        const PairStat st = block_combine(pair_stats_vec<D>(acc, e0, p.corr[mem[0]], p.corr[mem[1]]));
+        if (threadIdx.x == 0) {
+          double* o = stat_slot(p, s_lo, tile, 0);
+          o[0] = st.mx;
+          o[1] = st.ab;
+          o[2] = st.aa;
+          o[3] = st.bb;
+          p.done[tile] = 1;
+        }
+      }
     } else {
       for (int64_t e = t0 + threadIdx.x; e < t1; e += kThreads) {
         const int64_t s = p.bnd.shard_of(e);
         const uint8_t c = p.cls[s];
-        if (c == kLost) continue;
+        if (c == kLost) {
+          emit_predicted<D>(p, s_dst, fb_raw, merged_apart, e, c, p.pred[s] & kPredMask, 0.0);
+          continue;
+        }
         Acc m;
         if (p.acc_in) {  // chain continuation (width-1 shards are rejected on the host)
           Acc acc = (Acc)p.acc_in[e - p.ebeg];
@@ -453,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
           if (p.merged) p.merged[e] = D::widen(m);
           for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(m));
         } else {
-          p.ws[e] = D::widen(m);
+          emit_predicted<D>(p, s_dst, fb_raw, merged_apart, e, c, p.pred[s] & kPredMask, D::widen(m));
         }
       }
     }
@@ -588,134 +919,15 @@ __global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* cons
 }
 
 // ---------------------------------------------------------------------------
-// special shards: copies, statistics, decision, adoption
+// special shards: statistics, decision, adoption
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ double corrupt_value(const bfly_corruption_t& c, double mean, int64_t e,
-                                                const double* host_copies, int slot, int64_t P) {
-  switch (c.kind) {
-    case BFLY_CORR_ADD: return __dadd_rn(mean, c.a);
-    case BFLY_CORR_SCALE: return __dmul_rn(mean, c.a);
-    case BFLY_CORR_NOISE:
-    case BFLY_CORR_NOISE_ADD: {
-      const double noise = __dmul_rn(c.a, noise_unit(philox_word(c.key0, c.key1, (uint64_t)e)));
-      return c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(mean, noise);
-    }
-    case BFLY_CORR_HOST: return host_copies[(int64_t)slot * P + e];
-    default: return mean;
-  }
-}
-
-__device__ __forceinline__ double max_nan(double a, double b) {
-  return (isnan(a) || isnan(b)) ? nan64() : fmax(a, b);
-}
-
-struct PairStat {
-  double mx, ab, aa, bb;
-};
-
-__device__ __forceinline__ PairStat warp_combine(PairStat s) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    s.mx = max_nan(s.mx, __shfl_xor_sync(0xffffffffu, s.mx, off));
-    s.ab = __dadd_rn(s.ab, __shfl_xor_sync(0xffffffffu, s.ab, off));
-    s.aa = __dadd_rn(s.aa, __shfl_xor_sync(0xffffffffu, s.aa, off));
-    s.bb = __dadd_rn(s.bb, __shfl_xor_sync(0xffffffffu, s.bb, off));
-  }
-  return s;
-}
-
-// CTA-wide fixed-order combine; result valid in thread 0.
-__device__ PairStat block_combine(PairStat s) {
-  __shared__ PairStat part[kThreads / 32];
-  s = warp_combine(s);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();
-  if (lane == 0) part[w] = s;
-  __syncthreads();
-  if (w == 0) {
-    s = lane < kThreads / 32 ? part[lane] : PairStat{0.0, 0.0, 0.0, 0.0};
-    s = warp_combine(s);
-  }
-  return s;
-}
-
-// agreement decision from combined statistics (butterfly.py:127-133)
-__device__ __forceinline__ double score_of(const PairStat& s, double tol) {
-  if (!isnan(s.mx) && s.mx <= tol) return 1.0;
-  const double na = sqrt(s.aa), nb = sqrt(s.bb);
-  if (na == 0.0 || nb == 0.0) return 0.0;
-  const double c = __ddiv_rn(s.ab, __dmul_rn(na, nb));
-  if (isnan(c)) return c;
-  return c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
-}
-
-// Copies of eight consecutive elements e0..e0+7 (e0 % 8 == 0): one Philox4x64
-// call yields four noise words, so a group needs two calls per noisy assignee.
-__device__ __forceinline__ void corrupt8(const bfly_corruption_t& c, const double* m, int64_t e0, unsigned valid,
-                                         const double* host_copies, int slot, int64_t P, double* out) {
-  switch (c.kind) {
-    case BFLY_CORR_ADD:
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = __dadd_rn(m[i], c.a);
-      return;
-    case BFLY_CORR_SCALE:
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = __dmul_rn(m[i], c.a);
-      return;
-    case BFLY_CORR_NOISE:
-    case BFLY_CORR_NOISE_ADD: {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        Philox4x64 ctr;
-        ctr.v[0] = (uint64_t)(e0 >> 2) + h + 1;  // word e lives in block e/4 (+1: numpy pre-increment)
-        ctr.v[1] = ctr.v[2] = ctr.v[3] = 0;
-        const Philox4x64 o = philox4x64_10(ctr, c.key0, c.key1);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double noise = __dmul_rn(c.a, noise_unit(o.v[j]));
-          out[4 * h + j] = c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(m[4 * h + j], noise);
-        }
-      }
-      return;
-    }
-    case BFLY_CORR_HOST:
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = (valid >> i) & 1 ? host_copies[(int64_t)slot * P + e0 + i] : 0.0;
-      return;
-    default:
-#pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = m[i];
-  }
-}
-
-// ws[e0..e0+7]: one 64-byte vector when the group is whole, masked scalars otherwise
-__device__ __forceinline__ unsigned load_group(const double* ws, int64_t e0, int64_t lo, int64_t hi, double* m) {
-  unsigned valid = 0;
-  if (e0 >= lo && e0 + 8 <= hi) {
-    valid = 0xff;
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                   : "=d"(m[4 * h]), "=d"(m[4 * h + 1]), "=d"(m[4 * h + 2]), "=d"(m[4 * h + 3])
-                   : "l"(ws + e0 + 4 * h));
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const bool in = e0 + i >= lo && e0 + i < hi;
-      m[i] = in ? ws[e0 + i] : 0.0;
-      valid |= (unsigned)in << i;
-    }
-  }
-  return valid;
-}
-
+// Pair statistics of the special shards' tiles k_reduce did not cover (tiles shared
+// by two shards, partial tiles at element-range edges, r = 3, host copies).
 __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
-  const int64_t s = blockIdx.x;
+  const int64_t s = p.sbeg + blockIdx.x;
   if (p.cls[s] != kSpecial) return;
-  const int64_t lo = p.bnd.start(s) + (int64_t)blockIdx.y * kChunk;
-  const int64_t hi_s = p.bnd.start(s) + p.bnd.len(s);
-  const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
+  const int64_t start = p.bnd.start(s), hi_s = start + p.bnd.len(s);
   const int32_t* mem = p.assign + s * p.r;
   bool alive[kMaxR];
   bfly_corruption_t c[kMaxR];
@@ -723,44 +935,67 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
     alive[k] = !p.failed[mem[k]];
     c[k] = p.corr[mem[k]];
   }
-  const int64_t g_lo = lo & ~(int64_t)7;
-  for (int a = 0; a < p.r; ++a)
-    for (int b = a + 1; b < p.r; ++b) {
-      if (!alive[a] || !alive[b]) continue;
-      PairStat st{0.0, 0.0, 0.0, 0.0};
-      for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
-        double m[8], x[8], y[8];
-        const unsigned valid = load_group(p.ws, e0, lo, hi, m);
-        corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
-        corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (!((valid >> i) & 1)) continue;
-          st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
-          st.ab = fma(x[i], y[i], st.ab);
-          st.aa = fma(x[i], x[i], st.aa);
-          st.bb = fma(y[i], y[i], st.bb);
+  // the CTA scans kThreads tiles at a time and works through the ones k_reduce left
+  __shared__ int64_t todo[kThreads];
+  __shared__ int n_todo;
+  const int64_t t_first = start / p.stile, t_last = (hi_s - 1) / p.stile;
+  for (int64_t batch = t_first + (int64_t)blockIdx.y * kThreads; batch <= t_last;
+       batch += (int64_t)gridDim.y * kThreads) {
+    if (threadIdx.x == 0) n_todo = 0;
+    __syncthreads();
+    const int64_t tc = batch + threadIdx.x;
+    const bool need = tc <= t_last && !p.done[tc];
+    const unsigned ballot = __ballot_sync(0xffffffffu, need);
+    int base = 0;
+    if ((threadIdx.x & 31) == 0 && ballot) base = atomicAdd(&n_todo, __popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (need) todo[base + __popc(ballot & ((1u << (threadIdx.x & 31)) - 1))] = tc;
+    __syncthreads();
+    const int nt = n_todo;
+    for (int it = 0; it < nt; ++it) {
+      const int64_t t = todo[it];  // order within the batch is irrelevant: one slot per tile
+      const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
+      const int64_t g_lo = lo & ~(int64_t)7;
+      for (int a = 0; a < p.r; ++a)
+        for (int b = a + 1; b < p.r; ++b) {
+          if (!alive[a] || !alive[b]) continue;
+          PairStat st{0.0, 0.0, 0.0, 0.0};
+          for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
+            double m[8], x[8], y[8];
+            const unsigned valid = load_group(p.ws, e0, lo, hi, m);
+            corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
+            corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
+  #pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (!((valid >> i) & 1)) continue;
+              st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
+              st.ab = fma(x[i], y[i], st.ab);
+              st.aa = fma(x[i], x[i], st.aa);
+              st.bb = fma(y[i], y[i], st.bb);
+            }
+          }
+          st = block_combine(st);
+          if (threadIdx.x == 0) {
+            double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
+            o[0] = st.mx;
+            o[1] = st.ab;
+            o[2] = st.aa;
+            o[3] = st.bb;
+          }
         }
-      }
-      st = block_combine(st);
-      if (threadIdx.x == 0) {
-        double* o = p.stats + ((s * p.cps + blockIdx.y) * p.npairs + pair_index(p.r, a, b)) * 4;
-        o[0] = st.mx;
-        o[1] = st.ab;
-        o[2] = st.aa;
-        o[3] = st.bb;
-      }
     }
+    __syncthreads();  // todo / n_todo are rewritten by the next batch
+  }
 }
 
 // One warp per shard.
 __global__ void k_decide(Params p) {
-  const int64_t s = blockIdx.x;
+  const int64_t s = p.sbeg + blockIdx.x;
   if (p.cls[s] != kSpecial) return;
   const int lane = threadIdx.x;
   const int32_t* mem = p.assign + s * p.r;
-  const int64_t len = p.bnd.len(s);
-  const int64_t nchunks = (len + kChunk - 1) / kChunk;
+  const int64_t start = p.bnd.start(s), len = p.bnd.len(s);
+  const int64_t t0 = start / p.stile, ntiles = (start + len - 1) / p.stile - t0 + 1;
   int surv[kMaxR], ns = 0;
   for (int k = 0; k < p.r; ++k)
     if (!p.failed[mem[k]]) surv[ns++] = k;
@@ -769,8 +1004,8 @@ __global__ void k_decide(Params p) {
     for (int y = x + 1; y < ns; ++y) {
       const int pi = pair_index(p.r, surv[x], surv[y]);
       PairStat st{0.0, 0.0, 0.0, 0.0};
-      for (int64_t ch = lane; ch < nchunks; ch += 32) {
-        const double* o = p.stats + ((s * p.cps + ch) * p.npairs + pi) * 4;
+      for (int64_t ch = lane; ch < ntiles; ch += 32) {
+        const double* o = stat_slot(p, s, t0 + ch, pi);
         st.mx = max_nan(st.mx, o[0]);
         st.ab = __dadd_rn(st.ab, o[1]);
         st.aa = __dadd_rn(st.aa, o[2]);
@@ -845,7 +1080,7 @@ __global__ void k_entries3(Params p) {
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
-  const int64_t s = blockIdx.x;
+  const int64_t s = p.sbeg + blockIdx.x;
   const uint8_t c = p.cls[s];
   if (c == kFast) return;
   void** s_dst = const_cast<void**>(s_ptr);
@@ -860,6 +1095,15 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
     for (int k = 0; k < p.r; ++k)
       if (p.assign[s * p.r + k] == src_m) slot = k;
     cd = p.corr[src_m];
+  }
+  // k_reduce already wrote the predicted outcome; only the merged vector may still
+  // need the fallback values (when it doubles as the workspace of the means)
+  const uint8_t pr = p.pred[s] & kPredMask;
+  const bool as_predicted = src_m < 0 ? pr == kPredFallback : (pr == kPredMean && cd.kind == BFLY_CORR_NONE);
+  int n_dst = p.n_dst;
+  if (as_predicted) {
+    if (!(src_m < 0 && c == kSpecial && p.merged && p.merged == p.ws)) return;
+    n_dst = 0;
   }
   const void* fb_raw = p.fb_src ? p.fb_src : (p.n_alive > 0 ? p.src[0] : nullptr);
   for (int64_t e0 = (lo & ~(int64_t)7) + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
@@ -887,13 +1131,13 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
         st_f64x4(p.merged + e0, v[0], v[1], v[2], v[3]);
         st_f64x4(p.merged + e0 + 4, v[4], v[5], v[6], v[7]);
       }
-      for (int d = 0; d < p.n_dst; ++d) D::store8(s_dst[d], e0, v);
+      for (int d = 0; d < n_dst; ++d) D::store8(s_dst[d], e0, v);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if (!((valid >> i) & 1)) continue;
         if (p.merged) p.merged[e0 + i] = v[i];
-        for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e0 + i, v[i]);
+        for (int d = 0; d < n_dst; ++d) D::store(s_dst[d], e0 + i, v[i]);
       }
     }
   }
@@ -1007,7 +1251,7 @@ template <class D>
 static void launch_apply(const Params& p, cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_apply<D><<<dim3((unsigned)p.S, (unsigned)p.cps), kThreads, smem, st>>>(p);
+  k_apply<D><<<dim3((unsigned)(p.send - p.sbeg), (unsigned)p.cps), kThreads, smem, st>>>(p);
 }
 
 extern "C" {
@@ -1066,6 +1310,9 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.flagged = a->d_flagged;
   unsigned char* sc = (unsigned char*)a->d_scratch;
   p.cls = sc + L.off_cls;
+  p.pred = sc + L.off_pred;
+  p.done = sc + L.off_done;
+  p.stile = (int64_t)kThreads * (a->dtype == BFLY_F32 ? DF32::K : a->dtype == BFLY_BF16 ? DBF16::K : DF64W::K);
   p.source = a->d_source ? a->d_source : (int32_t*)(sc + L.off_source);
   p.stats = (double*)(sc + L.off_stats);
   p.scores = (double*)(sc + L.off_scores);
@@ -1079,6 +1326,9 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   if (p.ebeg < 0 || p.eend > p.P || p.ebeg > p.eend) return fail(BFLY_E_INVALID_ARG, "bad element range");
   if (p.acc_in && p.bnd.base == 1) return fail(BFLY_E_UNSUPPORTED, "chained reduction needs shards of >= 2 elements");
   p.fb_src = a->d_fallback_src ? a->d_fallback_src : nullptr;
+  p.sbeg = a->shard_begin;
+  p.send = (a->shard_begin == 0 && a->shard_end == 0) ? S : a->shard_end;
+  if (p.sbeg < 0 || p.send > S || p.sbeg > p.send) return fail(BFLY_E_INVALID_ARG, "bad shard range");
   return BFLY_OK;
 }
 
@@ -1090,12 +1340,13 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
 
   const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
-  const bool do_finish = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH;
+  const bool do_finish = (a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH) && p.send > p.sbeg;
   if (do_reduce) {
     if (p.ebeg == 0) {  // per-round setup runs with the first (or only) element range
       const int64_t nn = (int64_t)p.n * p.n;
       k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
       cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
+      cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
       k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
     }
     if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
@@ -1109,8 +1360,11 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
     }
   }
   if (do_finish) {
-    k_stats<<<dim3((unsigned)S, (unsigned)p.cps), kThreads, 0, st>>>(p);
-    k_decide<<<(unsigned)S, 32, 0, st>>>(p);
+    const unsigned ns = (unsigned)(p.send - p.sbeg);
+    const int64_t tps = (p.bnd.base + (p.bnd.rem ? 1 : 0) + p.stile - 1) / p.stile + 1;  // tiles per shard
+    const int64_t nb = (tps + kThreads - 1) / kThreads;  // tile batches per shard
+    k_stats<<<dim3(ns, (unsigned)(nb < 65535 ? nb : 65535)), kThreads, 0, st>>>(p);
+    k_decide<<<ns, 32, 0, st>>>(p);
     if (p.r > 2) {
       const int64_t nn = (int64_t)p.n * p.n;
       k_entries3<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p);

@@ -115,17 +115,17 @@ int bfly_stream_write_value(uint32_t* d_flag, uint32_t value, void* stream) {
 
 namespace bfly {
 
-enum RingOp : int32_t { kOpWait = 0, kOpWrite = 1, kOpChain = 2, kOpReduce = 3, kOpFanout = 4 };
-enum RingFlag : int32_t { kAccReady = 0, kAccFree = 1, kFinReady = 2, kFinFree = 3 };
+enum RingOp : int32_t { kOpWait = 0, kOpWrite = 1, kOpChain = 2, kOpReduce = 3, kOpFanout = 4, kOpFinish = 5 };
+enum RingFlag : int32_t { kAccReady = 0, kAccFree = 1, kFinReady = 2, kFinFree = 3, kReduced = 4 };
 
 struct Op {
-  int32_t kind, stream;  // stream 0 = C (chain/reduce), 1 = R (relay)
+  int32_t kind, stream;  // stream 0 = C (chain/reduce), 1 = R (relay), 2 = F (late shards, last rank)
   int32_t peer, flag, slot, k;
   uint32_t value;
 };
 
 // The ops of rank g for chunk k (ringsched.chunk_ops, same order).
-static int chunk_ops(int g, int G, int K, int NB, uint32_t round_index, int k, Op* out) {
+static int chunk_ops(int g, int G, int K, int NB, uint32_t round_index, int k, bool late, Op* out) {
   const int Z = G - 1;
   const uint64_t idx = (uint64_t)round_index * (uint64_t)K + (uint64_t)k;
   const int s = (int)(idx % (uint64_t)NB);
@@ -153,8 +153,16 @@ static int chunk_ops(int g, int G, int K, int NB, uint32_t round_index, int k, O
     add(kOpWait, 0, g, kAccReady, v);
     if (!first_use) add(kOpWait, 0, g, kFinFree, prev);
     add(kOpReduce, 0, 0, -1, 0);
-    add(kOpWrite, 0, 0, kFinReady, v);
-    add(kOpWrite, 0, Z - 1, kAccFree, v);
+    if (late) {
+      add(kOpWrite, 0, g, kReduced, v);
+      add(kOpWrite, 0, Z - 1, kAccFree, v);
+      add(kOpWait, 2, g, kReduced, v);
+      add(kOpFinish, 2, 0, -1, 0);
+      add(kOpWrite, 2, 0, kFinReady, v);
+    } else {
+      add(kOpWrite, 0, 0, kFinReady, v);
+      add(kOpWrite, 0, Z - 1, kAccFree, v);
+    }
   }
   return n;
 }
@@ -163,12 +171,13 @@ static int chunk_ops(int g, int G, int K, int NB, uint32_t round_index, int k, O
 
 extern "C" {
 
-int bfly_ring_ops(int32_t g, int32_t G, int32_t K, int32_t NB, uint32_t round_index, int32_t* out, int32_t cap) {
+int bfly_ring_ops(int32_t g, int32_t G, int32_t K, int32_t NB, uint32_t round_index, int32_t late, int32_t* out,
+                  int32_t cap) {
   if (G < 2 || NB < 2 || g < 0 || g >= G || K < 0) return -1;
   int n = 0;
   Op ops[16];
   for (int k = 0; k < K; ++k) {
-    const int m = chunk_ops(g, G, K, NB, round_index, k, ops);
+    const int m = chunk_ops(g, G, K, NB, round_index, k, late != 0, ops);
     for (int i = 0; i < m; ++i) {
       if (n + 1 > cap) return -1;
       int32_t* r = out + 7 * n;
@@ -191,12 +200,13 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
   if (rc) return rc;
   const int g = d->rank, G = d->world, K = d->k_chunks, NB = d->nb;
   const bool last = g == G - 1;
-  cudaStream_t sc = (cudaStream_t)d->stream_c, sr = (cudaStream_t)d->stream_r;
+  cudaStream_t sc = (cudaStream_t)d->stream_c, sr = (cudaStream_t)d->stream_r, sf = (cudaStream_t)d->stream_f;
+  const bool late = last && d->finish_ranges != nullptr;
   // run-ahead throttle: the host never has more than `window` chunks queued per
   // stream; a launch blocked on a full queue behind a wait must not keep the host
   // from issuing the other stream's ops that wait depends on
   const int W = d->window > 0 ? d->window : 4;
-  std::vector<cudaEvent_t> ev(2 * (W + 1));
+  std::vector<cudaEvent_t> ev(3 * (W + 1));
   for (auto& e : ev) {
     cudaError_t ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     if (ce != cudaSuccess) return cuda_fail(ce, "ring event");
@@ -211,10 +221,10 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
   for (int k = 0; k < K && result == BFLY_OK; ++k) {
     const int64_t b = (int64_t)k * d->chunk;
     const int64_t e = b + d->chunk < d->payload_len ? b + d->chunk : d->payload_len;
-    const int m = chunk_ops(g, G, K, NB, round_index, k, ops);
+    const int m = chunk_ops(g, G, K, NB, round_index, k, late, ops);
     for (int i = 0; i < m && result == BFLY_OK; ++i) {
       const Op& o = ops[i];
-      cudaStream_t st = o.stream == 0 ? sc : sr;
+      cudaStream_t st = o.stream == 0 ? sc : (o.stream == 1 ? sr : sf);
       const int s = o.slot;
       if (o.kind == kOpWait) {
         const unsigned fl = CU_STREAM_WAIT_VALUE_GEQ | (g_flush_supported ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
@@ -237,6 +247,18 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
         args.d_dst = (void* const*)d->reduce_tables[(int64_t)k * NB + s];
         args.n_dst = d->reduce_n;
         result = bfly_merge(&args, st);
+      } else if (o.kind == kOpFinish) {
+        // late shards lying inside chunk k are decided before the final chunk enters
+        // the relay, through the same scatter-back table (own replicas + rank 0's inbox)
+        if (d->finish_ranges[2 * k + 1] > d->finish_ranges[2 * k]) {
+          bfly_merge_args_t fa = args;
+          fa.phase = BFLY_PHASE_FINISH;
+          fa.shard_begin = d->finish_ranges[2 * k];
+          fa.shard_end = d->finish_ranges[2 * k + 1];
+          fa.d_dst = (void* const*)d->reduce_tables[(int64_t)k * NB + s];
+          fa.n_dst = d->reduce_n;
+          result = bfly_merge(&fa, st);
+        }
       } else if (o.kind == kOpFanout) {
         const void* src = (const void*)(d->peer_base[g] + d->off_fin + (uint64_t)s * d->chunk * d->esize);
         result = bfly_fanout(src, (void* const*)d->fan_tables[(int64_t)k * NB + s], d->fan_n,
@@ -244,12 +266,12 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
       }
     }
     const int slot_ev = k % (W + 1);
-    cudaEventRecord(ev[2 * slot_ev], sc);
-    cudaEventRecord(ev[2 * slot_ev + 1], sr);
-    if (k >= W) {  // wait for chunk k - W on both streams before queueing more
+    cudaEventRecord(ev[3 * slot_ev], sc);
+    cudaEventRecord(ev[3 * slot_ev + 1], sr);
+    cudaEventRecord(ev[3 * slot_ev + 2], late ? sf : sc);
+    if (k >= W) {  // wait for chunk k - W on every stream before queueing more
       const int old = (k - W) % (W + 1);
-      cudaEventSynchronize(ev[2 * old]);
-      cudaEventSynchronize(ev[2 * old + 1]);
+      for (int q = 0; q < 3; ++q) cudaEventSynchronize(ev[3 * old + q]);
     }
   }
   for (auto& e : ev) cudaEventDestroy(e);

@@ -300,6 +300,24 @@ class ButterflyMerge:
             self._args.d_dst, self._args.n_dst = saved
         return self
 
+    def run_finish_range(self, shard_begin: int, shard_end: int, stream=None, dst_table: tuple | None = None):
+        """FINISH (compare, decide, adopt / fall back, scatter back) for shards
+        [shard_begin, shard_end) only."""
+        if shard_end <= shard_begin or not self.needs_finish():
+            return self
+        a = self._args
+        saved = (a.d_dst, a.n_dst)
+        a.phase = L.PHASE_FINISH
+        a.shard_begin, a.shard_end = int(shard_begin), int(shard_end)
+        if dst_table is not None:
+            a.d_dst, a.n_dst = dst_table
+        try:
+            self._call(stream)
+        finally:
+            a.d_dst, a.n_dst = saved
+            a.shard_begin = a.shard_end = 0
+        return self
+
     def needs_finish(self) -> bool:
         return self.special or self.maybe_lost
 

@@ -164,15 +164,16 @@ class ShardedButterflyMerge:
         corrupted = {m for m in (corruptions or {}) if m not in failures}
         assign = plan.assign.cpu().numpy() if hasattr(plan.assign, "cpu") else np.asarray(plan.assign)
         runs = special_ranges(assign, self.P, failures, corrupted) if (corrupted or len(failures) >= 2) else []
-        self.special_runs = runs
-        if runs:
-            tab, off = [], 0
-            for lo, hi in runs:
-                off += (lo - off) % 16  # same 32-byte alignment on both sides (vector copies)
-                tab.append((lo, hi, off))
-                off += hi - lo
-            self._ranges = torch.tensor(tab, dtype=torch.int64, device=self.dev)
-            self._packed = torch.empty(off, dtype=local[0].dtype, device=self.dev)
+        # The last rank finishes a chunk's late (corrupted / lost) shards right after
+        # reducing it, before the final chunk enters the relay, so only shards that
+        # straddle a chunk boundary are finished after the ring and broadcast late.
+        self._finish_ranges, straddlers = self._chunk_shard_ranges(plan.n_shards)
+        self.straddlers = straddlers
+        late = [r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())] if G > 1 else runs
+        self.late_runs = late
+        self.special_runs = late  # kept name: ranges broadcast after the ring
+        self._fb_set = self._range_set(runs) if runs else None
+        self._late_set = self._range_set(late) if late else None
         # fallback values come from the lowest alive miner when no fallback is given
         self._needs_fb = bool(fallback is None and self.alive and runs)
         self.fb_owner, self._fb_buf = None, None
@@ -193,6 +194,9 @@ class ShardedButterflyMerge:
             self.job = ButterflyMerge(reps, plan, remote_sum=G > 1, n_div=len(self.alive), failures=failures,
                                       corruptions=corruptions, fallback=fallback, fallback_src=fb_src,
                                       scatter_back=True, want_merged=want_merged, tolerance=tolerance)
+        # last rank: late shards possible (corrupted survivors, or shards whose assignees
+        # all failed) -> each chunk's are finished on the late-shard stream
+        self._late_mode = bool(self.is_last and self.job.needs_finish())
         S, n = plan.n_shards, self.n
         self._res = torch.empty(8 * n * n + 4 * S + S + n, dtype=torch.uint8, device=self.dev)
         self.status = torch.empty(S, dtype=torch.uint8, device=self.dev)
@@ -205,6 +209,46 @@ class ShardedButterflyMerge:
         self._fb_table = self._table([self._fb_buf]) if self._fb_buf is not None else None
         if G > 1:
             self._setup_ring()
+
+    # -- late shards -------------------------------------------------------------
+    def _chunk_starts(self):
+        return [k * self.chunk for k in range(1, self.K)]
+
+    def _chunk_shard_ranges(self, S: int):
+        """Per chunk k, the shards lying entirely inside it ([s_begin, s_end)), and the
+        shards that straddle a chunk boundary."""
+        base, rem = divmod(self.P, S)
+
+        def start(s):
+            return s * base + min(s, rem)
+
+        def shard_of(e):
+            big = rem * (base + 1)
+            return e // (base + 1) if e < big else rem + (e - big) // base
+
+        ranges, straddle = [], []
+        for k in range(self.K):
+            b, e = self._bounds(k)
+            s0 = shard_of(b)
+            if start(s0) < b:
+                s0 += 1
+            s1 = shard_of(e - 1)
+            if start(s1 + 1) > e:  # start(S) == P, so s1 + 1 <= S is always valid
+                s1 -= 1
+            ranges.append((s0, max(s0, s1 + 1)))
+            if k > 0 and start(shard_of(b)) < b:
+                straddle.append(shard_of(b))
+        return ranges, sorted(set(straddle))
+
+    def _range_set(self, runs):
+        """Device table {lo, hi, packed offset} + packed buffer for element runs."""
+        tab, off = [], 0
+        for lo, hi in runs:
+            off += (lo - off) % 16  # same 32-byte alignment on both sides (vector copies)
+            tab.append((lo, hi, off))
+            off += hi - lo
+        return (torch.tensor(tab, dtype=torch.int64, device=self.dev),
+                torch.empty(off, dtype=self.local[0].dtype, device=self.dev))
 
     # -- peer-memory ring ------------------------------------------------------
     def _table(self, ptrs) -> torch.Tensor:
@@ -233,6 +277,7 @@ class ShardedButterflyMerge:
                 self._peer[r] = p.value
         dist.barrier()
         self._relay = torch.cuda.Stream(device=self.dev)
+        self._late = torch.cuda.Stream(device=self.dev)  # last rank: per-chunk late shards
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -267,6 +312,9 @@ class ShardedButterflyMerge:
             d.reduce_tables = ctypes.cast(self._red_arr, ctypes.c_void_p)
             d.reduce_n = len(self.local) + 1
             d.merge_args = ctypes.pointer(self.job._args)
+            if self._late_mode:
+                self._fin_arr = (ctypes.c_int64 * (2 * self.K))(*[x for r in self._finish_ranges for x in r])
+                d.finish_ranges = ctypes.cast(self._fin_arr, ctypes.c_void_p)
         else:
             self._fan_arr = (ctypes.c_uint64 * (self.K * NB))(
                 *[self._fan_tables[k, s].data_ptr() for k in range(self.K) for s in range(NB)])
@@ -298,7 +346,7 @@ class ShardedButterflyMerge:
     def _issue(self, op):
         lib, lay = L.lib(), self.layout
         kind, st = op[0], op[1]
-        stream = _stream_handle() if st == "C" else self._relay.cuda_stream
+        stream = {"C": _stream_handle(), "R": self._relay.cuda_stream, "F": self._late.cuda_stream}[st]
         if kind == "wait":
             _, _, flag, s, v = op
             L.check(lib.bfly_stream_wait_value(lay.flag(self._base, flag, s), v, stream))
@@ -317,6 +365,12 @@ class ShardedButterflyMerge:
             b, e = self._bounds(k)
             tab = self._reduce_tables[k, s]
             self.job.reduce_range(b, e, acc_in=lay.acc_slot(self._base, s), dst_table=(tab.data_ptr(), tab.numel()))
+        elif kind == "finish":
+            _, _, k, s, _fin_rank = op
+            tab = self._reduce_tables[k, s]
+            s0, s1 = self._finish_ranges[k]
+            with torch.cuda.stream(self._late):
+                self.job.run_finish_range(s0, s1, dst_table=(tab.data_ptr(), tab.numel()))
         elif kind == "fanout":
             _, _, k, s, _fwd = op
             b, e = self._bounds(k)
@@ -357,9 +411,10 @@ class ShardedButterflyMerge:
                 raise RuntimeError("multi-GPU ring did not complete")
             time.sleep(0.005)
 
-    def _copy_ranges(self, full, table, n_dst, scatter):
-        L.check(L.lib().bfly_copy_ranges(full, self._packed.data_ptr(), table, n_dst, self._ranges.data_ptr(),
-                                         self._ranges.shape[0], self.esize, scatter, _stream_handle()))
+    def _copy_ranges(self, rset, full, table, n_dst, scatter):
+        ranges, packed = rset
+        L.check(L.lib().bfly_copy_ranges(full, packed.data_ptr(), table, n_dst, ranges.data_ptr(), ranges.shape[0],
+                                         self.esize, scatter, _stream_handle()))
 
     # -- one round -------------------------------------------------------------
     def run(self) -> "ShardedButterflyMerge":
@@ -384,26 +439,30 @@ class ShardedButterflyMerge:
             # fallback values (the lowest alive miner's replica) for the late shards: packed
             # before the relay overwrites that replica, sent while the ring runs
             fb_work = None
+            self._relay.wait_stream(cur)
+            self._late.wait_stream(cur)
             if self._needs_fb and self.fb_owner != last:
                 if g == self.fb_owner:
-                    self._copy_ranges(self.local[self.alive[0] - self.offset].data_ptr(), None, 0, 0)
-                    fb_work = dist.isend(self._packed, dst=last)
-                elif self.is_last:
-                    fb_work = dist.irecv(self._packed, src=self.fb_owner)
+                    self._copy_ranges(self._fb_set, self.local[self.alive[0] - self.offset].data_ptr(), None, 0, 0)
+                    fb_work = dist.isend(self._fb_set[1], dst=last)
+                elif self.is_last:  # needed only by the late-shard stream, which it precedes
+                    with torch.cuda.stream(self._late):
+                        dist.recv(self._fb_set[1], src=self.fb_owner)
+                        self._copy_ranges(self._fb_set, None, self._fb_table.data_ptr(), 1, 1)
             mark("fallback")
-            self._relay.wait_stream(cur)
             marks, window = [], []
             if not self.debug:  # native executor: the whole round issued from C++
                 self._desc.stream_c = _stream_handle()
                 self._desc.stream_r = self._relay.cuda_stream
+                self._desc.stream_f = self._late.cuda_stream
                 with torch.cuda.device(self.dev):
                     L.check(L.lib().bfly_ring_round(ctypes.byref(self._desc), self._round & 0xFFFFFFFF))
             for k in range(self.K if self.debug else 0):  # debug: the same ops issued from Python
-                for op in rs.chunk_ops(g, G, self.K, NB, self._round, k):
+                for op in rs.chunk_ops(g, G, self.K, NB, self._round, k, self._late_mode):
                     self._issue(op)
                     if self.debug:
                         ev = torch.cuda.Event()
-                        ev.record(cur if op[1] == "C" else self._relay)
+                        ev.record({"C": cur, "R": self._relay, "F": self._late}[op[1]])
                         marks.append((op, ev))
                 # bounded run-ahead: never more than WINDOW chunks queued per stream
                 done = (torch.cuda.Event(), torch.cuda.Event())
@@ -416,28 +475,32 @@ class ShardedButterflyMerge:
                 self._watch(marks)
             self._marks = marks
             cur.wait_stream(self._relay)
+            cur.wait_stream(self._late)
         self._round += 1
         mark("ring")
 
-        # finish on the last rank, then per-shard results and the late shards
-        if G > 1 and fb_work is not None:
+        # finish the shards that straddle chunk boundaries, then distribute the
+        # per-shard results and those shards' final values
+        if fb_work is not None:
             fb_work.wait()
-            if self.is_last:
-                self._copy_ranges(None, self._fb_table.data_ptr(), 1, 1)
         if self.is_last:
-            self.job.run(L.PHASE_FINISH)
+            if G == 1:
+                self.job.run(L.PHASE_FINISH)
+            elif self.job.needs_finish():
+                for s in self.straddlers:
+                    self.job.run_finish_range(s, s + 1)
             pack_results(self.job.entries, self.job.source, self.job.status, self.job.flagged, self._res)
             if self.special_runs:
-                self._copy_ranges(self.local[0].data_ptr(), None, 0, 0)
+                self._copy_ranges(self._late_set, self.local[0].data_ptr(), None, 0, 0)
         mark("finish")
         if G > 1:
             dist.broadcast(self._res, src=last)
             mark("results")
             if self.special_runs:
-                dist.broadcast(self._packed, src=last)
+                dist.broadcast(self._late_set[1], src=last)
                 mark("late_bcast")
                 if not self.is_last:
-                    self._copy_ranges(None, self._local_table.data_ptr(), len(self.local), 1)
+                    self._copy_ranges(self._late_set, None, self._local_table.data_ptr(), len(self.local), 1)
                 mark("late_scatter")
             if self.want_merged:
                 if self.is_last:

@@ -23,6 +23,10 @@ last rank Z (stream "C"):
     wait acc_ready[s] >= v ; [v>NB] wait fin_free[s] >= v-NB
     reduce k -> own replicas + 0.fin_in[s]  divide, scatter back, push the final chunk
     write 0.fin_ready[s] = v ; write Z-1.acc_free[s] = v
+  with late shards (corrupted / lost) the chunk's shards are decided before the
+  final chunk is released, on stream "F" so the next reduce is not held up:
+    C: ... reduce k ; write reduced[s] = v (own) ; write Z-1.acc_free[s] = v
+    F: wait reduced[s] >= v ; finish k ; write 0.fin_ready[s] = v
 relay (stream "R"), ranks 0..Z-1, ring Z -> 0 -> 1 -> ... -> Z-1:
     wait fin_ready[s] >= v ; [succ and v>NB] wait fin_free[s] >= v-NB
     fanout k: fin_in[s] -> my replicas (+ succ.fin_in[s])
@@ -40,7 +44,7 @@ local write + copy-engine push pipeline cost 0.23 ms per chunk, the bulk stores
 
 from __future__ import annotations
 
-FLAGS = ("acc_ready", "acc_free", "fin_ready", "fin_free")
+FLAGS = ("acc_ready", "acc_free", "fin_ready", "fin_free", "reduced")
 
 
 def relay_pred(g: int, Z: int) -> int:
@@ -59,12 +63,13 @@ def slot(round_index: int, K: int, k: int, NB: int) -> int:
     return (round_index * K + k) % NB
 
 
-def chunk_ops(g: int, G: int, K: int, NB: int, round_index: int, k: int) -> list:
+def chunk_ops(g: int, G: int, K: int, NB: int, round_index: int, k: int, late: bool = False) -> list:
     """Ops of rank g for chunk k of one round (stream "C" ops, then stream "R" ops):
     ("wait", stream, flag, slot, value)         wait on a flag in MY region
     ("write", stream, peer, flag, slot, value)   write a flag in peer's region
     ("chain", stream, k, slot, dst_rank)
     ("reduce", stream, k, slot, fin_rank)
+    ("finish", stream, k, slot, fin_rank)      late shards of chunk k (``late`` only)
     ("fanout", stream, k, slot, fwd_rank|None)
     """
     if G < 2:
@@ -99,19 +104,26 @@ def chunk_ops(g: int, G: int, K: int, NB: int, round_index: int, k: int) -> list
         if not first_use:
             ops.append(("wait", "C", "fin_free", s, prev))
         ops.append(("reduce", "C", k, s, 0))
-        ops.append(("write", "C", 0, "fin_ready", s, v))
-        ops.append(("write", "C", Z - 1, "acc_free", s, v))
+        if late:
+            ops.append(("write", "C", g, "reduced", s, v))
+            ops.append(("write", "C", Z - 1, "acc_free", s, v))
+            ops.append(("wait", "F", "reduced", s, v))
+            ops.append(("finish", "F", k, s, 0))
+            ops.append(("write", "F", 0, "fin_ready", s, v))
+        else:
+            ops.append(("write", "C", 0, "fin_ready", s, v))
+            ops.append(("write", "C", Z - 1, "acc_free", s, v))
     return ops
 
 
-def round_ops(g: int, G: int, K: int, NB: int, round_index: int) -> list:
+def round_ops(g: int, G: int, K: int, NB: int, round_index: int, late: bool = False) -> list:
     """All ops of rank g for one round, chunk by chunk (see chunk_ops).
 
     The executor issues them chunk by chunk and keeps at most a few chunks in
     flight per stream: a host that enqueued far ahead could block inside a
     launch on a stream stalled at a wait, before issuing the other stream's ops
     the wait depends on."""
-    return [op for k in range(K) for op in chunk_ops(g, G, K, NB, round_index, k)]
+    return [op for k in range(K) for op in chunk_ops(g, G, K, NB, round_index, k, late)]
 
 
 def geq(flag_value: int, v: int) -> bool:

@@ -30,7 +30,7 @@ class Rank:
         self.final_written = set()
 
 
-def simulate(G, counts, P, C, NB, rounds, failures=(), seed=0, start_round=0):
+def simulate(G, counts, P, C, NB, rounds, failures=(), seed=0, start_round=0, late=False):
     rng = random.Random(seed)
     n = sum(counts)
     data_rng = np.random.default_rng(seed)
@@ -63,9 +63,9 @@ def simulate(G, counts, P, C, NB, rounds, failures=(), seed=0, start_round=0):
         want = (acc / len(alive)).astype(np.float32)
         queues = {}
         for g in range(G):
-            ops = rs.round_ops(g, G, K, NB, r)
-            queues[(g, "C")] = [o for o in ops if o[1] == "C"]
-            queues[(g, "R")] = [o for o in ops if o[1] == "R"]
+            ops = rs.round_ops(g, G, K, NB, r, late)
+            for st in ("C", "R", "F"):
+                queues[(g, st)] = [o for o in ops if o[1] == st]
             ranks[g].final_written = set()
         while any(queues.values()):
             runnable = []
@@ -119,19 +119,26 @@ def simulate(G, counts, P, C, NB, rounds, failures=(), seed=0, start_round=0):
                     x[b:e] = mean32
                 me.final_written.add(k)
                 assert ranks[fin_rank].fin_consumed[s], "fin slot overwritten before it was consumed"
-                ranks[fin_rank].fin_in[s] = ((r, k), mean32.copy())
+                # with late shards the chunk is incomplete until "finish" runs
+                ranks[fin_rank].fin_in[s] = ((r, k, "partial" if late else "final"), mean32.copy())
                 ranks[fin_rank].fin_consumed[s] = False
+            elif kind == "finish":
+                _, _, k, s, fin_rank = op
+                tag, f = ranks[fin_rank].fin_in[s]
+                assert tag == (r, k, "partial"), "finish saw the wrong chunk"
+                ranks[fin_rank].fin_in[s] = ((r, k, "final"), f)
             elif kind == "fanout":
                 _, _, k, s, fwd = op
                 b, e = bounds(k)
                 tag, f = me.fin_in[s]
-                assert tag == (r, k) and not me.fin_consumed[s], "fanout read the wrong chunk"
+                assert tag[:2] == (r, k) and not me.fin_consumed[s], "fanout read the wrong chunk"
+                assert tag[2] == "final", "fanout relayed a chunk whose late shards were not finished"
                 for x in me.rep:
                     x[b:e] = f
                 me.final_written.add(k)
                 if fwd is not None:
                     assert ranks[fwd].fin_consumed[s]
-                    ranks[fwd].fin_in[s] = ((r, k), f.copy())
+                    ranks[fwd].fin_in[s] = (tag, f.copy())
                     ranks[fwd].fin_consumed[s] = False
                 me.fin_consumed[s] = True
         for g in range(G):
@@ -141,12 +148,13 @@ def simulate(G, counts, P, C, NB, rounds, failures=(), seed=0, start_round=0):
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 @pytest.mark.parametrize("K_chunks,NB", [(1, 2), (2, 2), (5, 3), (17, 3), (9, 2)])
-def test_schedule_completes_and_is_exact(G, K_chunks, NB):
+@pytest.mark.parametrize("late", [False, True])
+def test_schedule_completes_and_is_exact(G, K_chunks, NB, late):
     counts = [2 + (g % 3) for g in range(G)]
     C = 64
     P = C * K_chunks - (7 if K_chunks > 1 else 0)
     for seed in range(3):
-        simulate(G, counts, P, C, NB, rounds=2, failures=(1,), seed=seed)
+        simulate(G, counts, P, C, NB, rounds=2, failures=(1,), seed=seed, late=late)
 
 
 def test_flag_wraparound():
@@ -154,6 +162,7 @@ def test_flag_wraparound():
     K = 4
     r0 = (0xFFFFFFFF // K) - 1
     simulate(3, [2, 1, 2], 4 * 32, 32, 2, rounds=3, seed=5, start_round=r0)
+    simulate(3, [2, 1, 2], 4 * 32, 32, 2, rounds=3, seed=6, start_round=r0, late=True)
 
 
 def test_waits_reference_earlier_work_only():
@@ -174,18 +183,19 @@ def test_rejects_single_rank_and_one_slot():
 
 @pytest.mark.parametrize("G", [2, 3, 5, 8])
 @pytest.mark.parametrize("K,NB,r", [(1, 2, 0), (7, 3, 0), (7, 3, 5), (13, 2, 2), (4, 3, (1 << 32) // 4 - 1)])
-def test_native_executor_issues_the_same_ops(G, K, NB, r):
+@pytest.mark.parametrize("late", [False, True])
+def test_native_executor_issues_the_same_ops(G, K, NB, r, late):
     """bfly_ring_round (C++) generates its ops with bfly_ring_ops' generator; it must
     equal ringsched.round_ops, the schedule the simulator above verifies."""
     import ctypes
 
     from paper_2507_17766_b200 import _lib
 
-    kinds = {"wait": 0, "write": 1, "chain": 2, "reduce": 3, "fanout": 4}
-    streams = {"C": 0, "R": 1}
+    kinds = {"wait": 0, "write": 1, "chain": 2, "reduce": 3, "fanout": 4, "finish": 5}
+    streams = {"C": 0, "R": 1, "F": 2}
     for g in range(G):
         want = []
-        for op in rs.round_ops(g, G, K, NB, r):
+        for op in rs.round_ops(g, G, K, NB, r, late):
             kind, st = op[0], op[1]
             if kind == "wait":
                 row = (kinds[kind], streams[st], g, rs.FLAGS.index(op[2]), op[3], -1, op[4])
@@ -196,7 +206,7 @@ def test_native_executor_issues_the_same_ops(G, K, NB, r):
                 row = (kinds[kind], streams[st], peer, -1, op[3], op[2], 0)
             want.append(row)
         buf = (ctypes.c_int32 * (7 * 16 * K))()
-        n = _lib.lib().bfly_ring_ops(g, G, K, NB, r & 0xFFFFFFFF, buf, 16 * K)
+        n = _lib.lib().bfly_ring_ops(g, G, K, NB, r & 0xFFFFFFFF, int(late), buf, 16 * K)
         got = [tuple(buf[7 * i:7 * i + 7]) for i in range(n)]
         got = [(a, b, c, d, e, (f if a >= 2 else -1), (h & 0xFFFFFFFF if a < 2 else 0)) for a, b, c, d, e, f, h in got]
         want = [(a, b, c, d, e, f, h & 0xFFFFFFFF) for a, b, c, d, e, f, h in want]
