@@ -106,6 +106,10 @@ typedef struct bfly_merge_args {
                                      NULL = d_src[0]                                   */
   int64_t shard_begin;            /* FINISH these shards only; 0,0 = all (the multi-GPU */
   int64_t shard_end;              /* last rank finishes each chunk's shards early)      */
+  const int32_t* d_shard_list;    /* FINISH these [n_shard_list] shards instead of the range
+                                     (device array; e.g. shards straddling chunk edges) */
+  int32_t n_shard_list;
+  int32_t pad3;
 } bfly_merge_args_t;
 
 /* ---- library ----------------------------------------------------------- */
@@ -200,6 +204,9 @@ typedef struct bfly_ring_desc {
                                     after reducing chunk k (shards inside the chunk), on
                                     stream_f, before the chunk enters the relay          */
   void* stream_f;                /* last rank: late-shard stream (with finish_ranges)  */
+  void* const* reduce_events;    /* last rank, optional: [k_chunks] cudaEvent_t (or NULL)
+                                    the C stream waits for before reducing chunk k (the
+                                    chunk's fallback values have arrived)               */
 } bfly_ring_desc_t;
 int bfly_ring_round(const bfly_ring_desc_t* desc, uint32_t round_index);
 /* The op list of one rank for one round as rows of 7 int32

@@ -97,6 +97,9 @@ class MergeArgs(ctypes.Structure):
         ("d_fallback_src", ctypes.c_void_p),
         ("shard_begin", ctypes.c_int64),
         ("shard_end", ctypes.c_int64),
+        ("d_shard_list", ctypes.c_void_p),
+        ("n_shard_list", ctypes.c_int32),
+        ("pad3", ctypes.c_int32),
     ]
 
 
@@ -126,6 +129,7 @@ class RingDesc(ctypes.Structure):
         ("stream_r", ctypes.c_void_p),
         ("finish_ranges", ctypes.c_void_p),
         ("stream_f", ctypes.c_void_p),
+        ("reduce_events", ctypes.c_void_p),
     ]
 
 

@@ -221,7 +221,13 @@ struct Params {
   int64_t ebeg, eend;    // element range of this REDUCE call
   const void* fb_src;    // replica supplying fallback values (the lowest alive miner's)
   int64_t sbeg, send;    // shard range of this FINISH call
+  const int32_t* slist;  // or this shard list
+  int32_t n_fin;         // shards of this FINISH call
 };
+
+__device__ __forceinline__ int64_t fin_shard(const Params& p, unsigned i) {
+  return p.slist ? (int64_t)p.slist[i] : p.sbeg + i;
+}
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000LL); }
 
@@ -925,7 +931,7 @@ __global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* cons
 // Pair statistics of the special shards' tiles k_reduce did not cover (tiles shared
 // by two shards, partial tiles at element-range edges, r = 3, host copies).
 __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
-  const int64_t s = p.sbeg + blockIdx.x;
+  const int64_t s = fin_shard(p, blockIdx.x);
   if (p.cls[s] != kSpecial) return;
   const int64_t start = p.bnd.start(s), hi_s = start + p.bnd.len(s);
   const int32_t* mem = p.assign + s * p.r;
@@ -990,7 +996,7 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
 
 // One warp per shard.
 __global__ void k_decide(Params p) {
-  const int64_t s = p.sbeg + blockIdx.x;
+  const int64_t s = fin_shard(p, blockIdx.x);
   if (p.cls[s] != kSpecial) return;
   const int lane = threadIdx.x;
   const int32_t* mem = p.assign + s * p.r;
@@ -1080,7 +1086,7 @@ __global__ void k_entries3(Params p) {
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
-  const int64_t s = p.sbeg + blockIdx.x;
+  const int64_t s = fin_shard(p, blockIdx.x);
   const uint8_t c = p.cls[s];
   if (c == kFast) return;
   void** s_dst = const_cast<void**>(s_ptr);
@@ -1251,7 +1257,7 @@ template <class D>
 static void launch_apply(const Params& p, cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_apply<D><<<dim3((unsigned)(p.send - p.sbeg), (unsigned)p.cps), kThreads, smem, st>>>(p);
+  k_apply<D><<<dim3((unsigned)p.n_fin, (unsigned)p.cps), kThreads, smem, st>>>(p);
 }
 
 extern "C" {
@@ -1329,6 +1335,9 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.sbeg = a->shard_begin;
   p.send = (a->shard_begin == 0 && a->shard_end == 0) ? S : a->shard_end;
   if (p.sbeg < 0 || p.send > S || p.sbeg > p.send) return fail(BFLY_E_INVALID_ARG, "bad shard range");
+  p.slist = a->d_shard_list;
+  if (p.slist && a->n_shard_list < 0) return fail(BFLY_E_INVALID_ARG, "bad shard list");
+  p.n_fin = p.slist ? a->n_shard_list : (int32_t)(p.send - p.sbeg);
   return BFLY_OK;
 }
 
@@ -1340,7 +1349,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
 
   const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
-  const bool do_finish = (a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH) && p.send > p.sbeg;
+  const bool do_finish = (a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH) && p.n_fin > 0;
   if (do_reduce) {
     if (p.ebeg == 0) {  // per-round setup runs with the first (or only) element range
       const int64_t nn = (int64_t)p.n * p.n;
@@ -1360,7 +1369,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
     }
   }
   if (do_finish) {
-    const unsigned ns = (unsigned)(p.send - p.sbeg);
+    const unsigned ns = (unsigned)p.n_fin;
     const int64_t tps = (p.bnd.base + (p.bnd.rem ? 1 : 0) + p.stile - 1) / p.stile + 1;  // tiles per shard
     const int64_t nb = (tps + kThreads - 1) / kThreads;  // tile batches per shard
     k_stats<<<dim3(ns, (unsigned)(nb < 65535 ? nb : 65535)), kThreads, 0, st>>>(p);

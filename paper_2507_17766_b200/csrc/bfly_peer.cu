@@ -240,6 +240,13 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
         double* acc_out = (double*)(d->peer_base[o.peer] + d->off_acc + (uint64_t)s * d->chunk * 8);
         result = bfly_chain_step(d->d_src_table, d->n_src, d->dtype, acc_in, acc_out, b, e, st);
       } else if (o.kind == kOpReduce) {
+        if (d->reduce_events && d->reduce_events[k]) {
+          cudaError_t ce = cudaStreamWaitEvent(st, (cudaEvent_t)d->reduce_events[k], 0);
+          if (ce != cudaSuccess) {
+            result = cuda_fail(ce, "ring reduce event");
+            break;
+          }
+        }
         args.phase = BFLY_PHASE_REDUCE;
         args.d_acc_in = (const double*)(d->peer_base[g] + d->off_acc + (uint64_t)s * d->chunk * 8);
         args.elem_begin = b;

@@ -300,6 +300,19 @@ class ButterflyMerge:
             self._args.d_dst, self._args.n_dst = saved
         return self
 
+    def run_finish_list(self, shards: torch.Tensor, stream=None):
+        """FINISH for the shards listed in ``shards`` (int32 device tensor) only."""
+        if shards.numel() == 0 or not self.needs_finish():
+            return self
+        a = self._args
+        a.phase = L.PHASE_FINISH
+        a.d_shard_list, a.n_shard_list = shards.data_ptr(), int(shards.numel())
+        try:
+            self._call(stream)
+        finally:
+            a.d_shard_list, a.n_shard_list = None, 0
+        return self
+
     def run_finish_range(self, shard_begin: int, shard_end: int, stream=None, dst_table: tuple | None = None):
         """FINISH (compare, decide, adopt / fall back, scatter back) for shards
         [shard_begin, shard_end) only."""

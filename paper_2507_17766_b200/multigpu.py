@@ -169,10 +169,15 @@ class ShardedButterflyMerge:
         # straddle a chunk boundary are finished after the ring and broadcast late.
         self._finish_ranges, straddlers = self._chunk_shard_ranges(plan.n_shards)
         self.straddlers = straddlers
+        self._straddle_dev = torch.tensor(straddlers, dtype=torch.int32, device=self.dev)
         late = [r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())] if G > 1 else runs
         self.late_runs = late
         self.special_runs = late  # kept name: ranges broadcast after the ring
-        self._fb_set = self._range_set(runs) if runs else None
+        # fallback runs split at chunk boundaries, so each chunk's values travel (and are
+        # waited for) on their own: the last rank reduces chunk k once chunk k's arrived
+        fb_runs = self._split_at_chunks(runs) if G > 1 else runs
+        self._fb_set = self._range_set(fb_runs) if runs else None
+        self._fb_chunks = self._chunk_rows(fb_runs) if runs else []
         self._late_set = self._range_set(late) if late else None
         # fallback values come from the lowest alive miner when no fallback is given
         self._needs_fb = bool(fallback is None and self.alive and runs)
@@ -240,13 +245,45 @@ class ShardedButterflyMerge:
                 straddle.append(shard_of(b))
         return ranges, sorted(set(straddle))
 
-    def _range_set(self, runs):
-        """Device table {lo, hi, packed offset} + packed buffer for element runs."""
-        tab, off = [], 0
+    def _split_at_chunks(self, runs):
+        out = []
+        for lo, hi in runs:
+            while lo < hi:
+                cut = min(hi, (lo // self.chunk + 1) * self.chunk)
+                out.append((lo, cut))
+                lo = cut
+        return out
+
+    @staticmethod
+    def _packed_offsets(runs):
+        offs, off = [], 0
         for lo, hi in runs:
             off += (lo - off) % 16  # same 32-byte alignment on both sides (vector copies)
-            tab.append((lo, hi, off))
+            offs.append(off)
             off += hi - lo
+        return offs, off
+
+    def _chunk_rows(self, runs):
+        """Fallback transfers: (first chunk, first row, end row, packed begin, packed end)
+        per group of chunks 0 | 1-2 | 3-6 | 7-14 | ... — each group travels while the
+        reduce works through the previous one, with few host calls."""
+        offs, _ = self._packed_offsets(runs)
+        rows = {}
+        for i, (lo, hi) in enumerate(runs):
+            k = lo // self.chunk
+            grp = (k + 1).bit_length() - 1  # chunks [2^j - 1, 2^(j+1) - 1)
+            r0, r1, o0, o1 = rows.get(grp, (i, i, offs[i], offs[i]))
+            rows[grp] = (r0, i + 1, o0, offs[i] + hi - lo)
+        out = []
+        for grp in sorted(rows):
+            r0 = rows[grp][0]
+            out.append((runs[r0][0] // self.chunk,) + rows[grp])
+        return out
+
+    def _range_set(self, runs):
+        """Device table {lo, hi, packed offset} + packed buffer for element runs."""
+        offs, off = self._packed_offsets(runs)
+        tab = [(lo, hi, o) for (lo, hi), o in zip(runs, offs)]
         return (torch.tensor(tab, dtype=torch.int64, device=self.dev),
                 torch.empty(off, dtype=self.local[0].dtype, device=self.dev))
 
@@ -278,6 +315,8 @@ class ShardedButterflyMerge:
         dist.barrier()
         self._relay = torch.cuda.Stream(device=self.dev)
         self._late = torch.cuda.Stream(device=self.dev)  # last rank: per-chunk late shards
+        self._fbs = torch.cuda.Stream(device=self.dev)  # last rank: fallback values in
+        self._fb_events = {k: torch.cuda.Event() for k, *_ in self._fb_chunks} if self.is_last else {}
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -441,24 +480,42 @@ class ShardedButterflyMerge:
             fb_work = None
             self._relay.wait_stream(cur)
             self._late.wait_stream(cur)
+            fb_events = None
             if self._needs_fb and self.fb_owner != last:
-                if g == self.fb_owner:
+                ranges, packed = self._fb_set
+                if g == self.fb_owner:  # packed once, sent chunk by chunk
                     self._copy_ranges(self._fb_set, self.local[self.alive[0] - self.offset].data_ptr(), None, 0, 0)
-                    fb_work = dist.isend(self._fb_set[1], dst=last)
-                elif self.is_last:  # needed only by the late-shard stream, which it precedes
-                    with torch.cuda.stream(self._late):
-                        dist.recv(self._fb_set[1], src=self.fb_owner)
-                        self._copy_ranges(self._fb_set, None, self._fb_table.data_ptr(), 1, 1)
+                    fb_work = [dist.isend(packed[o0:o1], dst=last) for _, _, _, o0, o1 in self._fb_chunks]
+                elif self.is_last:
+                    # chunk k's fallback values arrive on their own stream while the chain
+                    # runs; the reduce of chunk k (which writes predicted fallback values)
+                    # waits for them through an event
+                    self._fbs.wait_stream(cur)
+                    with torch.cuda.stream(self._fbs):
+                        for k, r0, r1, o0, o1 in self._fb_chunks:
+                            dist.recv(packed[o0:o1], src=self.fb_owner)
+                            self._copy_ranges((ranges[r0:r1], packed), None, self._fb_table.data_ptr(), 1, 1)
+                            self._fb_events[k].record(self._fbs)
+                    fb_events = self._fb_events
             mark("fallback")
             marks, window = [], []
             if not self.debug:  # native executor: the whole round issued from C++
                 self._desc.stream_c = _stream_handle()
                 self._desc.stream_r = self._relay.cuda_stream
                 self._desc.stream_f = self._late.cuda_stream
+                if fb_events:
+                    self._ev_arr = (ctypes.c_void_p * self.K)(
+                        *[fb_events[k].cuda_event if k in fb_events else None for k in range(self.K)])
+                    # one event per group, at its first chunk: the in-order C stream covers the rest
+                    self._desc.reduce_events = ctypes.cast(self._ev_arr, ctypes.c_void_p)
+                else:
+                    self._desc.reduce_events = None
                 with torch.cuda.device(self.dev):
                     L.check(L.lib().bfly_ring_round(ctypes.byref(self._desc), self._round & 0xFFFFFFFF))
             for k in range(self.K if self.debug else 0):  # debug: the same ops issued from Python
                 for op in rs.chunk_ops(g, G, self.K, NB, self._round, k, self._late_mode):
+                    if op[0] == "reduce" and fb_events and k in fb_events:
+                        cur.wait_event(fb_events[k])
                     self._issue(op)
                     if self.debug:
                         ev = torch.cuda.Event()
@@ -476,19 +533,19 @@ class ShardedButterflyMerge:
             self._marks = marks
             cur.wait_stream(self._relay)
             cur.wait_stream(self._late)
+            cur.wait_stream(self._fbs)
         self._round += 1
         mark("ring")
 
         # finish the shards that straddle chunk boundaries, then distribute the
         # per-shard results and those shards' final values
-        if fb_work is not None:
-            fb_work.wait()
+        for w in fb_work or ():
+            w.wait()
         if self.is_last:
             if G == 1:
                 self.job.run(L.PHASE_FINISH)
-            elif self.job.needs_finish():
-                for s in self.straddlers:
-                    self.job.run_finish_range(s, s + 1)
+            elif self.job.needs_finish() and self.straddlers:
+                self.job.run_finish_list(self._straddle_dev)
             pack_results(self.job.entries, self.job.source, self.job.status, self.job.flagged, self._res)
             if self.special_runs:
                 self._copy_ranges(self._late_set, self.local[0].data_ptr(), None, 0, 0)
