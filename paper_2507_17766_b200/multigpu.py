@@ -469,6 +469,9 @@ class ShardedButterflyMerge:
                 tm.append((name, ev))
 
         mark("start")
+        if self.debug == 3:  # timeline: every op's completion time from here (tools/ring_timeline.py)
+            self._t0 = torch.cuda.Event(enable_timing=True)
+            self._t0.record(cur)
         fb_work = None
         if G == 1:
             for k in range(self.K):
@@ -518,7 +521,7 @@ class ShardedButterflyMerge:
                         cur.wait_event(fb_events[k])
                     self._issue(op)
                     if self.debug:
-                        ev = torch.cuda.Event()
+                        ev = torch.cuda.Event(enable_timing=self.debug == 3)
                         ev.record({"C": cur, "R": self._relay, "F": self._late}[op[1]])
                         marks.append((op, ev))
                 # bounded run-ahead: never more than WINDOW chunks queued per stream
@@ -573,6 +576,12 @@ class ShardedButterflyMerge:
         if self.debug == 2 and G > 1:
             self._watch(self._marks)
         return self
+
+    def timeline(self) -> list:
+        """BFLY_DEBUG_RING=3: (op, ms after the round started) for every op of the last
+        round, once it has completed."""
+        torch.cuda.synchronize(self.dev)
+        return [(op, self._t0.elapsed_time(ev)) for op, ev in self._marks]
 
     def launches_per_run(self) -> int:
         """Our kernels per round on this rank (bench.py gpu_launches)."""
