@@ -168,6 +168,18 @@ int bfly_set_chain_bulk(int32_t on);
 int bfly_upload_wire(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
                      int32_t threads, void* stream);
 
+/* The drop-in merge of host payloads as one pipeline (run_all_reduce's upload +
+ * reduce stages, butterfly.py:205-240, and the copy of the merged vector back):
+ * the upload of bfly_upload_wire runs element-major in n_chunks chunks and, as
+ * each chunk lands, bfly_merge(args) reduces it (phase REDUCE over the chunk's
+ * elements; the first chunk runs the per-round setup) and args->d_merged[chunk] is
+ * copied to h_merged (NULL: no copy) while later chunks are still converting and
+ * uploading.  The caller runs phase FINISH afterwards when shards need it (and then
+ * copies those shards' merged values again). */
+int bfly_merge_host(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
+                    const bfly_merge_args_t* args, double* h_merged, int32_t n_chunks, int32_t threads,
+                    void* stream);
+
 /* ---- peer memory for the multi-GPU merge (one process per GPU, one node) ---- */
 /* cudaMalloc a zero-filled region and export its CUDA IPC handle (64 bytes). */
 int bfly_ipc_alloc(size_t bytes, void** d_ptr, uint8_t handle[64]);

@@ -46,6 +46,7 @@ EXPORTS = (
     "bfly_stream_wait_value",
     "bfly_stream_write_value",
     "bfly_upload_wire",
+    "bfly_merge_host",
     "bfly_ring_round",
     "bfly_ring_ops",
 )
@@ -171,6 +172,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
+    L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
     L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]

@@ -259,6 +259,7 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
 
     # -- device merge ------------------------------------------------------
     reps = [None] * n
+    pipelined = False
     host_f64 = [m for m in alive if not isinstance(payloads[miners[m]], torch.Tensor)]
     if host_f64 and len(host_f64) == len(alive):
         # host payloads: the upload stage's "<f4" serialisation (butterfly.py:213) runs on
@@ -267,7 +268,11 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         wire = [torch.empty(P, dtype=torch.float32, device=dev) for _ in alive]
         h_ptrs = (ctypes.c_void_p * len(alive))(*[h.ctypes.data for h in hosts])
         d_ptrs = (ctypes.c_void_p * len(alive))(*[t.data_ptr() for t in wire])
-        L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _stream_handle()))
+        # without host callables the upload, the reduce and the copy of the merged
+        # vector back run as one pipeline (bfly_merge_host) once the job exists
+        pipelined = not callables
+        if not pipelined:
+            L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _stream_handle()))
         for m, t in zip(alive, wire):
             reps[m] = t
         unmerged_possible = len(failed) >= 2 or bool(descriptors) or bool(callables)
@@ -310,14 +315,24 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
                         raise ShapeError(f"reduction shapes differ: {arr.shape} vs {(hi - lo,)}")
                     raise ValueError(f"could not broadcast reduction of shape {arr.shape} into ({hi - lo},)")
         job.run(L.PHASE_FINISH, host_copies=torch.from_numpy(host_copies).to(dev))
+    elif pipelined:
+        # merged values stream back chunk by chunk unless FINISH may still change them
+        early = not _device_merged and not job.needs_finish()
+        merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True) if early else None  # cached pinned
+        L.check(L.lib().bfly_merge_host(h_ptrs, len(alive), P, d_ptrs, ctypes.byref(job._args),
+                                        merged_host.data_ptr() if early else None, _merge_chunks(P), 0,
+                                        _stream_handle()))
+        if job.needs_finish():
+            job.run(L.PHASE_FINISH)
     else:
         job.run(L.PHASE_ALL)
 
     if _device_merged:  # stage glue (stage.py): the merged weights stay in HBM
         merged = job.merged
     else:
-        merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
-        merged_host.copy_(job.merged, non_blocking=True)
+        if not (pipelined and early):
+            merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
+            merged_host.copy_(job.merged, non_blocking=True)
         merged = merged_host.numpy()  # the array keeps the pinned tensor alive
     status_codes = job.status.cpu().numpy()
     entries = job.entries.cpu().numpy()
@@ -336,6 +351,11 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         agreement_matrix=AgreementMatrix(n_miners=n, entries=entries),
         flagged={miners[i] for i in flagged_idx},
     )
+
+
+def _merge_chunks(P: int) -> int:
+    """Pipeline depth of bfly_merge_host: chunks of >= 4M elements, at most 32."""
+    return max(1, min(32, P >> 22))
 
 
 def _chunk(size: int, start: int, length: int | None) -> int:

@@ -4,18 +4,21 @@
 // The reference's upload stage serialises every surviving miner's payload as
 // "<f4" bytes (butterfly.py:213, payload.astype("<f4").tobytes()).  Doing that
 // conversion on the host halves the PCIe bytes (4 B instead of 8 B per weight).
-// The conversion runs on a team of host threads into a ring of pinned staging
-// slots, and each slot is copied to the device asynchronously while the next one
-// is being converted, so conversion and PCIe overlap.  Rounding is IEEE
-// round-to-nearest-even, the same as numpy's astype.
+// The conversion runs on a team of host threads, each with its own ring of small
+// pinned staging slots and its own copy stream, so conversion and PCIe overlap
+// and the staging stays cache-resident.  Rounding is IEEE round-to-nearest-even,
+// the same as numpy's astype.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
+#include <memory>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -25,109 +28,70 @@ namespace bfly {
 
 namespace {
 
-constexpr int kSlots = 4;
-constexpr int64_t kSlotElems = 1 << 22;  // 16 MB of fp32 per slot
-
-struct Staging {
-  float* slot[kSlots] = {};
-  cudaEvent_t done[kSlots] = {};
-  int device = -1;
+// Each worker thread owns a small ring of pinned slots and its own copy stream:
+// it converts one block of one payload into a slot and queues that slot's H2D copy
+// itself, so no thread ever waits for another.  Blocks are small enough that the
+// ring's lines are still in the host's last-level cache when the copy engine reads
+// them back: the host memory traffic stays near the 8 B/element of the fp64 read.
+struct Worker {
+  std::vector<float*> slot;
+  std::vector<cudaEvent_t> done;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fin = nullptr;
 };
 
-std::mutex g_staging_mu;
-std::vector<Staging*> g_staging;  // one ring per device, kept for the process lifetime
+struct Pool {
+  int device = -1;
+  int64_t block = 0;
+  int ring = 0;
+  std::vector<Worker> workers;
+};
 
-int get_staging(Staging** out) {
+std::mutex g_pool_mu;
+std::vector<Pool*> g_pools;  // one per (device, shape), kept for the process lifetime
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoll(v) : dflt;
+}
+
+int get_pool(int threads, Pool** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  std::lock_guard<std::mutex> lk(g_staging_mu);
-  for (Staging* s : g_staging)
-    if (s->device == dev) {
-      *out = s;
+  const int64_t block = env_int("BFLY_UPLOAD_BLOCK", 1 << 19);  // 2 MB copies: tools/upload_probe.py
+  const int ring = (int)env_int("BFLY_UPLOAD_RING", 3);
+  if (block < 1024 || ring < 2) return fail(BFLY_E_INVALID_ARG, "bad BFLY_UPLOAD_BLOCK / BFLY_UPLOAD_RING");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (Pool* p : g_pools)
+    if (p->device == dev && p->block == block && p->ring == ring && (int)p->workers.size() >= threads) {
+      *out = p;
       return BFLY_OK;
     }
-  Staging* s = new Staging();
-  s->device = dev;
-  for (int i = 0; i < kSlots; ++i) {
-    e = cudaHostAlloc((void**)&s->slot[i], sizeof(float) * kSlotElems, cudaHostAllocPortable);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc staging");
-    e = cudaEventCreateWithFlags(&s->done[i], cudaEventDisableTiming);
+  Pool* p = new Pool();
+  p->device = dev;
+  p->block = block;
+  p->ring = ring;
+  p->workers.resize(threads);
+  for (Worker& w : p->workers) {
+    w.slot.resize(ring);
+    w.done.resize(ring);
+    for (int i = 0; i < ring; ++i) {
+      e = cudaHostAlloc((void**)&w.slot[i], sizeof(float) * block, cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc staging");
+      e = cudaEventCreateWithFlags(&w.done[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+    }
+    e = cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    e = cudaEventCreateWithFlags(&w.fin, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
-    e = cudaEventRecord(s->done[i], 0);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    for (int i = 0; i < ring; ++i) cudaEventRecord(w.done[i], w.stream);
   }
-  g_staging.push_back(s);
-  *out = s;
+  g_pools.push_back(p);
+  *out = p;
   return BFLY_OK;
 }
-
-// Fork-join team: the calling thread hands out one unit at a time and works on
-// its own share; the team converts [begin, end) of src into dst.
-class Team {
- public:
-  explicit Team(int n) : n_(n) {
-    for (int t = 1; t < n_; ++t) threads_.emplace_back([this, t] { loop(t); });
-  }
-  ~Team() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
-    }
-    cv_.notify_all();
-    for (auto& th : threads_) th.join();
-  }
-  void convert(const double* src, float* dst, int64_t len) {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      src_ = src;
-      dst_ = dst;
-      len_ = len;
-      pending_ = n_ - 1;
-      ++gen_;
-    }
-    cv_.notify_all();
-    work(0);
-    std::unique_lock<std::mutex> lk(mu_);
-    done_cv_.wait(lk, [this] { return pending_ == 0; });
-  }
-
- private:
-  void work(int t) {
-    const int64_t per = (len_ + n_ - 1) / n_;
-    const int64_t b = std::min<int64_t>(len_, per * t), e = std::min<int64_t>(len_, b + per);
-    const double* s = src_;
-    float* d = dst_;
-    for (int64_t i = b; i < e; ++i) d[i] = (float)s[i];
-  }
-  void loop(int t) {
-    uint64_t seen = 0;
-    for (;;) {
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
-        if (stop_) return;
-      }
-      work(t);
-      {
-        std::lock_guard<std::mutex> lk(mu_);
-        if (--pending_ == 0) done_cv_.notify_one();
-      }
-    }
-  }
-  int n_;
-  std::vector<std::thread> threads_;
-  std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  uint64_t gen_ = 0;
-  int pending_ = 0;
-  bool stop_ = false;
-  const double* src_ = nullptr;
-  float* dst_ = nullptr;
-  int64_t len_ = 0;
-};
 
 }  // namespace
 }  // namespace bfly
@@ -138,25 +102,162 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
                                 int32_t threads, void* stream) {
   if (!h_payloads || !d_wire || n < 0 || P < 0) return fail(BFLY_E_INVALID_ARG, "bad upload arguments");
   if (n == 0 || P == 0) return BFLY_OK;
-  Staging* stg = nullptr;
-  int rc = get_staging(&stg);
-  if (rc) return rc;
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
-  Team team(threads);
+  Pool* pool = nullptr;
+  int rc = get_pool(threads, &pool);
+  if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  int slot = 0;
-  for (int32_t m = 0; m < n; ++m) {
-    for (int64_t b = 0; b < P; b += kSlotElems) {
-      const int64_t len = std::min<int64_t>(kSlotElems, P - b);
-      cudaError_t e = cudaEventSynchronize(stg->done[slot]);  // the slot's previous copy has left
-      if (e != cudaSuccess) return cuda_fail(e, "staging event");
-      team.convert(h_payloads[m] + b, stg->slot[slot], len);
-      e = cudaMemcpyAsync(d_wire[m] + b, stg->slot[slot], sizeof(float) * len, cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) return cuda_fail(e, "staging H2D");
-      e = cudaEventRecord(stg->done[slot], st);
-      if (e != cudaSuccess) return cuda_fail(e, "staging record");
-      slot = (slot + 1) % kSlots;
+  // the copies must not start before work already queued on the caller's stream
+  // (e.g. a previous round still reading the destination buffers)
+  cudaEvent_t start;
+  cudaError_t e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  cudaEventRecord(start, st);
+  const int64_t B = pool->block, per = (P + B - 1) / B, total = per * (int64_t)n;
+  std::atomic<int64_t> next{0};
+  std::atomic<int> err{BFLY_OK};
+  std::string err_msg;
+  std::mutex err_mu;
+  auto body = [&](int t) {
+    Worker& w = pool->workers[t];
+    cudaSetDevice(pool->device);
+    cudaStreamWaitEvent(w.stream, start, 0);
+    int64_t count = 0;
+    for (int64_t id = next.fetch_add(1); id < total && err.load() == BFLY_OK; id = next.fetch_add(1)) {
+      const int32_t m = (int32_t)(id / per);
+      const int64_t b = (id % per) * B, len = std::min<int64_t>(B, P - b);
+      const int k = (int)(count++ % pool->ring);
+      cudaError_t ce = cudaEventSynchronize(w.done[k]);  // the slot's previous copy has left
+      if (ce == cudaSuccess) {
+        const double* src = h_payloads[m] + b;
+        float* dst = w.slot[k];
+        for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];  // RNE, as numpy's astype
+        ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
+      }
+      if (ce == cudaSuccess) ce = cudaEventRecord(w.done[k], w.stream);
+      if (ce != cudaSuccess) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        err_msg = cudaGetErrorString(ce);
+        err.store(BFLY_E_CUDA);
+      }
+    }
+    cudaEventRecord(w.fin, w.stream);
+  };
+  std::vector<std::thread> team;
+  for (int t = 1; t < threads; ++t) team.emplace_back(body, t);
+  body(0);
+  for (auto& th : team) th.join();
+  for (int t = 0; t < threads; ++t) cudaStreamWaitEvent(st, pool->workers[t].fin, 0);
+  cudaEventDestroy(start);
+  if (err.load() != BFLY_OK) return fail(BFLY_E_CUDA, "upload: " + err_msg);
+  return BFLY_OK;
+}
+
+// The drop-in merge of host payloads as one pipeline: the upload runs element-major
+// in chunks; as soon as every worker has queued its copies of chunk c, the calling
+// thread reduces chunk c on the device and copies its merged values back, while the
+// workers convert and upload the next chunks (PCIe is full duplex).
+extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
+                               const bfly_merge_args_t* args, double* h_merged, int32_t n_chunks, int32_t threads,
+                               void* stream) {
+  if (!h_payloads || !d_wire || !args || n < 1 || P < 1 || n_chunks < 1)
+    return fail(BFLY_E_INVALID_ARG, "bad merge-host arguments");
+  if (h_merged && !args->d_merged) return fail(BFLY_E_INVALID_ARG, "h_merged needs d_merged");
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  Pool* pool = nullptr;
+  int rc = get_pool(threads, &pool);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t B = pool->block;
+  int64_t CL = (P + n_chunks - 1) / n_chunks;
+  CL = (CL + B - 1) / B * B;  // chunk = whole blocks
+  const int NC = (int)((P + CL - 1) / CL);
+  const int64_t bpc = CL / B;  // blocks per full chunk and miner
+  auto chunk_len = [&](int c) { return std::min<int64_t>(CL, P - (int64_t)c * CL); };
+  // block ids: chunk-major, then miner, then block within the chunk
+  std::vector<int64_t> first_id(NC + 1, 0);
+  for (int c = 0; c < NC; ++c) first_id[c + 1] = first_id[c] + (int64_t)n * ((chunk_len(c) + B - 1) / B);
+  const int64_t total = first_id[NC];
+
+  std::vector<cudaEvent_t> ev((size_t)threads * NC);
+  for (auto& e : ev) {
+    cudaError_t ce = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaEventCreate");
+  }
+  cudaEvent_t start;
+  cudaError_t e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+  cudaEventRecord(start, st);
+  std::unique_ptr<std::atomic<int>[]> queued(new std::atomic<int>[NC]);
+  for (int c = 0; c < NC; ++c) queued[c].store(0);
+  std::atomic<int64_t> next{0};
+  std::atomic<int> err{BFLY_OK};
+  std::string err_msg;
+  std::mutex err_mu;
+  auto set_err = [&](cudaError_t ce) {
+    std::lock_guard<std::mutex> lk(err_mu);
+    err_msg = cudaGetErrorString(ce);
+    err.store(BFLY_E_CUDA);
+  };
+  auto worker = [&](int t) {
+    Worker& w = pool->workers[t];
+    cudaSetDevice(pool->device);
+    cudaStreamWaitEvent(w.stream, start, 0);
+    int64_t count = 0;
+    int cur = 0;  // chunks below `cur` are fully queued by this worker
+    auto pass = [&](int upto) {  // mark chunks [cur, upto) queued on this worker's stream
+      for (; cur < upto; ++cur) {
+        cudaEventRecord(ev[(size_t)t * NC + cur], w.stream);
+        queued[cur].fetch_add(1);
+      }
+    };
+    for (int64_t id = next.fetch_add(1); id < total; id = next.fetch_add(1)) {
+      int c = cur;
+      while (id >= first_id[c + 1]) ++c;
+      pass(c);
+      if (err.load() != BFLY_OK) continue;
+      const int64_t local = id - first_id[c], nb = (chunk_len(c) + B - 1) / B;
+      const int32_t m = (int32_t)(local / nb);
+      const int64_t b = (int64_t)c * CL + (local % nb) * B;
+      const int64_t len = std::min<int64_t>(B, (int64_t)c * CL + chunk_len(c) - b);
+      const int k = (int)(count++ % pool->ring);
+      cudaError_t ce = cudaEventSynchronize(w.done[k]);
+      if (ce == cudaSuccess) {
+        const double* src = h_payloads[m] + b;
+        float* dst = w.slot[k];
+        for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];  // RNE, as numpy's astype
+        ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
+      }
+      if (ce == cudaSuccess) ce = cudaEventRecord(w.done[k], w.stream);
+      if (ce != cudaSuccess) set_err(ce);
+    }
+    pass(NC);
+  };
+  (void)bpc;
+  std::vector<std::thread> team;
+  for (int t = 0; t < threads; ++t) team.emplace_back(worker, t);
+  bfly_merge_args_t a = *args;
+  a.phase = BFLY_PHASE_REDUCE;
+  a.shard_begin = a.shard_end = 0;
+  a.d_shard_list = nullptr;
+  a.n_shard_list = 0;
+  int result = BFLY_OK;
+  for (int c = 0; c < NC; ++c) {
+    while (queued[c].load() < threads) std::this_thread::yield();
+    if (result != BFLY_OK || err.load() != BFLY_OK) continue;
+    for (int t = 0; t < threads; ++t) cudaStreamWaitEvent(st, ev[(size_t)t * NC + c], 0);
+    a.elem_begin = (int64_t)c * CL;
+    a.elem_end = a.elem_begin + chunk_len(c);
+    result = bfly_merge(&a, st);
+    if (result == BFLY_OK && h_merged) {
+      cudaError_t ce = cudaMemcpyAsync(h_merged + a.elem_begin, args->d_merged + a.elem_begin,
+                                       sizeof(double) * chunk_len(c), cudaMemcpyDeviceToHost, st);
+      if (ce != cudaSuccess) result = cuda_fail(ce, "merged D2H");
     }
   }
-  return BFLY_OK;
+  for (auto& th : team) th.join();
+  for (auto& x : ev) cudaEventDestroy(x);
+  cudaEventDestroy(start);
+  if (err.load() != BFLY_OK) return fail(BFLY_E_CUDA, "upload: " + err_msg);
+  return result;
 }
