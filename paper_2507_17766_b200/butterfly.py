@@ -20,6 +20,7 @@ There is no CPU fallback: without a CUDA device these functions raise.
 from __future__ import annotations
 
 import ctypes
+import os
 import json
 import math
 from dataclasses import dataclass, field
@@ -354,8 +355,10 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
 
 
 def _merge_chunks(P: int) -> int:
-    """Pipeline depth of bfly_merge_host: chunks of >= 4M elements, at most 32."""
-    return max(1, min(32, P >> 22))
+    """Pipeline depth of bfly_merge_host: chunks of >= 4M elements, at most 32
+    (BFLY_MERGE_CHUNKS overrides)."""
+    forced = os.environ.get("BFLY_MERGE_CHUNKS")
+    return int(forced) if forced else max(1, min(32, P >> 22))
 
 
 def _chunk(size: int, start: int, length: int | None) -> int:

@@ -154,8 +154,30 @@ CASES = [
 ]
 
 
+# Shards of many k_reduce tiles: the reduce writes each special shard's predicted outcome
+# and accumulates its pair statistics itself (r = 2); mispredictions (a zero `add`, a unit
+# `scale`, colluders sharing a noise key all agree) are rewritten by k_apply.
+LONG_CASES = [
+    (4, (1 << 20) + 77, 2, "f32", (), {1: (orc.NOISE, 2.0, 5, 6)}, False),
+    (6, (1 << 20) + 5, 2, "f32", (0,), {2: (orc.ADD, 0.0), 3: (orc.SCALE, 1.0), 4: (orc.NOISE, 1.0, 7, 7),
+                                        5: (orc.NOISE, 1.0, 7, 7)}, True),
+    (6, (1 << 20) + 5, 2, "f32", (), {2: (orc.ADD, 0.0), 4: (orc.NOISE, 1.0, 7, 7), 5: (orc.NOISE, 1.0, 7, 7)},
+     False),
+    (5, (1 << 19) + 11, 2, "bf16", (), {1: (orc.NOISE_ADD, 0.01, 3, 4)}, True),
+    (4, (1 << 18) + 3, 2, "f64", (3,), {2: (orc.SCALE, 2.0)}, False),
+    (7, 35 * 4096 + 3, 3, "f32", (1,), {2: (orc.NOISE, 1.0, 3, 4)}, True),   # r=3: predicted means
+    (7, 35 * 4096 + 3, 3, "f32", (), {2: (orc.NOISE, 1.0, 3, 4), 4: (orc.ADD, 0.0)}, False),
+]
+
+
+@pytest.mark.parametrize("keep_means", [False, True], ids=["ws_in_merged", "ws_apart"])
+@pytest.mark.parametrize("case", LONG_CASES, ids=lambda c: f"n{c[0]}_P{c[1]}_r{c[2]}_{c[3]}")
+def test_device_merge_long_shards_match_oracle(cuda_device, case, keep_means):
+    test_device_merge_matches_oracle(cuda_device, case, keep_means)
+
+
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"n{c[0]}_P{c[1]}_r{c[2]}_{c[3]}")
-def test_device_merge_matches_oracle(cuda_device, case):
+def test_device_merge_matches_oracle(cuda_device, case, keep_means=False):
     from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
 
     n, P, r, dtype, failures, specs, use_fb = case
@@ -172,7 +194,7 @@ def test_device_merge_matches_oracle(cuda_device, case):
     dreps = _to_torch(reps, dtype, cuda_device)
     job = ButterflyMerge(dreps, plan, failures=failures, corruptions=_descriptors(specs),
                          fallback=None if fb is None else torch.from_numpy(fb).to(cuda_device),
-                         scatter_back=True, want_merged=True)
+                         scatter_back=True, want_merged=True, keep_means=keep_means)
     job.run()
     torch.cuda.synchronize()
     assert_same_floats(job.merged.cpu().numpy(), want["merged"])
@@ -206,3 +228,29 @@ def test_agreement_and_mean_reducer_gpu(cuda_device):
     for rows, width in ((1, 1), (7, 1), (9, 1), (200, 1), (3, 5), (64, 1001)):
         x = (rng.uniform(-1, 1, (rows, width)) * 10.0 ** rng.integers(-8, 8, (rows, width)))
         assert_same_floats(bf.mean_reducer(x), x.mean(axis=0))
+
+
+@pytest.mark.parametrize("with_bad", [False, True], ids=["honest", "failures_and_corruptions"])
+def test_pipelined_host_merge_matches_oracle(cuda_device, monkeypatch, with_bad):
+    """bfly_merge_host with several chunks (small staging blocks): the upload, the
+    per-chunk reduce and the per-chunk copy back agree with the oracle bit for bit."""
+    from paper_2507_17766_b200 import butterfly as bf
+    from paper_2507_17766_b200.device import Corruption
+    from paper_2507_17766_b200.simkernel import BlobStore
+
+    monkeypatch.setenv("BFLY_UPLOAD_BLOCK", "4096")
+    monkeypatch.setenv("BFLY_MERGE_CHUNKS", "7")
+    n, P = 6, 100_003
+    rng = np.random.default_rng(77)
+    payloads = [rng.uniform(-1, 1, P) * 10.0 ** rng.integers(-3, 3) for _ in range(n)]
+    plan = bf.plan_shards(bf.enumerate_pairs(n), P, bf.BYTES_PER_WEIGHT, 5)
+    failures = (4,) if with_bad else ()
+    specs = {1: (orc.NOISE, 1.0, 3, 4)} if with_bad else {}
+    corr = {m: Corruption(KIND[s[0]], s[1], (s[2], s[3])) for m, s in specs.items()}
+    res = bf.run_all_reduce(BlobStore(), {f"m{k}": payloads[k] for k in range(n)}, plan,
+                            failures=frozenset(failures), corruptions=corr)
+    assign = np.array(plan.assignment, dtype=np.int32)
+    bounds = np.array([b for b, _ in plan.bounds] + [P], dtype=np.int64)
+    want = orc.merge(payloads, assign, bounds, failures=failures, corruptions=specs, dtype=orc.F64WIRE)
+    assert_same_floats(res.merged, want["merged"])
+    assert res.shard_status == [("merged", "lost", "disagreement")[c] for c in want["status"]]
