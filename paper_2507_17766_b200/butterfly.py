@@ -170,23 +170,31 @@ def mean_reducer(stack):
 
 
 class _LazyBlob:
-    """Store object whose bytes are produced on first read (sizes are exact up front)."""
+    """Store object whose bytes are produced on first read (sizes are exact up front).
 
-    __slots__ = ("_n", "_make", "_data")
+    Objects of the merge are views of device-resident vectors in the "<f4" wire format:
+    a ranged read (``blob[a:b]``, what ``BlobStore.get(actor, key, start, length)``
+    does) copies only those elements back when a ``part`` reader is given; anything
+    else materialises the whole object once."""
 
-    def __init__(self, nbytes: int, make):
-        self._n, self._make, self._data = nbytes, make, None
+    __slots__ = ("_n", "_make", "_data", "_part")
+
+    def __init__(self, nbytes: int, make, part=None):
+        self._n, self._make, self._data, self._part = nbytes, make, None, part
 
     def _bytes(self) -> bytes:
         if self._data is None:
             self._data = bytes(self._make())
-            self._make = None
+            self._make = self._part = None
         return self._data
 
     def __len__(self):
         return self._n
 
     def __getitem__(self, item):
+        if self._data is None and self._part is not None and isinstance(item, slice) and item.step in (None, 1):
+            start, stop, _ = item.indices(self._n)
+            return self._part(start, stop) if stop > start else b""
         return self._bytes()[item]
 
     def __bytes__(self):
@@ -196,6 +204,25 @@ class _LazyBlob:
         return self._bytes() == bytes(other)
 
     __hash__ = None
+
+
+def _wire_part(values, header: bytes = b""):
+    """Ranged reader of ``header + values.astype("<f4")`` for a 1-D float vector
+    (device tensor or numpy): only the elements under [start, stop) are copied."""
+    h = len(header)
+
+    def part(start: int, stop: int) -> bytes:
+        out = header[start:stop] if start < h else b""
+        a, b = max(start, h) - h, stop - h
+        if b > a:
+            e0, e1 = a // 4, (b + 3) // 4
+            chunk = values[e0:e1]
+            if isinstance(chunk, torch.Tensor):
+                chunk = chunk.detach().to("cpu", torch.float64).numpy()
+            raw = np.asarray(chunk, dtype=np.float64).astype("<f4").tobytes()
+            out += raw[a - 4 * e0:b - 4 * e0]
+        return out
+    return part
 
 
 def _meter(store, actor: str) -> object:
@@ -380,7 +407,7 @@ def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, me
     for m in alive:  # upload stage
         key = f"{prefix}/miner/{miners[m]}/weights"
         src = payloads[miners[m]]
-        objects[key] = _LazyBlob(wsize, lambda src=src: _wire_bytes(src))
+        objects[key] = _LazyBlob(wsize, lambda src=src: _wire_bytes(src), _wire_part(src))
         _meter(store, str(miners[m])).bytes_uploaded += _wire(store, wsize)
         weight_keys[m] = key
     for s, (i, j) in enumerate(plan.assignment):  # reduce stage
@@ -393,11 +420,11 @@ def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, me
             if (s, x) in host_reductions:
                 red = np.asarray(host_reductions[(s, x)])
                 nbytes = 4 * red.size
-                make = (lambda red=red: red.astype("<f4").tobytes())
+                make, part = (lambda red=red: red.astype("<f4").tobytes()), None
             else:
                 nbytes = 4 * (hi - lo)
-                make = _reduction_maker(job, x, lo, hi, merged, special[s], descriptors)
-            objects[f"{prefix}/miner/{miners[x]}/merged/{s}"] = _LazyBlob(nbytes, make)
+                make, part = _reduction_maker(job, x, lo, hi, merged, special[s], descriptors)
+            objects[f"{prefix}/miner/{miners[x]}/merged/{s}"] = _LazyBlob(nbytes, make, part)
             mt.bytes_uploaded += _wire(store, nbytes)
     for m in alive:  # redistribution stage (metering only)
         mt = _meter(store, str(miners[m]))
@@ -423,20 +450,24 @@ def _wire_bytes(src) -> bytes:
 
 
 def _reduction_maker(job, x, lo, hi, merged, special, descriptors):
-    """Bytes of assignee x's re-uploaded reduction ("<f4", butterfly.py:235-240)."""
+    """(whole, ranged) readers of assignee x's re-uploaded reduction ("<f4",
+    butterfly.py:235-240)."""
     if not special:  # all survivors honest: every reduction equals the merged mean
-        return lambda: _host(merged[lo:hi]).astype("<f4").tobytes()
+        return (lambda: _host(merged[lo:hi]).astype("<f4").tobytes()), _wire_part(merged[lo:hi])
 
-    def make():
-        mean = job.means[lo:hi]
-        if x in descriptors:
-            out = torch.empty_like(mean)
-            desc = descriptors[x].struct()
-            L.check(L.lib().bfly_apply_corruption(desc, mean.data_ptr(), lo, hi - lo, out.data_ptr(),
-                                                  _stream_handle()))
-            mean = out
-        return mean.cpu().numpy().astype("<f4").tobytes()
-    return make
+    class _Copy:  # element range of the assignee's copy, computed on the device on demand
+        def __getitem__(self, sl):
+            a, b = lo + sl.start, lo + min(sl.stop, hi - lo)
+            mean = job.means[a:b]
+            if x in descriptors:
+                out = torch.empty_like(mean)
+                L.check(L.lib().bfly_apply_corruption(descriptors[x].struct(), mean.data_ptr(), a, b - a,
+                                                      out.data_ptr(), _stream_handle()))
+                mean = out
+            return mean
+
+    copy = _Copy()
+    return (lambda: _host(copy[0:hi - lo]).astype("<f4").tobytes()), _wire_part(copy)
 
 
 # ---------------------------------------------------------------------------

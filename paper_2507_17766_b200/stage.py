@@ -98,7 +98,8 @@ def _merge_layer(store, layer: StageLayer, seed: int, epoch: int, stage_label: s
         def blob(w=merged, L=L, d_in=d_in, d_out=d_out):
             return _HEADER.pack(L, d_in, d_out, 0) + w.detach().cpu().numpy().astype("<f4").tobytes()
 
-        store.objects[f"{prefix}/miner/{lone}/weights"] = bf._LazyBlob(nbytes, blob)
+        store.objects[f"{prefix}/miner/{lone}/weights"] = bf._LazyBlob(
+            nbytes, blob, bf._wire_part(merged, _HEADER.pack(L, d_in, d_out, 0)))
         bf._meter(store, lone).bytes_uploaded += _wire(store, nbytes)
         for m in roster:
             if m.miner_id != lone:
@@ -121,7 +122,8 @@ def _merge_layer(store, layer: StageLayer, seed: int, epoch: int, stage_label: s
         merged = res.merged
         # non-participants copy the consolidated merged state (orchestrator.py:575-579)
         key = f"{prefix}/merged-weights"
-        store.objects[key] = bf._LazyBlob(4 * P, lambda w=merged: w.detach().cpu().numpy().astype("<f4").tobytes())
+        store.objects[key] = bf._LazyBlob(4 * P, lambda w=merged: w.detach().cpu().numpy().astype("<f4").tobytes(),
+                                          bf._wire_part(merged))
         bf._meter(store, "orchestrator").bytes_uploaded += _wire(store, 4 * P)
         for m in roster:
             if m.miner_id not in index_of:

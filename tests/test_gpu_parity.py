@@ -254,3 +254,28 @@ def test_pipelined_host_merge_matches_oracle(cuda_device, monkeypatch, with_bad)
     want = orc.merge(payloads, assign, bounds, failures=failures, corruptions=specs, dtype=orc.F64WIRE)
     assert_same_floats(res.merged, want["merged"])
     assert res.shard_status == [("merged", "lost", "disagreement")[c] for c in want["status"]]
+
+
+def test_store_objects_ranged_reads_gpu(cuda_device):
+    """Every store object of a merge with a device-corrupted assignee: ranged reads
+    (copied back range by range from HBM) equal slices of the whole object."""
+    from paper_2507_17766_b200 import butterfly as bf
+    from paper_2507_17766_b200.device import Corruption
+    from paper_2507_17766_b200.simkernel import BlobStore
+
+    n, P = 5, 10_007
+    rng = np.random.default_rng(5)
+    payloads = {f"m{k}": rng.uniform(-1, 1, P) for k in range(n)}
+    plan = bf.plan_shards(bf.enumerate_pairs(n), P, bf.BYTES_PER_WEIGHT, 9)
+    store = BlobStore()
+    bf.run_all_reduce(store, payloads, plan, corruptions={2: Corruption.noise(1.0, (4, 5))})
+    for key, obj in store.objects.items():
+        if not isinstance(obj, bf._LazyBlob):
+            continue
+        size = len(obj)
+        cuts = [(0, 5), (3, 9), (size // 3, size // 3 + 101), (size - 6, size)]
+        parts = [obj[a:b] for a, b in cuts]
+        whole = bytes(obj)
+        assert len(whole) == size
+        for (a, b), got in zip(cuts, parts):
+            assert got == whole[a:b], (key, a, b)
