@@ -112,6 +112,18 @@ typedef struct bfly_merge_args {
   int32_t pad3;
 } bfly_merge_args_t;
 
+/* ---- validator replay checks ---------------------- */
+/* For each of n_pairs (recomputed, reported) activation pairs, packed back to back in
+ * d_rec / d_rep with pair i at [d_offsets[i], d_offsets[i+1]): the reference's
+ * replay check `_check` (validator.py:148-167) — cosine similarity (validator.py:33-46),
+ * then 0 if below h_policy[0] (cosine_threshold), if the norm ratio |rep|/|rec| is
+ * outside [h_policy[1], h_policy[2]] (magnitude band, only when |rec| > 0), or if
+ * max|rec - rep| / max(|rec|, 1) > h_policy[3] (max_rel_deviation).  d_sim[i] gets
+ * the similarity, d_cos[i] (optional) the plain cosine.  Shapes are the caller's
+ * business (ShapeError is raised on the host). */
+int bfly_replay_check(const double* d_rec, const double* d_rep, const int64_t* d_offsets, int32_t n_pairs,
+                      const double* h_policy, double* d_sim, double* d_cos, void* stream);
+
 /* ---- library ----------------------------------------------------------- */
 const char* bfly_version(void);
 const char* bfly_last_error(void);

@@ -11,6 +11,7 @@ algorithm.  ``philox_key`` uses hashlib exactly like simkernel.py:203-205.
 from __future__ import annotations
 
 import ctypes
+import math
 import hashlib
 import os
 import subprocess
@@ -168,3 +169,43 @@ def threads_available() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------- validator replay checks
+# (test infrastructure like the rest of this module)
+
+
+def cosine_similarity(a, b) -> float:
+    """validator.cosine_similarity (validator.py:33-46): a.b / (|a| |b|) with |x| =
+    sqrt(x.x); two zero vectors -> 1.0, exactly one zero vector -> 0.0."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    with np.errstate(all="ignore"):
+        na, nb = math.sqrt(float(np.dot(a, a))), math.sqrt(float(np.dot(b, b)))
+        if na == 0.0 and nb == 0.0:
+            return 1.0
+        if na == 0.0 or nb == 0.0:
+            return 0.0
+        return float(np.dot(a, b)) / (na * nb)
+
+
+def replay_check(recomputed, reported, policy) -> float:
+    """validator._check (validator.py:148-167) for policy = (cosine_threshold,
+    magnitude_low, magnitude_high, max_rel_deviation): the cosine, or 0.0 when it is
+    below the threshold, when the norm ratio leaves the band (only if |rec| > 0), or
+    when the largest deviation relative to max(|rec|, 1) exceeds the limit."""
+    thr, lo, hi, max_rel = policy
+    rec = np.asarray(recomputed, dtype=np.float64)
+    rep = np.asarray(reported, dtype=np.float64)
+    sim = cosine_similarity(rec, rep)
+    if sim < thr:
+        return 0.0
+    with np.errstate(all="ignore"):
+        n_rec, n_rep = math.sqrt(float(np.dot(rec, rec))), math.sqrt(float(np.dot(rep, rep)))
+        if n_rec > 0.0 and not (lo <= n_rep / n_rec <= hi):
+            return 0.0
+        dev = np.abs(rec - rep) / np.maximum(np.abs(rec), 1.0)
+        worst = float(np.max(dev)) if dev.size else 0.0
+    if worst > max_rel:
+        return 0.0
+    return sim

@@ -47,6 +47,7 @@ EXPORTS = (
     "bfly_stream_write_value",
     "bfly_upload_wire",
     "bfly_merge_host",
+    "bfly_replay_check",
     "bfly_ring_round",
     "bfly_ring_ops",
 )
@@ -172,6 +173,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
+    L.bfly_replay_check.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
     L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
     L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
