@@ -107,6 +107,7 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
   int rc = get_pool(threads, &pool);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  const bool skip_copy = env_int("BFLY_UPLOAD_NOCOPY", 0) != 0;  // diagnostics: conversion alone
   // the copies must not start before work already queued on the caller's stream
   // (e.g. a previous round still reading the destination buffers)
   cudaEvent_t start;
@@ -132,7 +133,8 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
         const double* src = h_payloads[m] + b;
         float* dst = w.slot[k];
         for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];  // RNE, as numpy's astype
-        ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
+        if (!skip_copy)
+          ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
       }
       if (ce == cudaSuccess) ce = cudaEventRecord(w.done[k], w.stream);
       if (ce != cudaSuccess) {

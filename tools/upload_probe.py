@@ -31,8 +31,8 @@ d_ptrs = (ctypes.c_void_p * n)(*[w.data_ptr() for w in wire])
 gb = n * P * 4 / 1e9
 print(f"cpus {os.cpu_count()} miners {n} P 2^{a.log2p}: {gb:.2f} GB fp32 wire", flush=True)
 for threads in (16,):
-    for block in (1 << 17, 1 << 18, 1 << 19, 1 << 20):
-        for ring in (3, 4, 6):
+    for block in (1 << 19,):
+        for ring in (2, 3):
             os.environ["BFLY_UPLOAD_BLOCK"] = str(block)
             os.environ["BFLY_UPLOAD_RING"] = str(ring)
             best = 1e9
@@ -44,6 +44,20 @@ for threads in (16,):
                 best = min(best, time.perf_counter() - t)
             print(f"threads {threads:2d} block {block:8d} ring {ring}: {best * 1e3:7.1f} ms  "
                   f"{gb / best:6.1f} GB/s wire", flush=True)
+os.environ["BFLY_UPLOAD_BLOCK"], os.environ["BFLY_UPLOAD_RING"] = str(1 << 19), "3"
+for nocopy in ("1", "0"):
+    os.environ["BFLY_UPLOAD_NOCOPY"] = nocopy
+    for threads in (16, 8, 4, 2, 1):
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            L.check(L.lib().bfly_upload_wire(h_ptrs, n, P, d_ptrs, threads, _stream_handle()))
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t)
+        print(f"{'convert only' if nocopy == '1' else 'convert+copy'} threads {threads:2d}: {best * 1e3:7.1f} ms  "
+              f"{gb / best:6.1f} GB/s wire", flush=True)
+os.environ.pop("BFLY_UPLOAD_NOCOPY")
 ok = all(torch.equal(w.cpu(), h.float()) for w, h in zip(wire[:2], host[:2]))
 print("values exact:", ok)
 os.environ.pop("BFLY_UPLOAD_BLOCK")
