@@ -171,6 +171,10 @@ int bfly_set_max_ctas(int32_t max_ctas);
  * x 16M elements: 0.21 vs 0.32 ms on B200, tools/peer_bw.py). */
 int bfly_set_chain_bulk(int32_t on);
 
+/* Fan-out stores through TMA bulk copies (32 KB tiles staged in shared memory, one
+ * cp.async.bulk per destination) instead of 256-bit stores; default off. */
+int bfly_set_fanout_bulk(int32_t on);
+
 /* Upload n fp64 host payloads of P elements (pageable or pinned) as fp32 wire
  * values ("<f4", butterfly.py:213) into the device buffers d_wire[i]: `threads`
  * host threads (0 = all cores) convert into a pinned staging ring while earlier
@@ -231,6 +235,8 @@ typedef struct bfly_ring_desc {
   void* const* reduce_events;    /* last rank, optional: [k_chunks] cudaEvent_t (or NULL)
                                     the C stream waits for before reducing chunk k (the
                                     chunk's fallback values have arrived)               */
+  const int64_t* chunk_edges;    /* optional [k_chunks+1] element boundaries of the chunks
+                                    (each <= chunk); NULL = uniform chunks of `chunk`   */
 } bfly_ring_desc_t;
 int bfly_ring_round(const bfly_ring_desc_t* desc, uint32_t round_index);
 /* The op list of one rank for one round as rows of 7 int32

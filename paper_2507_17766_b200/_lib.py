@@ -48,6 +48,7 @@ EXPORTS = (
     "bfly_upload_wire",
     "bfly_merge_host",
     "bfly_replay_check",
+    "bfly_set_fanout_bulk",
     "bfly_ring_round",
     "bfly_ring_ops",
 )
@@ -132,6 +133,7 @@ class RingDesc(ctypes.Structure):
         ("finish_ranges", ctypes.c_void_p),
         ("stream_f", ctypes.c_void_p),
         ("reduce_events", ctypes.c_void_p),
+        ("chunk_edges", ctypes.c_void_p),
     ]
 
 
@@ -173,6 +175,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
+    L.bfly_set_fanout_bulk.argtypes = [i32]
     L.bfly_replay_check.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
     L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]

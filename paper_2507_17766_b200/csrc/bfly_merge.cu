@@ -908,6 +908,52 @@ __global__ void __launch_bounds__(kThreads) k_ranges(const unsigned char* full, 
 }
 
 // Scatter one final vector into several replicas (multi-GPU fan-out).
+// The same with TMA bulk stores: a CTA stages a 32 KB tile in shared memory (double
+// buffer) and one thread issues one cp.async.bulk store per destination.
+constexpr int kFanTile = 32768;
+__global__ void __launch_bounds__(kThreads) k_fanout_bulk(const void* src, void* const* dst, int n_dst,
+                                                          int64_t nbytes) {
+  extern __shared__ __align__(128) unsigned char fan_smem[];
+  unsigned char* stage = fan_smem;  // [2][kFanTile]
+  void** s_dst = reinterpret_cast<void**>(fan_smem + 2 * kFanTile);
+  const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, dst, n_dst, (uintptr_t)src);
+  const int64_t ntiles = aligned ? nbytes / kFanTile : 0;
+  int buf = 0, issued = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    V8 x[kFanTile / 32 / kThreads];
+#pragma unroll
+    for (int i = 0; i < kFanTile / 32 / kThreads; ++i)
+      x[i] = ld_stream(reinterpret_cast<const V8*>((const unsigned char*)src + t * kFanTile) + i * kThreads +
+                       threadIdx.x);
+    if (threadIdx.x == 0 && issued >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();  // stage[buf] no longer read by the stores issued two tiles ago
+#pragma unroll
+    for (int i = 0; i < kFanTile / 32 / kThreads; ++i)
+      reinterpret_cast<V8*>(stage + buf * kFanTile)[i * kThreads + threadIdx.x] = x[i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(stage + buf * kFanTile);
+      for (int d = 0; d < n_dst; ++d)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         (unsigned char*)s_dst[d] + t * kFanTile),
+                     "r"(sa), "r"((unsigned)kFanTile)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    ++issued;
+    buf ^= 1;
+  }
+  if (threadIdx.x == 0 && issued) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // tail bytes (and everything when unaligned)
+  const int64_t done = ntiles * kFanTile;
+  for (int64_t b = done + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned char v = ((const unsigned char*)src)[b];
+    for (int d = 0; d < n_dst; ++d) ((unsigned char*)s_dst[d])[b] = v;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* const* dst, int n_dst, int64_t nbytes) {
   extern __shared__ __align__(16) const void* s_ptr[];
   void** s_dst = const_cast<void**>(s_ptr);
@@ -1234,6 +1280,7 @@ using namespace bfly;
 // resident CTA per SM it leaves SMs free for concurrent NCCL kernels.
 static int g_max_ctas = 0;
 static int g_chain_bulk = 1;  // k_chain stores through TMA bulk copies (bfly_set_chain_bulk)
+static int g_fanout_bulk = 0;  // k_fanout stores through TMA bulk copies (bfly_set_fanout_bulk)
 static int64_t cap_grid(int64_t grid) {
   if (g_max_ctas > 0 && grid > g_max_ctas) grid = g_max_ctas;
   return grid < 1 ? 1 : grid;
@@ -1479,9 +1526,25 @@ int bfly_set_max_ctas(int32_t max_ctas) {
   return BFLY_OK;
 }
 
+int bfly_set_fanout_bulk(int32_t on) {
+  g_fanout_bulk = on ? 1 : 0;
+  return BFLY_OK;
+}
+
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream) {
   if (!d_src || n_dst < 0 || (n_dst > 0 && !d_dst) || nbytes < 0) return fail(BFLY_E_INVALID_ARG, "bad fanout arguments");
   if (n_dst == 0 || nbytes == 0) return BFLY_OK;
+  if (g_fanout_bulk) {
+    int64_t grid = nbytes / kFanTile;
+    if (grid > (int64_t)sm_count() * 3) grid = (int64_t)sm_count() * 3;
+    grid = cap_grid(grid);
+    const size_t smem = 2 * kFanTile + sizeof(void*) * (size_t)n_dst;
+    cudaFuncSetAttribute(k_fanout_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_fanout_bulk<<<(unsigned)grid, kThreads, smem, (cudaStream_t)stream>>>(d_src, d_dst, n_dst, nbytes);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "bfly_fanout launch");
+    return BFLY_OK;
+  }
   int64_t grid = (nbytes / 32 + kThreads - 1) / kThreads;
   if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
   grid = cap_grid(grid);

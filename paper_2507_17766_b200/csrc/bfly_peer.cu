@@ -219,8 +219,16 @@ int bfly_ring_round(const bfly_ring_desc_t* d, uint32_t round_index) {
   Op ops[16];
   int result = BFLY_OK;
   for (int k = 0; k < K && result == BFLY_OK; ++k) {
-    const int64_t b = (int64_t)k * d->chunk;
-    const int64_t e = b + d->chunk < d->payload_len ? b + d->chunk : d->payload_len;
+    int64_t b = (int64_t)k * d->chunk;
+    int64_t e = b + d->chunk < d->payload_len ? b + d->chunk : d->payload_len;
+    if (d->chunk_edges) {
+      b = d->chunk_edges[k];
+      e = d->chunk_edges[k + 1];
+      if (e - b > d->chunk || e < b) {
+        result = fail(BFLY_E_INVALID_ARG, "chunk larger than an inbox slot");
+        break;
+      }
+    }
     const int m = chunk_ops(g, G, K, NB, round_index, k, late, ops);
     for (int i = 0; i < m && result == BFLY_OK; ++i) {
       const Op& o = ops[i];

@@ -35,7 +35,9 @@ bit-identical to the single-GPU (and reference) result.
 
 from __future__ import annotations
 
+import bisect
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -46,7 +48,7 @@ from . import errors
 from . import ringsched as rs
 from .device import ButterflyMerge, _DTYPES, _stream_handle
 
-NB = 3  # inbox slots per ring
+NB = int(os.environ.get("BFLY_RING_NB", "3"))  # inbox slots per ring
 WINDOW = 4  # chunks the host may run ahead of the GPUs per stream
 
 
@@ -87,9 +89,30 @@ def unpack_results(buf, entries, source, status, flagged):
     flagged.copy_(buf[o + S:o + S + n])
 
 
+def chunk_edges(P: int, chunk: int, ramp: bool = True) -> list:
+    """Element boundaries of the pipelined chunks.  Full chunks of `chunk` elements, but
+    with `ramp` the first and last few halve down to chunk/16: the ring's fill (the first
+    chunk crosses every rank before the last one can reduce it) and drain (the last
+    chunk's relay) then cost a few small steps instead of 2(G-1) full ones."""
+    ramp_sizes = [chunk >> j for j in (4, 3, 2, 1) if (chunk >> j) >= (1 << 16) and (chunk >> j) % 4096 == 0]
+    if not ramp or not ramp_sizes or P < 2 * sum(ramp_sizes) + 2 * chunk:
+        sizes = [chunk] * (P // chunk) + ([P % chunk] if P % chunk else [])
+    else:
+        mid = P - 2 * sum(ramp_sizes)
+        tail = mid % 4096  # keeps every inner boundary on a 4096-element (tile) edge
+        mid -= tail
+        body = [chunk] * (mid // chunk) + ([mid % chunk] if mid % chunk else [])
+        sizes = ramp_sizes + body + ramp_sizes[::-1]
+        sizes[-1] += tail
+    edges = [0]
+    for x in sizes:
+        edges.append(edges[-1] + x)
+    return edges
+
+
 class _Region:
     """Layout of one rank's IPC region: NB fp64 running-sum slots, NB final-vector
-    slots, and the four flag arrays of ringsched (uint32 x NB each)."""
+    slots, and the flag arrays of ringsched (uint32 x NB each)."""
 
     def __init__(self, chunk: int, esize: int):
         def align(x):
@@ -98,7 +121,7 @@ class _Region:
         self.acc = 0
         self.fin = align(NB * chunk * 8)
         self.flags = align(self.fin + NB * chunk * esize)
-        self.total = align(self.flags + 4 * NB * 4)
+        self.total = align(self.flags + len(rs.FLAGS) * NB * 4)
         self.chunk, self.esize = chunk, esize
 
     def acc_slot(self, base: int, s: int) -> int:
@@ -137,8 +160,9 @@ class ShardedButterflyMerge:
         self.dtype = _DTYPES[local[0].dtype]
         if chunk % 4096:
             raise errors.InvalidArgumentError("chunk must be a multiple of 4096 elements")
-        self.chunk = int(min(chunk, ((self.P + 4095) // 4096) * 4096))
-        self.K = -(-self.P // self.chunk)
+        self.chunk = int(min(chunk, ((self.P + 4095) // 4096) * 4096))  # inbox slot size
+        self.edges = chunk_edges(self.P, self.chunk, ramp=G > 1)
+        self.K = len(self.edges) - 1
         counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(G)]
         dist.all_gather(counts, torch.tensor([len(local)], dtype=torch.int64, device=self.dev))
         self.counts = [int(c.item()) for c in counts]
@@ -217,7 +241,10 @@ class ShardedButterflyMerge:
 
     # -- late shards -------------------------------------------------------------
     def _chunk_starts(self):
-        return [k * self.chunk for k in range(1, self.K)]
+        return self.edges[1:-1]
+
+    def _chunk_of(self, e: int) -> int:
+        return bisect.bisect_right(self.edges, e) - 1
 
     def _chunk_shard_ranges(self, S: int):
         """Per chunk k, the shards lying entirely inside it ([s_begin, s_end)), and the
@@ -249,7 +276,7 @@ class ShardedButterflyMerge:
         out = []
         for lo, hi in runs:
             while lo < hi:
-                cut = min(hi, (lo // self.chunk + 1) * self.chunk)
+                cut = min(hi, self.edges[self._chunk_of(lo) + 1])
                 out.append((lo, cut))
                 lo = cut
         return out
@@ -270,14 +297,14 @@ class ShardedButterflyMerge:
         offs, _ = self._packed_offsets(runs)
         rows = {}
         for i, (lo, hi) in enumerate(runs):
-            k = lo // self.chunk
+            k = self._chunk_of(lo)
             grp = (k + 1).bit_length() - 1  # chunks [2^j - 1, 2^(j+1) - 1)
             r0, r1, o0, o1 = rows.get(grp, (i, i, offs[i], offs[i]))
             rows[grp] = (r0, i + 1, o0, offs[i] + hi - lo)
         out = []
         for grp in sorted(rows):
             r0 = rows[grp][0]
-            out.append((runs[r0][0] // self.chunk,) + rows[grp])
+            out.append((self._chunk_of(runs[r0][0]),) + rows[grp])
         return out
 
     def _range_set(self, runs):
@@ -324,7 +351,7 @@ class ShardedButterflyMerge:
         # relay ranks fan out into their replicas and the successor's inbox
         self._reduce_tables, self._fan_tables = {}, {}
         for k in range(self.K):
-            b = k * self.chunk
+            b = self.edges[k]
             for s in range(NB):
                 if self.is_last:
                     fin0 = lay.fin_slot(self._peer[0], s) - b * self.esize
@@ -339,6 +366,8 @@ class ShardedButterflyMerge:
         d = L.RingDesc()
         d.rank, d.world, d.k_chunks, d.nb = g, self.world, self.K, NB
         d.payload_len, d.chunk, d.dtype, d.esize = self.P, self.chunk, self.dtype, self.esize
+        self._edge_arr = (ctypes.c_int64 * (self.K + 1))(*self.edges)
+        d.chunk_edges = ctypes.cast(self._edge_arr, ctypes.c_void_p)
         self._peer_arr = (ctypes.c_uint64 * self.world)(*[self._peer[r] for r in range(self.world)])
         d.peer_base = ctypes.cast(self._peer_arr, ctypes.c_void_p)
         d.off_acc, d.off_fin, d.off_flags = lay.acc, lay.fin, lay.flags
@@ -379,8 +408,7 @@ class ShardedButterflyMerge:
             pass
 
     def _bounds(self, k):
-        b = k * self.chunk
-        return b, min(b + self.chunk, self.P)
+        return self.edges[k], self.edges[k + 1]
 
     def _issue(self, op):
         lib, lay = L.lib(), self.layout
@@ -439,14 +467,14 @@ class ShardedButterflyMerge:
                 for op, ev in marks:
                     if not ev.query() and op[1] not in stuck:
                         stuck[op[1]] = op
-                flags = torch.empty(4 * NB, dtype=torch.int32, device=self.dev)
+                flags = torch.empty(len(rs.FLAGS) * NB, dtype=torch.int32, device=self.dev)
                 side = torch.cuda.Stream(device=self.dev)
                 with torch.cuda.stream(side):
                     L.lib().bfly_fanout(self._base + self.layout.flags,
-                                        self._table([flags]).data_ptr(), 1, 16 * NB, side.cuda_stream)
+                                        self._table([flags]).data_ptr(), 1, 4 * len(rs.FLAGS) * NB, side.cuda_stream)
                 side.synchronize()
                 print(f"[rank {self.rank}] ring stuck after {deadline}s: {stuck}; flags "
-                      f"{dict(zip(rs.FLAGS, flags.view(4, NB).tolist()))}", file=sys.stderr, flush=True)
+                      f"{dict(zip(rs.FLAGS, flags.view(len(rs.FLAGS), NB).tolist()))}", file=sys.stderr, flush=True)
                 raise RuntimeError("multi-GPU ring did not complete")
             time.sleep(0.005)
 

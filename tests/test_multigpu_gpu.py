@@ -83,6 +83,11 @@ CASES = [
      "chunk": 65536, "bf16": True},
     {"counts": [3, 4], "P": 35 * 2000 + 3, "seed": 10, "failures": [0], "corr": {"6": [3, 1.0, 4, 4]},
      "fallback": False, "chunk": 8192, "r": 3},
+    # ramped chunk sizes (1M/16 .. 1M .. 1M/16, multigpu.chunk_edges), fallback values in chunk groups
+    {"counts": [3, 3], "P": 5_000_011, "seed": 12, "failures": [4], "corr": {"1": [3, 2.0, 9, 9], "5": [1, 0.0]},
+     "fallback": False, "chunk": 1 << 20},
+    {"counts": [2, 2, 2, 2], "P": 6_000_007, "seed": 13, "failures": [], "corr": {"3": [3, 1.0, 2, 3]},
+     "fallback": False, "chunk": 1 << 20},
 ]
 
 
