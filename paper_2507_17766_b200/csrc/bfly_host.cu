@@ -41,6 +41,7 @@ struct Worker {
 };
 
 struct Pool {
+  std::mutex busy;  // one upload at a time uses the workers' slots and streams
   int device = -1;
   int64_t block = 0;
   int ring = 0;
@@ -106,6 +107,7 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
   Pool* pool = nullptr;
   int rc = get_pool(threads, &pool);
   if (rc) return rc;
+  std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
   const bool skip_copy = env_int("BFLY_UPLOAD_NOCOPY", 0) != 0;  // diagnostics: conversion alone
   // the copies must not start before work already queued on the caller's stream
@@ -169,6 +171,7 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
   Pool* pool = nullptr;
   int rc = get_pool(threads, &pool);
   if (rc) return rc;
+  std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t B = pool->block;
   int64_t CL = (P + n_chunks - 1) / n_chunks;

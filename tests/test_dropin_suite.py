@@ -241,3 +241,20 @@ def test_store_contents_materialise_like_the_reference():
     # both members of every disagreeing pair are flagged (butterfly.py:266-267)
     partners = {m for pair in plan.assignment if 2 in pair for m in pair if m != 1}
     assert res.flagged == partners
+
+
+def test_monte_carlo_resilience_matches_reference():
+    """Fixture from the reference's own monte_carlo_resilience (tests/golden/resilience_mc.json,
+    made by tests/golden/make_resilience_golden.py): identical floats."""
+    import json
+    from pathlib import Path
+
+    want = json.loads((Path(__file__).parent / "golden" / "resilience_mc.json").read_text())
+    for key, vals in want.items():
+        n, trials, seed = (int(x) for x in key.split("_"))
+        got = bf.monte_carlo_resilience(n, [int(k) for k in vals], trials=trials, seed=seed)
+        assert {str(k): v for k, v in got.items()} == vals
+    with pytest.raises(InvalidArgumentError):
+        bf.monte_carlo_resilience(5, [6], trials=3, seed=0)
+    with pytest.raises(TooFewMinersError):
+        bf.monte_carlo_resilience(1, [0], trials=3, seed=0)
