@@ -201,6 +201,10 @@ int bfly_merge_host(const double* const* h_payloads, int32_t n, int64_t P, float
 int bfly_ipc_alloc(size_t bytes, void** d_ptr, uint8_t handle[64]);
 /* Map a neighbour's region (peer access over NVLink enabled lazily). */
 int bfly_ipc_open(const uint8_t handle[64], void** d_ptr);
+/* Export an existing device buffer (e.g. a framework tensor inside a larger cudaMalloc
+ * block): the IPC handle of its allocation and the byte offset of d_ptr in it.  The
+ * importer maps the handle with bfly_ipc_open and adds the offset. */
+int bfly_ipc_export(const void* d_ptr, uint8_t handle[64], uint64_t* offset);
 int bfly_ipc_close(void* d_ptr);
 int bfly_ipc_free(void* d_ptr);
 /* Stream-ordered cross-GPU signalling (CUDA stream memory operations, no SM spin):

@@ -49,6 +49,7 @@ EXPORTS = (
     "bfly_merge_host",
     "bfly_replay_check",
     "bfly_set_fanout_bulk",
+    "bfly_ipc_export",
     "bfly_ring_round",
     "bfly_ring_ops",
 )
@@ -176,6 +177,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
     L.bfly_set_fanout_bulk.argtypes = [i32]
+    L.bfly_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.bfly_replay_check.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
     L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]

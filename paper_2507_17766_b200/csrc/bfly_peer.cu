@@ -22,9 +22,11 @@ namespace bfly {
 
 typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_addr_range)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 static PFN_wait32 g_wait32 = nullptr;
 static PFN_write32 g_write32 = nullptr;
+static PFN_addr_range g_addr_range = nullptr;
 static std::once_flag g_once;
 static int g_flush_supported = 0;
 
@@ -39,6 +41,10 @@ static int load_driver_ops() {
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       g_write32 = (PFN_write32)fn;
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_addr_range = (PFN_addr_range)fn;
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess)
       cudaDeviceGetAttribute(&g_flush_supported, (cudaDeviceAttr)98 /* CAN_FLUSH_REMOTE_WRITES */, dev);
@@ -73,6 +79,21 @@ int bfly_ipc_open(const uint8_t handle[64], void** d_ptr) {
   memcpy(&h, handle, 64);
   cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  return BFLY_OK;
+}
+
+int bfly_ipc_export(const void* d_ptr, uint8_t handle[64], uint64_t* offset) {
+  if (!d_ptr || !handle || !offset) return fail(BFLY_E_INVALID_ARG, "bad ipc export arguments");
+  load_driver_ops();
+  if (!g_addr_range) return fail(BFLY_E_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (g_addr_range(&base, &size, (CUdeviceptr)d_ptr) != CUDA_SUCCESS) return fail(BFLY_E_CUDA, "cuMemGetAddressRange");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, (void*)base);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle (export)");
+  memcpy(handle, &h, 64);
+  *offset = (uint64_t)((CUdeviceptr)d_ptr - base);
   return BFLY_OK;
 }
 

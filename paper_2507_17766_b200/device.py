@@ -251,7 +251,8 @@ class ButterflyMerge:
         a.scratch_bytes = scratch_bytes
         a.tolerance = float(tolerance)
         a.n_div = self.n_div
-        a.d_fallback_src = fallback_src.data_ptr() if fallback_src is not None else None
+        a.d_fallback_src = (None if fallback_src is None else
+                            fallback_src if isinstance(fallback_src, int) else fallback_src.data_ptr())
         self._args = a
         self._host_copies = None
         self._acc_in = None

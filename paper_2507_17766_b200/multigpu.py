@@ -35,7 +35,6 @@ bit-identical to the single-GPU (and reference) result.
 
 from __future__ import annotations
 
-import bisect
 import ctypes
 import os
 
@@ -87,6 +86,38 @@ def unpack_results(buf, entries, source, status, flagged):
     o += 4 * S
     status.copy_(buf[o:o + S])
     flagged.copy_(buf[o + S:o + S + n])
+
+
+_IPC_MAPS = {}  # IPC handle -> [mapped base, users]: a process maps an allocation once
+
+
+def _ipc_export(t: torch.Tensor) -> tuple:
+    """(IPC handle of the allocation holding t, byte offset of t in it)."""
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_uint64()
+    with torch.cuda.device(t.device):
+        L.check(L.lib().bfly_ipc_export(t.data_ptr(), h, ctypes.byref(off)))
+    return bytes(h), int(off.value)
+
+
+def _ipc_map(handle: bytes, dev) -> int:
+    ent = _IPC_MAPS.get(handle)
+    if ent is None:
+        p = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            L.check(L.lib().bfly_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(handle), ctypes.byref(p)))
+        ent = _IPC_MAPS[handle] = [p.value, 0]
+    ent[1] += 1
+    return ent[0]
+
+
+def _ipc_unmap(handle: bytes):
+    ent = _IPC_MAPS.get(handle)
+    if ent is not None:
+        ent[1] -= 1
+        if ent[1] == 0:
+            L.lib().bfly_ipc_close(ctypes.c_void_p(ent[0]))
+            del _IPC_MAPS[handle]
 
 
 def chunk_edges(P: int, chunk: int, ramp: bool = True) -> list:
@@ -197,20 +228,25 @@ class ShardedButterflyMerge:
         late = [r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())] if G > 1 else runs
         self.late_runs = late
         self.special_runs = late  # kept name: ranges broadcast after the ring
-        # fallback runs split at chunk boundaries, so each chunk's values travel (and are
-        # waited for) on their own: the last rank reduces chunk k once chunk k's arrived
-        fb_runs = self._split_at_chunks(runs) if G > 1 else runs
-        self._fb_set = self._range_set(fb_runs) if runs else None
-        self._fb_chunks = self._chunk_rows(fb_runs) if runs else []
         self._late_set = self._range_set(late) if late else None
-        # fallback values come from the lowest alive miner when no fallback is given
+        # fallback values come from the lowest alive miner when no fallback is given; when
+        # that replica lives on another rank the last rank reads it in place over NVLink
+        # (IPC-mapped): chunk k of it is only overwritten by the relay, which starts after
+        # the last rank has reduced and finished chunk k
         self._needs_fb = bool(fallback is None and self.alive and runs)
-        self.fb_owner, self._fb_buf = None, None
+        self.fb_owner, self._fb_buf, self._fb_ptr, self._fb_handle = None, None, None, None
         if self._needs_fb:
             m0 = self.alive[0]
             self.fb_owner = next(r for r in range(G) if sum(self.counts[: r + 1]) > m0)
-            if self.is_last and self.fb_owner != self.rank:
-                self._fb_buf = torch.empty_like(local[0])
+        if G > 1 and self._needs_fb and self.fb_owner != G - 1:
+            info = _ipc_export(local[m0 - self.offset]) if self.rank == self.fb_owner else None
+            infos = [None] * G
+            dist.all_gather_object(infos, info)
+            if self.is_last:
+                self._fb_handle, off = infos[self.fb_owner]
+                self._fb_ptr = _ipc_map(self._fb_handle, self.dev) + off
+                if late:  # shards straddling chunk edges finish after the relay: copy theirs first
+                    self._fb_buf = torch.empty_like(local[0])
 
         self.job = None
         if self.is_last:
@@ -219,7 +255,7 @@ class ShardedButterflyMerge:
                 reps[self.offset + i] = t
             fb_src = None
             if self._needs_fb:
-                fb_src = self._fb_buf if self._fb_buf is not None else reps[self.alive[0]]
+                fb_src = self._fb_ptr if self._fb_ptr is not None else reps[self.alive[0]]
             self.job = ButterflyMerge(reps, plan, remote_sum=G > 1, n_div=len(self.alive), failures=failures,
                                       corruptions=corruptions, fallback=fallback, fallback_src=fb_src,
                                       scatter_back=True, want_merged=want_merged, tolerance=tolerance)
@@ -242,9 +278,6 @@ class ShardedButterflyMerge:
     # -- late shards -------------------------------------------------------------
     def _chunk_starts(self):
         return self.edges[1:-1]
-
-    def _chunk_of(self, e: int) -> int:
-        return bisect.bisect_right(self.edges, e) - 1
 
     def _chunk_shard_ranges(self, S: int):
         """Per chunk k, the shards lying entirely inside it ([s_begin, s_end)), and the
@@ -272,15 +305,6 @@ class ShardedButterflyMerge:
                 straddle.append(shard_of(b))
         return ranges, sorted(set(straddle))
 
-    def _split_at_chunks(self, runs):
-        out = []
-        for lo, hi in runs:
-            while lo < hi:
-                cut = min(hi, self.edges[self._chunk_of(lo) + 1])
-                out.append((lo, cut))
-                lo = cut
-        return out
-
     @staticmethod
     def _packed_offsets(runs):
         offs, off = [], 0
@@ -289,23 +313,6 @@ class ShardedButterflyMerge:
             offs.append(off)
             off += hi - lo
         return offs, off
-
-    def _chunk_rows(self, runs):
-        """Fallback transfers: (first chunk, first row, end row, packed begin, packed end)
-        per group of chunks 0 | 1-2 | 3-6 | 7-14 | ... — each group travels while the
-        reduce works through the previous one, with few host calls."""
-        offs, _ = self._packed_offsets(runs)
-        rows = {}
-        for i, (lo, hi) in enumerate(runs):
-            k = self._chunk_of(lo)
-            grp = (k + 1).bit_length() - 1  # chunks [2^j - 1, 2^(j+1) - 1)
-            r0, r1, o0, o1 = rows.get(grp, (i, i, offs[i], offs[i]))
-            rows[grp] = (r0, i + 1, o0, offs[i] + hi - lo)
-        out = []
-        for grp in sorted(rows):
-            r0 = rows[grp][0]
-            out.append((self._chunk_of(runs[r0][0]),) + rows[grp])
-        return out
 
     def _range_set(self, runs):
         """Device table {lo, hi, packed offset} + packed buffer for element runs."""
@@ -342,8 +349,6 @@ class ShardedButterflyMerge:
         dist.barrier()
         self._relay = torch.cuda.Stream(device=self.dev)
         self._late = torch.cuda.Stream(device=self.dev)  # last rank: per-chunk late shards
-        self._fbs = torch.cuda.Stream(device=self.dev)  # last rank: fallback values in
-        self._fb_events = {k: torch.cuda.Event() for k, *_ in self._fb_chunks} if self.is_last else {}
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -399,6 +404,9 @@ class ShardedButterflyMerge:
                     if r != self.rank:
                         lib.bfly_ipc_close(ctypes.c_void_p(p))
                 lib.bfly_ipc_free(ctypes.c_void_p(self._base))
+                if self._fb_handle is not None:
+                    _ipc_unmap(self._fb_handle)
+                    self._fb_handle = None
             self._peer = None
 
     def __del__(self):
@@ -500,7 +508,6 @@ class ShardedButterflyMerge:
         if self.debug == 3:  # timeline: every op's completion time from here (tools/ring_timeline.py)
             self._t0 = torch.cuda.Event(enable_timing=True)
             self._t0.record(cur)
-        fb_work = None
         if G == 1:
             for k in range(self.K):
                 b, e = self._bounds(k)
@@ -508,45 +515,21 @@ class ShardedButterflyMerge:
         else:
             # fallback values (the lowest alive miner's replica) for the late shards: packed
             # before the relay overwrites that replica, sent while the ring runs
-            fb_work = None
             self._relay.wait_stream(cur)
             self._late.wait_stream(cur)
-            fb_events = None
-            if self._needs_fb and self.fb_owner != last:
-                ranges, packed = self._fb_set
-                if g == self.fb_owner:  # packed once, sent chunk by chunk
-                    self._copy_ranges(self._fb_set, self.local[self.alive[0] - self.offset].data_ptr(), None, 0, 0)
-                    fb_work = [dist.isend(packed[o0:o1], dst=last) for _, _, _, o0, o1 in self._fb_chunks]
-                elif self.is_last:
-                    # chunk k's fallback values arrive on their own stream while the chain
-                    # runs; the reduce of chunk k (which writes predicted fallback values)
-                    # waits for them through an event
-                    self._fbs.wait_stream(cur)
-                    with torch.cuda.stream(self._fbs):
-                        for k, r0, r1, o0, o1 in self._fb_chunks:
-                            dist.recv(packed[o0:o1], src=self.fb_owner)
-                            self._copy_ranges((ranges[r0:r1], packed), None, self._fb_table.data_ptr(), 1, 1)
-                            self._fb_events[k].record(self._fbs)
-                    fb_events = self._fb_events
+            if self._fb_buf is not None:  # straddling late ranges' fallback values, before any relay
+                self._copy_ranges(self._late_set, self._fb_ptr, None, 0, 0)
+                self._copy_ranges(self._late_set, None, self._fb_table.data_ptr(), 1, 1)
             mark("fallback")
             marks, window = [], []
             if not self.debug:  # native executor: the whole round issued from C++
                 self._desc.stream_c = _stream_handle()
                 self._desc.stream_r = self._relay.cuda_stream
                 self._desc.stream_f = self._late.cuda_stream
-                if fb_events:
-                    self._ev_arr = (ctypes.c_void_p * self.K)(
-                        *[fb_events[k].cuda_event if k in fb_events else None for k in range(self.K)])
-                    # one event per group, at its first chunk: the in-order C stream covers the rest
-                    self._desc.reduce_events = ctypes.cast(self._ev_arr, ctypes.c_void_p)
-                else:
-                    self._desc.reduce_events = None
                 with torch.cuda.device(self.dev):
                     L.check(L.lib().bfly_ring_round(ctypes.byref(self._desc), self._round & 0xFFFFFFFF))
             for k in range(self.K if self.debug else 0):  # debug: the same ops issued from Python
                 for op in rs.chunk_ops(g, G, self.K, NB, self._round, k, self._late_mode):
-                    if op[0] == "reduce" and fb_events and k in fb_events:
-                        cur.wait_event(fb_events[k])
                     self._issue(op)
                     if self.debug:
                         ev = torch.cuda.Event(enable_timing=self.debug == 3)
@@ -564,19 +547,22 @@ class ShardedButterflyMerge:
             self._marks = marks
             cur.wait_stream(self._relay)
             cur.wait_stream(self._late)
-            cur.wait_stream(self._fbs)
         self._round += 1
         mark("ring")
 
         # finish the shards that straddle chunk boundaries, then distribute the
         # per-shard results and those shards' final values
-        for w in fb_work or ():
-            w.wait()
         if self.is_last:
             if G == 1:
                 self.job.run(L.PHASE_FINISH)
             elif self.job.needs_finish() and self.straddlers:
-                self.job.run_finish_list(self._straddle_dev)
+                a = self.job._args
+                if self._fb_buf is not None:  # the owner's replica may hold relayed values by now
+                    a.d_fallback_src = self._fb_buf.data_ptr()
+                try:
+                    self.job.run_finish_list(self._straddle_dev)
+                finally:
+                    a.d_fallback_src = self._fb_ptr if self._fb_ptr is not None else a.d_fallback_src
             pack_results(self.job.entries, self.job.source, self.job.status, self.job.flagged, self._res)
             if self.special_runs:
                 self._copy_ranges(self._late_set, self.local[0].data_ptr(), None, 0, 0)
