@@ -368,7 +368,7 @@ def run_multi(cfg, args, rank, world):
                        "params": P, "replica_dtype": dtype, "redundancy": r, "deceptive": len(bad),
                        "parallelism": f"miners in contiguous blocks over {world} GPUs; fp64 running-sum chain "
                                       f"(NCCL send/recv, {args.chunk}-element chunks) + broadcast of the result",
-                       "l2": "inputs %.0f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
+                       "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
             "params_merged_per_s": P / t_step,
             "roofline": {"bound": "hbm" if per_gpu_hbm / hbm_peak > float(nvl.item()) / nvl_peak else "nvlink",
                          "achieved": per_gpu_hbm / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
@@ -475,7 +475,7 @@ def run_stages(cfg, args, rank, world):
             "data": "synthetic uniform(-1,1) bf16 replicas (torch Philox)",
             "config": {"workload": WORKLOAD["c4"], "miners_per_stage": n, "params_per_stage": P, "stages": world,
                        "replica_dtype": dtype, "redundancy": r, "parallelism": "one stage per GPU (replicas only)",
-                       "l2": "inputs %.0f GB per GPU >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
+                       "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
             "params_merged_per_s": world * P / t_step,
             "roofline": {"bound": "hbm", "achieved": merge_bytes(n, P, esize) / t_step / 1e9, "peak": hbm_peak,
                          "unit": "GB/s", "frac": merge_bytes(n, P, esize) / t_step / 1e9 / hbm_peak,
@@ -581,7 +581,7 @@ def main():
         "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
         "config": {"workload": WORKLOAD[name], "miners": n, "params": P, "replica_dtype": dtype,
                    "redundancy": r, "deceptive": k_bad, "parallelism": "single GPU",
-                   "l2": "inputs %.0f GB >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
+                   "l2": "inputs %.2f GB >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
         "params_merged_per_s": P / t_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_from_profiles(name),
