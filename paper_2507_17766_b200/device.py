@@ -256,6 +256,7 @@ class ButterflyMerge:
         self._args = a
         self._host_copies = None
         self._acc_in = None
+        self._graph = None  # CUDA graph of one round (capture())
 
     def _call(self, stream):
         with torch.cuda.device(self.dev):
@@ -273,8 +274,38 @@ class ButterflyMerge:
         self._args.phase = phase
         self._args.d_acc_in = None
         self._args.elem_begin = self._args.elem_end = 0
-        self._call(stream)
+        if self._graph is not None and phase == L.PHASE_ALL and host_copies is None:
+            self._replay(stream)
+        else:
+            self._call(stream)
         return self
+
+    def capture(self) -> "ButterflyMerge":
+        """Record one whole round (phase ALL) as a CUDA graph; later ``run()`` calls replay
+        it — one launch instead of 4-8, which matters for small payloads.  The graph
+        reads the same buffers each replay, so the replicas may be refilled in place
+        between rounds; the plan, failures and corruptions are fixed at construction."""
+        if self.remote_sum:
+            raise errors.InvalidArgumentError("a chained merge is issued chunk by chunk; capture the single-GPU job")
+        self._graph = None
+        self.run()  # warm-up outside the capture (function attributes, lazy module loading)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
+            self._args.phase = L.PHASE_ALL
+            self._call(None)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        self._graph = g
+        return self
+
+    def _replay(self, stream):
+        if stream is None:
+            self._graph.replay()
+            return
+        with torch.cuda.stream(stream):
+            self._graph.replay()
 
     def reduce_range(self, begin: int, end: int, acc_in=None, stream=None, dst_table: tuple | None = None):
         """REDUCE elements [begin, end) — call with begin == 0 first in every round.

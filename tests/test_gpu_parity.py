@@ -279,3 +279,32 @@ def test_store_objects_ranged_reads_gpu(cuda_device):
         assert len(whole) == size
         for (a, b), got in zip(cuts, parts):
             assert got == whole[a:b], (key, a, b)
+
+
+def test_captured_round_replays_match_oracle(cuda_device):
+    """ButterflyMerge.capture(): one round as a CUDA graph; replays over replicas refilled
+    in place give the oracle's results every round (corrupted and failed miners included)."""
+    from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
+
+    n, P, seed = 6, (1 << 18) + 3, 11
+    specs = {2: (orc.NOISE, 1.0, 3, 4)}
+    plan = DevicePlan(n, P, seed, device=cuda_device)
+    assign, bounds = orc.plan(n, P, seed)
+    dreps = [torch.empty(P, dtype=torch.float32, device=cuda_device) for _ in range(n)]
+    job = ButterflyMerge(dreps, plan, failures=(4,), corruptions=_descriptors(specs), want_merged=True)
+    rng = np.random.default_rng(5)
+    for rnd in range(4):
+        reps = [rng.uniform(-1, 1, P).astype(np.float32) for _ in range(n)]
+        for t, r in zip(dreps, reps):
+            t.copy_(torch.from_numpy(r))
+        if rnd == 1:
+            job.capture()  # the capture's warm-up ran this round already; replay it again
+            for t, r in zip(dreps, reps):
+                t.copy_(torch.from_numpy(r))
+        job.run()
+        torch.cuda.synchronize()
+        want = orc.merge(reps, assign, bounds, failures=(4,), corruptions=specs)
+        assert_same_floats(job.merged.cpu().numpy(), want["merged"])
+        assert np.array_equal(job.status.cpu().numpy(), want["status"])
+        assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
+        assert_same_floats(dreps[0].cpu().numpy(), want["merged"].astype(np.float32))
