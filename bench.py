@@ -349,7 +349,9 @@ def run_multi(cfg, args, rank, world):
     nb = job.bytes_per_round()
     nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
     dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
-    launches = job.launches_per_run() * args.steps
+    lt = torch.tensor([job.launches_per_run() * args.steps], dtype=torch.int64, device=dev)
+    dist.all_reduce(lt)  # every rank's kernels: the whole job's launches
+    launches = int(lt.item())
     e2e = None if args.no_e2e else run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0)
     if rank == 0:
         peaks = _peaks()

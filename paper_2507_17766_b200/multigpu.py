@@ -209,6 +209,7 @@ class ShardedButterflyMerge:
         self.plan = plan
         self.want_merged = want_merged
         self.is_last = self.rank == G - 1
+        self.plan_r = int(getattr(plan, "redundancy", 2))
         self._round = 0
         self.debug = int(__import__("os").environ.get("BFLY_DEBUG_RING", "0"))
         self.timing = bool(int(__import__("os").environ.get("BFLY_RING_TIMING", "0")))  # per-phase ms in .timings
@@ -599,10 +600,18 @@ class ShardedButterflyMerge:
 
     def launches_per_run(self) -> int:
         """Our kernels per round on this rank (bench.py gpu_launches)."""
+        fin = 3 + (1 if self.plan_r > 2 else 0)  # k_stats, k_decide, [k_entries3], k_apply
+        if self.world == 1:
+            return 2 + self.K + (fin if self.job.needs_finish() else 0)
         if self.is_last:
-            extra = self.job.launches_per_run() - 3 + (1 if self.special_runs else 0)
-            return self.K + 2 + max(extra, 0)
-        return 2 * self.K + (1 if self.special_runs else 0)
+            n = 2 + self.K  # k_fill_nan + k_classify, then one k_reduce per chunk
+            if self._late_mode:
+                n += fin * sum(1 for b, e in self._finish_ranges if e > b)
+                n += fin if self.straddlers else 0
+            n += 2 if self._fb_buf is not None else 0  # straddlers' fallback ranges: gather + scatter
+            n += 1 if self.special_runs else 0  # late ranges packed for the broadcast
+            return n
+        return 2 * self.K + (1 if self.special_runs else 0)  # k_chain + k_fanout per chunk
 
     def bytes_per_round(self) -> dict:
         """Algorithmic HBM and NVLink bytes of this rank for one round."""
