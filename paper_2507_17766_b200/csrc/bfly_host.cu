@@ -33,12 +33,62 @@ namespace {
 // itself, so no thread ever waits for another.  Blocks are small enough that the
 // ring's lines are still in the host's last-level cache when the copy engine reads
 // them back: the host memory traffic stays near the 8 B/element of the fp64 read.
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoll(v) : dflt;
+}
+
 struct Worker {
   std::vector<float*> slot;
   std::vector<cudaEvent_t> done;
+  std::vector<double*> raw;  // device ring for blocks copied as fp64 and converted on the GPU
   cudaStream_t stream = nullptr;
   cudaEvent_t fin = nullptr;
+  int64_t count = 0, raw_count = 0;
 };
+
+// fp64 payload block (copied raw) -> fp32 wire values, RNE like numpy's astype
+__global__ void k_wire(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __double2float_rn(src[i]);
+}
+
+// One block of one payload onto the device, by this worker: converted on the host into a
+// pinned slot and copied, or (raw) copied as fp64 into a device slot and converted there.
+// Raw blocks cost 8 B of PCIe per element but no host write / re-read: mixing them in
+// balances host-memory traffic (16 B per converted element) against PCIe (4 B).
+cudaError_t upload_block(Worker& w, int ring, const double* src, float* dst, int64_t len, bool raw) {
+  if (raw) {
+    const int k = (int)(w.raw_count++ % ring);
+    cudaError_t ce = cudaMemcpyAsync(w.raw[k], src, sizeof(double) * len, cudaMemcpyHostToDevice, w.stream);
+    if (ce != cudaSuccess) return ce;
+    const int64_t grid = std::min<int64_t>((len + 255) / 256, 1024);
+    k_wire<<<(unsigned)grid, 256, 0, w.stream>>>(w.raw[k], dst, len);
+    return cudaGetLastError();
+  }
+  const int k = (int)(w.count++ % ring);
+  cudaError_t ce = cudaEventSynchronize(w.done[k]);  // the slot's previous copy has left
+  if (ce != cudaSuccess) return ce;
+  float* slot = w.slot[k];
+  for (int64_t i = 0; i < len; ++i) slot[i] = (float)src[i];  // RNE, as numpy's astype
+  ce = cudaMemcpyAsync(dst, slot, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
+  if (ce != cudaSuccess) return ce;
+  return cudaEventRecord(w.done[k], w.stream);
+}
+
+// every `raw_every`-th block goes raw when all payloads are page-locked (0: never)
+int raw_every_for(const double* const* h, int32_t n) {
+  const int64_t every = env_int("BFLY_UPLOAD_RAW_EVERY", 0);  // off: measured slower (profiles/)
+  if (every <= 0) return 0;
+  for (int32_t m = 0; m < n; ++m) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h[m]) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return 0;
+    }
+  }
+  return (int)every;
+}
 
 struct Pool {
   std::mutex busy;  // one upload at a time uses the workers' slots and streams
@@ -50,11 +100,6 @@ struct Pool {
 
 std::mutex g_pool_mu;
 std::vector<Pool*> g_pools;  // one per (device, shape), kept for the process lifetime
-
-int64_t env_int(const char* name, int64_t dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoll(v) : dflt;
-}
 
 int get_pool(int threads, Pool** out) {
   int dev = 0;
@@ -83,6 +128,11 @@ int get_pool(int threads, Pool** out) {
       e = cudaEventCreateWithFlags(&w.done[i], cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
+    w.raw.resize(ring);
+    for (int i = 0; i < ring; ++i) {
+      e = cudaMalloc((void**)&w.raw[i], sizeof(double) * block);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc raw staging");
+    }
     e = cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     e = cudaEventCreateWithFlags(&w.fin, cudaEventDisableTiming);
@@ -109,7 +159,7 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
   if (rc) return rc;
   std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
-  const bool skip_copy = env_int("BFLY_UPLOAD_NOCOPY", 0) != 0;  // diagnostics: conversion alone
+  const int raw_every = raw_every_for(h_payloads, n);
   // the copies must not start before work already queued on the caller's stream
   // (e.g. a previous round still reading the destination buffers)
   cudaEvent_t start;
@@ -125,20 +175,11 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
     Worker& w = pool->workers[t];
     cudaSetDevice(pool->device);
     cudaStreamWaitEvent(w.stream, start, 0);
-    int64_t count = 0;
     for (int64_t id = next.fetch_add(1); id < total && err.load() == BFLY_OK; id = next.fetch_add(1)) {
       const int32_t m = (int32_t)(id / per);
       const int64_t b = (id % per) * B, len = std::min<int64_t>(B, P - b);
-      const int k = (int)(count++ % pool->ring);
-      cudaError_t ce = cudaEventSynchronize(w.done[k]);  // the slot's previous copy has left
-      if (ce == cudaSuccess) {
-        const double* src = h_payloads[m] + b;
-        float* dst = w.slot[k];
-        for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];  // RNE, as numpy's astype
-        if (!skip_copy)
-          ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
-      }
-      if (ce == cudaSuccess) ce = cudaEventRecord(w.done[k], w.stream);
+      const bool raw = raw_every > 0 && id % raw_every == raw_every - 1;
+      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len, raw);
       if (ce != cudaSuccess) {
         std::lock_guard<std::mutex> lk(err_mu);
         err_msg = cudaGetErrorString(ce);
@@ -173,6 +214,7 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
   if (rc) return rc;
   std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
+  const int raw_every = raw_every_for(h_payloads, n);
   const int64_t B = pool->block;
   int64_t CL = (P + n_chunks - 1) / n_chunks;
   CL = (CL + B - 1) / B * B;  // chunk = whole blocks
@@ -208,7 +250,6 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
     Worker& w = pool->workers[t];
     cudaSetDevice(pool->device);
     cudaStreamWaitEvent(w.stream, start, 0);
-    int64_t count = 0;
     int cur = 0;  // chunks below `cur` are fully queued by this worker
     auto pass = [&](int upto) {  // mark chunks [cur, upto) queued on this worker's stream
       for (; cur < upto; ++cur) {
@@ -225,15 +266,8 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
       const int32_t m = (int32_t)(local / nb);
       const int64_t b = (int64_t)c * CL + (local % nb) * B;
       const int64_t len = std::min<int64_t>(B, (int64_t)c * CL + chunk_len(c) - b);
-      const int k = (int)(count++ % pool->ring);
-      cudaError_t ce = cudaEventSynchronize(w.done[k]);
-      if (ce == cudaSuccess) {
-        const double* src = h_payloads[m] + b;
-        float* dst = w.slot[k];
-        for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];  // RNE, as numpy's astype
-        ce = cudaMemcpyAsync(d_wire[m] + b, dst, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
-      }
-      if (ce == cudaSuccess) ce = cudaEventRecord(w.done[k], w.stream);
+      const bool raw = raw_every > 0 && id % raw_every == raw_every - 1;
+      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len, raw);
       if (ce != cudaSuccess) set_err(ce);
     }
     pass(NC);

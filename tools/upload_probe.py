@@ -30,9 +30,9 @@ h_ptrs = (ctypes.c_void_p * n)(*[h.data_ptr() for h in host])
 d_ptrs = (ctypes.c_void_p * n)(*[w.data_ptr() for w in wire])
 gb = n * P * 4 / 1e9
 print(f"cpus {os.cpu_count()} miners {n} P 2^{a.log2p}: {gb:.2f} GB fp32 wire", flush=True)
-for threads in (16,):
+for threads in (os.cpu_count(),):
     for block in (1 << 19,):
-        for ring in (2, 3):
+        for ring in (3,):
             os.environ["BFLY_UPLOAD_BLOCK"] = str(block)
             os.environ["BFLY_UPLOAD_RING"] = str(ring)
             best = 1e9
@@ -44,25 +44,24 @@ for threads in (16,):
                 best = min(best, time.perf_counter() - t)
             print(f"threads {threads:2d} block {block:8d} ring {ring}: {best * 1e3:7.1f} ms  "
                   f"{gb / best:6.1f} GB/s wire", flush=True)
-os.environ["BFLY_UPLOAD_BLOCK"], os.environ["BFLY_UPLOAD_RING"] = str(1 << 19), "3"
-for nocopy in ("1", "0"):
-    os.environ["BFLY_UPLOAD_NOCOPY"] = nocopy
-    for threads in (16, 8, 4, 2, 1):
-        best = 1e9
-        for _ in range(3):
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            L.check(L.lib().bfly_upload_wire(h_ptrs, n, P, d_ptrs, threads, _stream_handle()))
-            torch.cuda.synchronize()
-            best = min(best, time.perf_counter() - t)
-        print(f"{'convert only' if nocopy == '1' else 'convert+copy'} threads {threads:2d}: {best * 1e3:7.1f} ms  "
-              f"{gb / best:6.1f} GB/s wire", flush=True)
-os.environ.pop("BFLY_UPLOAD_NOCOPY")
+for every in ("0", "8", "5", "4", "3"):
+    os.environ["BFLY_UPLOAD_RAW_EVERY"] = every
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        L.check(L.lib().bfly_upload_wire(h_ptrs, n, P, d_ptrs, 0, _stream_handle()))
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t)
+    ok = all(torch.equal(w.cpu(), h.float()) for w, h in zip(wire[:3], host[:3]))
+    print(f"raw every {every}: {best * 1e3:7.1f} ms  {gb / best:6.1f} GB/s wire  exact {ok}", flush=True)
+
 ok = all(torch.equal(w.cpu(), h.float()) for w, h in zip(wire[:2], host[:2]))
 print("values exact:", ok)
 os.environ.pop("BFLY_UPLOAD_BLOCK")
 os.environ.pop("BFLY_UPLOAD_RING")
 payloads = {m: host[m].numpy() for m in range(n)}
+os.environ.pop("BFLY_UPLOAD_RAW_EVERY")
 plan = bf.plan_shards(bf.enumerate_pairs(n), P, 4, 0)
 for _ in range(4):
     torch.cuda.synchronize()
