@@ -226,7 +226,10 @@ class ShardedButterflyMerge:
         self._finish_ranges, straddlers = self._chunk_shard_ranges(plan.n_shards)
         self.straddlers = straddlers
         self._straddle_dev = torch.tensor(straddlers, dtype=torch.int32, device=self.dev)
-        late = [r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())] if G > 1 else runs
+        # BFLY_RING_LATE=0 (diagnostics): no per-chunk finishing, every special shard after the ring
+        self._per_chunk_finish = os.environ.get("BFLY_RING_LATE", "1") != "0"
+        late = ([r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())]
+                if G > 1 and self._per_chunk_finish else runs)
         self.late_runs = late
         self.special_runs = late  # kept name: ranges broadcast after the ring
         self._late_set = self._range_set(late) if late else None
@@ -262,7 +265,7 @@ class ShardedButterflyMerge:
                                       scatter_back=True, want_merged=want_merged, tolerance=tolerance)
         # last rank: late shards possible (corrupted survivors, or shards whose assignees
         # all failed) -> each chunk's are finished on the late-shard stream
-        self._late_mode = bool(self.is_last and self.job.needs_finish())
+        self._late_mode = bool(self.is_last and self.job.needs_finish() and self._per_chunk_finish)
         S, n = plan.n_shards, self.n
         self._res = torch.empty(8 * n * n + 4 * S + S + n, dtype=torch.uint8, device=self.dev)
         self.status = torch.empty(S, dtype=torch.uint8, device=self.dev)
@@ -348,8 +351,10 @@ class ShardedButterflyMerge:
                 L.check(lib.bfly_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p)))
                 self._peer[r] = p.value
         dist.barrier()
-        self._relay = torch.cuda.Stream(device=self.dev)
-        self._late = torch.cuda.Stream(device=self.dev)  # last rank: per-chunk late shards
+        self._relay = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("BFLY_RELAY_PRIORITY", "0")))
+        # last rank: per-chunk late shards, high priority so a chunk's decision does not queue
+        # behind the next chunk's reduce CTAs (the relay waits for it)
+        self._late = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("BFLY_LATE_PRIORITY", "-1")))
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -556,6 +561,11 @@ class ShardedButterflyMerge:
         if self.is_last:
             if G == 1:
                 self.job.run(L.PHASE_FINISH)
+            elif self.job.needs_finish() and not self._late_mode:
+                if self._fb_buf is not None:
+                    self.job._args.d_fallback_src = self._fb_buf.data_ptr()
+                self.job.run(L.PHASE_FINISH)
+                self.job._args.d_fallback_src = self._fb_ptr if self._fb_ptr is not None else self.job._args.d_fallback_src
             elif self.job.needs_finish() and self.straddlers:
                 a = self.job._args
                 if self._fb_buf is not None:  # the owner's replica may hold relayed values by now
