@@ -1410,7 +1410,9 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
         case BFLY_F32:  // U=4, 3 CTAs/SM, 16 CTAs/SM grid: best of tools/tune_reduce.py (profiles/)
           launch_reduce<DF32, 4, 3, true>(p, st, 16);
           break;
-        case BFLY_BF16: launch_reduce<DBF16>(p, st); break;
+        case BFLY_BF16:  // U=8, 1 CTA/SM bound, 16 CTAs/SM grid: best of the bf16 sweep (profiles/)
+          launch_reduce<DBF16, 8, 1, true>(p, st, 16);
+          break;
         default: launch_reduce<DF64W>(p, st); break;
       }
     }
@@ -1445,7 +1447,23 @@ int bfly_tune_reduce(const bfly_merge_args_t* a, int variant, int grid_per_sm, v
   int rc = build_params(a, p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (a->dtype != BFLY_F32) return fail(BFLY_E_UNSUPPORTED, "tuning covers fp32");
+  if (a->dtype == BFLY_BF16) {
+    switch (variant) {
+      case 0: launch_reduce<DBF16, 4, 1, false>(p, st, grid_per_sm); break;
+      case 1: launch_reduce<DBF16, 4, 2, true>(p, st, grid_per_sm); break;
+      case 2: launch_reduce<DBF16, 8, 1, true>(p, st, grid_per_sm); break;
+      case 3: launch_reduce<DBF16, 2, 2, true>(p, st, grid_per_sm); break;
+      case 4: launch_reduce<DBF16, 4, 3, true>(p, st, grid_per_sm); break;
+      case 5: launch_reduce<DBF16, 2, 3, true>(p, st, grid_per_sm); break;
+      case 6: launch_reduce<DBF16, 2, 4, true>(p, st, grid_per_sm); break;
+      case 7: launch_reduce<DBF16, 4, 1, true>(p, st, grid_per_sm); break;
+      default: return fail(BFLY_E_INVALID_ARG, "unknown variant");
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "bfly_tune_reduce launch");
+    return BFLY_OK;
+  }
+  if (a->dtype != BFLY_F32) return fail(BFLY_E_UNSUPPORTED, "tuning covers fp32 and bf16");
   switch (variant) {
     case 0: launch_reduce<DF32, 4, 1, false>(p, st, grid_per_sm); break;
     case 1: launch_reduce<DF32, 4, 2, true>(p, st, grid_per_sm); break;

@@ -19,24 +19,28 @@ from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan, _stream_han
 
 VARIANTS = {0: (4, 1, 'auto'), 1: (4, 2, 1), 2: (8, 1, 1), 3: (8, 2, 1), 4: (4, 3, 1), 5: (16, 1, 1), 6: (2, 4, 1),
             7: (4, 1, 1)}
+VARIANTS_BF16 = {0: (4, 1, 'auto'), 1: (4, 2, 1), 2: (8, 1, 1), 3: (2, 2, 1), 4: (4, 3, 1), 5: (2, 3, 1),
+                 6: (2, 4, 1), 7: (4, 1, 1)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--miners", type=int, default=16)
 ap.add_argument("--params", type=int, default=1_000_000_000)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+ap.add_argument("--r", type=int, default=2)
 a = ap.parse_args()
 tune = ctypes.CDLL(str(ROOT / "build" / "libbfly_tune.so"))
 tune.bfly_tune_reduce.argtypes = [ctypes.POINTER(L.MergeArgs), ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
 dev = torch.device("cuda:0")
-reps = make_replicas(a.miners, a.params, "fp32", dev)
-plan = DevicePlan(a.miners, a.params, 0, device=dev)
+reps = make_replicas(a.miners, a.params, a.dtype, dev)
+plan = DevicePlan(a.miners, a.params, 0, redundancy=a.r, device=dev)
 job = ButterflyMerge(reps, plan)
 job.run()
 torch.cuda.synchronize()
 args = job._args
 args.phase = L.PHASE_REDUCE
-alg = 2 * a.miners * a.params * 4
-for v, (U, minb, outer) in VARIANTS.items():
+alg = 2 * a.miners * a.params * (2 if a.dtype == "bf16" else 4)
+for v, (U, minb, outer) in (VARIANTS_BF16 if a.dtype == "bf16" else VARIANTS).items():
     for gps in (1, 2, 4, 8, 16):
         rc = tune.bfly_tune_reduce(ctypes.byref(args), v, gps, _stream_handle())
         if rc:
