@@ -211,3 +211,20 @@ def test_native_executor_issues_the_same_ops(G, K, NB, r, late):
         got = [(a, b, c, d, e, (f if a >= 2 else -1), (h & 0xFFFFFFFF if a < 2 else 0)) for a, b, c, d, e, f, h in got]
         want = [(a, b, c, d, e, f, h & 0xFFFFFFFF) for a, b, c, d, e, f, h in want]
         assert got == want, (g, G, K, NB, r)
+
+
+@pytest.mark.parametrize("P,chunk", [(10**9, 1 << 24), (4096 * 8 + 5, 8192), (6_000_007, 1 << 20), (1 << 20, 1 << 20),
+                                     (50_000_000, 1 << 22), (3, 4096)])
+def test_chunk_edges_cover_the_payload(P, chunk):
+    """multigpu.chunk_edges: contiguous cover of [0, P), every chunk fits an inbox slot,
+    inner edges on 4096-element (k_reduce tile) boundaries, ramps mirror each other."""
+    from paper_2507_17766_b200.multigpu import chunk_edges
+
+    for ramp in (False, True):
+        e = chunk_edges(P, chunk, ramp=ramp)
+        sizes = [b - a for a, b in zip(e, e[1:])]
+        assert e[0] == 0 and e[-1] == P and all(0 < x <= chunk for x in sizes)
+        assert all(x % 4096 == 0 for x in e[1:-1])
+        if ramp and sizes[0] < chunk:
+            head = [x for x in sizes[:4] if x < chunk]
+            assert sizes[-len(head):][::-1][1:] == head[1:]  # mirrored (the last one absorbs the tail)
