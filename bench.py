@@ -368,8 +368,9 @@ def run_multi(cfg, args, rank, world):
             "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
             "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "miners_per_gpu": n_local,
                        "params": P, "replica_dtype": dtype, "redundancy": r, "deceptive": len(bad),
-                       "parallelism": f"miners in contiguous blocks over {world} GPUs; fp64 running-sum chain "
-                                      f"(NCCL send/recv, {args.chunk}-element chunks) + broadcast of the result",
+                       "parallelism": f"miners in contiguous blocks over {world} GPUs; fp64 running sums chained "
+                                      f"rank to rank (TMA bulk stores into IPC-mapped peer inboxes over NVLink, "
+                                      f"up to {args.chunk}-element chunks), final vector relayed round the ring",
                        "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
             "params_merged_per_s": P / t_step,
             "roofline": {"bound": "hbm" if per_gpu_hbm / hbm_peak > float(nvl.item()) / nvl_peak else "nvlink",
