@@ -5,7 +5,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-O2,-Wall -Xptxas -v --expt-relaxed-constexpr
 PKG := paper_2507_17766_b200
 SRCS := $(PKG)/csrc/bfly_plan.cu $(PKG)/csrc/bfly_merge.cu $(PKG)/csrc/bfly_peer.cu $(PKG)/csrc/bfly_host.cu \
-        $(PKG)/csrc/bfly_validate.cu
+        $(PKG)/csrc/bfly_validate.cu $(PKG)/csrc/bfly_ring.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h) include/bfly.h
 LIB := $(PKG)/libbfly.so
 

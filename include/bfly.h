@@ -248,6 +248,41 @@ int bfly_ring_round(const bfly_ring_desc_t* desc, uint32_t round_index);
 int bfly_ring_ops(int32_t rank, int32_t world, int32_t k_chunks, int32_t nb, uint32_t round_index,
                   int32_t late, int32_t* out, int32_t cap);
 
+/* The whole multi-GPU round in ONE persistent kernel per GPU (k_ring): the payload is
+ * cut into tiles dealt round-robin to `lanes` lanes; lane c of every rank is a CTA
+ * (a CTA pair on ranks < last: chain + relay) that hands tile after tile to lane c of
+ * the neighbouring rank through a slot ring in the neighbour's IPC region, with
+ * 64-bit monotonic flags stored / polled by the SMs (st.release.sys / ld.acquire.sys)
+ * — the transfer of tile i overlaps the reduction of tile i+1.  Same values as
+ * bfly_ring_round (running fp64 sums in ascending miner order); only for rounds in
+ * which every shard is fast (no corrupted survivor, fewer than r failures) and every
+ * shard has >= 2 elements.  Replaces, for those rounds, the chunked ring of
+ * bfly_ring_round (which stays for rounds with corrupted / lost shards).          */
+typedef struct bfly_ring_fused_desc {
+  int32_t rank, world;           /* this process's rank and the ring size            */
+  int32_t lanes, nb;             /* lanes (equal on every rank), slots per lane      */
+  int32_t dtype;                 /* BFLY_* element type of the replicas              */
+  int32_t n_src, n_dst, n_div;   /* alive local replicas, all local replicas, divisor */
+  int64_t payload_len;           /* P                                                */
+  uint64_t round_index;          /* rounds already run on this region (flags are monotonic) */
+  const uint64_t* peer_base;     /* [world] region base of every rank as mapped here  */
+  const void* const* d_src;      /* device table of the alive local replicas          */
+  void* const* d_dst;            /* device table of every local replica (scatter-back) */
+  double* d_merged;              /* last rank, optional: fp64 merged vector            */
+  const bfly_merge_args_t* merge_args; /* last rank, optional: the round's per-shard
+                                    setup (status / entries / flags) runs first       */
+} bfly_ring_fused_desc_t;
+/* Lanes this device runs (all CTAs co-resident: cooperative launch). */
+int32_t bfly_ring_fused_lanes(int32_t dtype);
+/* Byte layout of one rank's region for (lanes, nb, dtype): offsets of the final-vector
+ * slots and of the flags, and the total size to allocate (bfly_ipc_alloc zeroes it). */
+int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* off_fin, int64_t* off_flags,
+                           int64_t* total);
+int bfly_ring_fused(const bfly_ring_fused_desc_t* desc, void* stream);
+/* Diagnostics: with BFLY_RING_PROFILE set, per CTA 20 counters of the last k_ring
+ * launch (cycles spent in each wait, per role); copies n of them, returns the count. */
+int bfly_ring_fused_profile(unsigned long long* host_out, int32_t n);
+
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);
 

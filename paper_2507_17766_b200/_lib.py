@@ -23,6 +23,10 @@ PHASE_ALL, PHASE_REDUCE, PHASE_FINISH = 0, 1, 2
 
 # every symbol include/bfly.h declares (tests/test_capi.py checks the export table)
 EXPORTS = (
+    "bfly_ring_fused",
+    "bfly_ring_fused_lanes",
+    "bfly_ring_fused_layout",
+    "bfly_ring_fused_profile",
     "bfly_version",
     "bfly_last_error",
     "bfly_n_shards",
@@ -138,6 +142,26 @@ class RingDesc(ctypes.Structure):
     ]
 
 
+class RingFusedDesc(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("lanes", ctypes.c_int32),
+        ("nb", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("n_src", ctypes.c_int32),
+        ("n_dst", ctypes.c_int32),
+        ("n_div", ctypes.c_int32),
+        ("payload_len", ctypes.c_int64),
+        ("round_index", ctypes.c_uint64),
+        ("peer_base", ctypes.c_void_p),
+        ("d_src", ctypes.c_void_p),
+        ("d_dst", ctypes.c_void_p),
+        ("d_merged", ctypes.c_void_p),
+        ("merge_args", ctypes.POINTER(MergeArgs)),
+    ]
+
+
 _lib = None
 
 
@@ -183,6 +207,11 @@ def lib() -> ctypes.CDLL:
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
     L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
+    L.bfly_ring_fused_lanes.argtypes = [i32]
+    L.bfly_ring_fused_lanes.restype = i32
+    L.bfly_ring_fused_layout.argtypes = [i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.bfly_ring_fused.argtypes = [ctypes.POINTER(RingFusedDesc), vp]
+    L.bfly_ring_fused_profile.argtypes = [vp, i32]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)
     _lib = L

@@ -1,0 +1,875 @@
+// bfly_ring.cu — the multi-GPU merge round as ONE persistent, TMA-driven kernel per GPU.
+//
+// The reference reduces every shard over all miners in one process in ascending
+// miner order (butterfly.py:216-240, mean_reducer :156-158).  With the miners in
+// contiguous blocks over G GPUs that order is kept exactly by carrying the fp64
+// running sums from GPU to GPU (chain g = 0 .. G-1), dividing on the last GPU and
+// relaying the final values round the ring (last -> 0 -> 1 -> ... -> G-2) into every
+// replica (the scatter-back, orchestrator.py:581-590).
+//
+// k_ring runs that whole round in one launch, tile by tile:
+//   * the payload is cut into tiles of TE elements (4 KB of each replica), dealt
+//     round-robin to L lanes = one CTA per SM (tile t -> lane t % L, step t / L);
+//     lane c of rank g exchanges only with lane c of its neighbours;
+//   * per CTA, warp-specialised and asynchronous:
+//       LOADER warp   TMA bulk loads (cp.async.bulk ... mbarrier::complete_tx) of the
+//                     incoming running sums (inbox slot) and of the replica tiles into
+//                     a ring of shared-memory stages — up to NS x RB x 4 KB in flight;
+//       8 COMPUTE warps  read the stages, fp64 adds in ascending miner order (the
+//                     last rank also divides), write the outgoing tile to shared memory;
+//       STORER warp   TMA bulk stores of that tile into the next rank's inbox slot over
+//                     NVLink (and, on the last rank, into every local replica), then
+//                     publishes it;
+//       RELAY warps   (ranks < last) a bulk load of the final tile from the inbox and
+//                     bulk stores into every local replica and the successor's inbox:
+//                     the scatter-back without a single SM load or store;
+//   * each rank's inboxes are NB-slot rings per lane in its IPC region; producer and
+//     consumer order themselves with 64-bit monotonic counters (ready / free) in the
+//     waiter's region: the producer stores `ready` with st.release.sys after its bulk
+//     group has landed, the consumer polls with ld.acquire.sys and returns the slot
+//     (`free`) once it has been loaded.  No kernel launches, stream memory operations
+//     or host round trips per tile: NVLink transfers of tile i overlap the HBM stream
+//     of tile i+1 and the ring fills in G tile steps.  The inboxes (L x NB x 12 KB)
+//     stay small enough to live in L2.
+// Deadlock freedom: every wait of step j points at step j of an earlier stage of the
+// path (chain 0..last, relay 0..last-1) or at step j - NB; the chain and the relay of a
+// lane run in different warps, and all CTAs are co-resident (cooperative launch).
+// Every wait traps after kRingTimeoutNs instead of hanging the GPU.
+//
+// Only rounds whose shards are all fast use it (no corrupted survivor, fewer than r
+// failures): their final value is the mean, so no decision waits for the whole
+// vector.  Rounds with corrupted / lost shards run the chunked ring of bfly_peer.cu.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+
+#include "bfly_elem.cuh"
+#include "bfly_internal.cuh"
+
+namespace bfly {
+
+enum FusedFlag : int { kFAccReady = 0, kFAccFree = 1, kFFinReady = 2, kFFinFree = 3, kFAbort = 4 };
+constexpr unsigned long long kRingTimeoutNs = 20ull * 1000 * 1000 * 1000;
+constexpr int kRingCompute = kThreads;        // 8 compute warps
+constexpr int kRingThreads = kThreads + 160;  // + loader, storer, relay loader, relay storer, publisher
+constexpr int kWLoad = kThreads / 32, kWStore = kWLoad + 1, kWRLoad = kWLoad + 2, kWRStore = kWLoad + 3,
+              kWPub = kWLoad + 4;
+constexpr int kNS = 4;            // replica stages
+constexpr int kRB = 8;            // replica tiles per stage
+constexpr int kNR = 4;            // relay stages
+constexpr int kNO = 4;            // outgoing-tile stages
+constexpr int kMaxLag = 3;        // a step is published p.lag (1..3) steps later, when its bytes have landed
+constexpr int kTileBytes = 4096;  // one replica's share of a tile
+
+struct RingParams {
+  int g, G, L, NB;
+  int64_t P, T;  // elements, tiles
+  uint64_t round;
+  unsigned char* my;     // own region
+  unsigned char* nxt;    // chain target (g + 1), or rank 0 for the last rank
+  unsigned char* prv;    // acc credits go here (g - 1); null on rank 0
+  unsigned char* fsucc;  // relay successor (g + 1 < last), else null
+  unsigned char* fpred;  // relay predecessor (last for rank 0, else g - 1)
+  int64_t off_fin, off_flags;
+  const void* const* src;
+  int n_src;
+  void* const* dst;
+  int n_dst;
+  int n_div;
+  double* merged;
+  unsigned long long* prof;  // diagnostics (BFLY_RING_PROFILE): wait cycles per CTA and counter
+  int pub_every;             // publish every pub_every-th step (each publication covers the ones before)
+  int pub_relaxed;           // 1: after wait_group the flag is a relaxed store (no MEMBAR.SYS)
+  int lag;                   // publication lag in steps (1..kMaxLag)
+};
+
+template <class D>
+struct RingGeom {
+  static constexpr int ESIZE = 32 / D::K;       // bytes per replica element
+  static constexpr int KE = 16 / ESIZE;         // elements per thread (16 B of each replica)
+  static constexpr int TE = kRingCompute * KE;  // tile elements
+  using Acc = typename D::Acc;                  // running sums travel at accumulator width
+  static constexpr int ACC_BYTES = TE * (int)sizeof(Acc);
+  static constexpr int FIN_BYTES = TE * ESIZE;  // == kTileBytes
+  // shared memory: replica stages | 2 acc stages | 2 out stages | relay stages | barriers | pointers
+  static constexpr int OFF_REP = 0;
+  static constexpr int OFF_ACC = OFF_REP + kNS * kRB * kTileBytes;
+  static constexpr int OFF_OUT = OFF_ACC + 2 * ACC_BYTES;
+  static constexpr int OFF_REL = OFF_OUT + kNO * ACC_BYTES;
+  static constexpr int OFF_BAR = OFF_REL + kNR * FIN_BYTES;
+  static constexpr int N_BAR = 2 * kNS + 4 + 2 * kNO + 2 * kNR;
+  static constexpr int OFF_MAIL = OFF_BAR + 8 * N_BAR;  // landed-step counters: [0] chain / reduce, [1] relay
+  static constexpr int OFF_PTR = OFF_MAIL + 16;
+};
+
+// ---------------------------------------------------------------------------
+// flags, mbarriers, bulk copies
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t* flag_at(unsigned char* region, const RingParams& p, int f, int lane) {
+  return reinterpret_cast<uint64_t*>(region + p.off_flags) + (int64_t)f * p.L + lane;
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* a) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* a, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+// consumer -> producer: the slot has been loaded (its bulk load completed before the
+// barrier this thread waited on), so no fence is needed
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* a, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+// Publish `v` (steps landed) to the consumer.  The bulk group holding the data has
+// completed (cp.async.bulk.wait_group: its writes are performed at the destination),
+// so the flag may follow as a plain system-scope store; pub_relaxed == 0 keeps the
+// formal release (a MEMBAR.SYS per publication).
+__device__ __forceinline__ void publish(const RingParams& p, uint64_t* f, uint64_t v) {
+  if (p.pub_relaxed)
+    st_relaxed_sys(f, v);
+  else
+    st_release_sys(f, v);
+}
+// storer -> publisher warp: `v` steps have landed (CTA-scope release through shared memory)
+__device__ __forceinline__ void mail_post(uint64_t* box, uint64_t v) {
+  asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(box)), "l"(v)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t mail_read(const uint64_t* box) {
+  uint64_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];"
+               : "=l"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(box))
+               : "memory");
+  return v;
+}
+
+// Wait-cycle counters of one role (diagnostics only; p.prof == null in production).
+constexpr int kProfSlots = 20;
+struct Prof {
+  unsigned long long* out;
+  unsigned long long acc[4] = {0, 0, 0, 0};
+  long long t = 0;
+  __device__ explicit Prof(const RingParams& p, int first)
+      : out(p.prof ? p.prof + blockIdx.x * kProfSlots + first : nullptr) {}
+  __device__ __forceinline__ void start() {
+    if (out) t = clock64();
+  }
+  __device__ __forceinline__ void stop(int k) {
+    if (out) acc[k] += (unsigned long long)(clock64() - t);
+  }
+  __device__ __forceinline__ void flush() {
+    if (out)
+      for (int k = 0; k < 4; ++k) out[k] = acc[k];
+  }
+};
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __noinline__ void ring_abort(const RingParams& p) {
+  volatile uint64_t* abort_word = flag_at(p.my, p, kFAbort, 0);
+  *abort_word = 1;
+  __threadfence_system();
+  __trap();
+}
+
+// Wait until *f >= v, caching the last value read (the upstream usually runs ahead,
+// so most steps need no load).  Traps when the ring stops making progress.
+__device__ __forceinline__ void flag_wait(const RingParams& p, const uint64_t* f, uint64_t v, uint64_t& known) {
+  if (known >= v) return;
+  known = ld_acquire_sys(f);
+  if (known < v) {
+    const uint64_t t0 = global_ns();
+    const volatile uint64_t* abort_word = flag_at(p.my, p, kFAbort, 0);
+    while ((known = ld_acquire_sys(f)) < v) {
+      __nanosleep(20);
+      if (*abort_word || global_ns() - t0 > kRingTimeoutNs) ring_abort(p);
+    }
+  }
+  // the bulk copies that follow (async proxy) are ordered after the acquire
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_addr(b)),
+               "r"(bytes)
+               : "memory");
+}
+// wait for the completion of the phase with the given parity
+__device__ __forceinline__ void mbar_wait(const RingParams& p, uint64_t* b, unsigned parity) {
+  uint64_t t0 = 0;
+  for (int spin = 0;; ++spin) {
+    unsigned done;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if ((spin & 1023) == 1023) {
+      const uint64_t t = global_ns();
+      if (!t0)
+        t0 = t;
+      else if (t - t0 > kRingTimeoutNs)
+        ring_abort(p);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_stream(void* sdst, const void* gsrc, unsigned bytes, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+// shared -> global (a peer inbox slot, or a local replica with an evict-first hint)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_stream(void* gdst, const void* ssrc, unsigned bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int KEEP>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(KEEP) : "memory");
+}
+// every bulk group but the newest KEEP has landed; the flag publishing it may follow
+template <int KEEP>
+__device__ __forceinline__ void bulk_wait_landed() {
+  asm volatile("cp.async.bulk.wait_group %0;\n\tfence.proxy.async.global;" ::"n"(KEEP) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_landed_n(int keep) {
+  if (keep <= 1)
+    bulk_wait_landed<1>();
+  else if (keep == 2)
+    bulk_wait_landed<2>();
+  else
+    bulk_wait_landed<3>();
+}
+
+__device__ __forceinline__ unsigned round16(int64_t b) { return (unsigned)((b + 15) & ~(int64_t)15); }
+
+template <class D>
+__device__ __forceinline__ typename D::Acc* acc_slot(unsigned char* region, const RingParams& p, int lane, int slot) {
+  return reinterpret_cast<typename D::Acc*>(region) + ((int64_t)lane * p.NB + slot) * RingGeom<D>::TE;
+}
+template <class D>
+__device__ __forceinline__ unsigned char* fin_slot(unsigned char* region, const RingParams& p, int lane, int slot) {
+  return region + p.off_fin + ((int64_t)lane * p.NB + slot) * RingGeom<D>::FIN_BYTES;
+}
+
+// 16 bytes of one replica -> KE values / KE values -> 16 bytes (through the 32-byte
+// helpers of bfly_elem.cuh; the unused half is dead code)
+template <class D>
+__device__ __forceinline__ void unpack16(const uint4& v, typename D::Acc* x) {
+  V8 w;
+  w.w[0] = v.x, w.w[1] = v.y, w.w[2] = v.z, w.w[3] = v.w;
+  w.w[4] = w.w[5] = w.w[6] = w.w[7] = 0;
+  typename D::Acc t[D::K];
+  D::unpack(w, t);
+#pragma unroll
+  for (int k = 0; k < RingGeom<D>::KE; ++k) x[k] = t[k];
+}
+template <class D>
+__device__ __forceinline__ uint4 pack16(const typename D::Acc* x) {
+  typename D::Acc t[D::K];
+#pragma unroll
+  for (int k = 0; k < D::K; ++k) t[k] = k < RingGeom<D>::KE ? x[k] : D::zero();
+  const V8 w = D::pack(t);
+  return make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+}
+
+// ---------------------------------------------------------------------------
+// the roles
+// ---------------------------------------------------------------------------
+
+struct Lane {
+  int c;
+  int64_t steps;
+  uint64_t base;  // monotonic flags: the steps of earlier rounds on this region
+};
+
+template <class D>
+__device__ __forceinline__ int64_t tile_start(const RingParams& p, const Lane& ln, int64_t i) {
+  return (ln.c + i * p.L) * (int64_t)RingGeom<D>::TE;
+}
+
+// barriers (in shared memory, after the stages)
+struct Bars {
+  uint64_t *rep_full, *rep_empty, *acc_full, *acc_empty, *out_full, *out_empty, *rel_full, *rel_empty;
+  template <class D>
+  __device__ static Bars at(unsigned char* sm) {
+    uint64_t* b = reinterpret_cast<uint64_t*>(sm + RingGeom<D>::OFF_BAR);
+    Bars r;
+    r.rep_full = b;
+    r.rep_empty = b + kNS;
+    r.acc_full = b + 2 * kNS;
+    r.acc_empty = b + 2 * kNS + 2;
+    r.out_full = b + 2 * kNS + 4;
+    r.out_empty = b + 2 * kNS + 4 + kNO;
+    r.rel_full = b + 2 * kNS + 4 + 2 * kNO;
+    r.rel_empty = b + 2 * kNS + 4 + 2 * kNO + kNR;
+    return r;
+  }
+};
+
+// LOADER (lane 0 of warp kWLoad): incoming sums and replica tiles into the stages
+template <class D>
+__device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* sm, const void** s_src) {
+  using G = RingGeom<D>;
+  const Bars B = Bars::at<D>(sm);
+  const bool has_in = p.g > 0;
+  uint64_t* ready_in = flag_at(p.my, p, kFAccReady, ln.c);
+  const uint64_t pol = policy_evict_first();
+  uint64_t known = 0;
+  int64_t rs = 0;  // replica stage uses so far
+  Prof pf(p, 0);
+  for (int64_t i = 0; i < ln.steps; ++i) {
+    const uint64_t j = ln.base + (uint64_t)i;
+    const int64_t t0 = tile_start<D>(p, ln, i);
+    const int64_t n = min((int64_t)G::TE, p.P - t0);
+    // the replica tiles first: they do not wait for the upstream rank
+    for (int q0 = 0; n == G::TE && q0 < p.n_src; q0 += kRB, ++rs) {
+      const int s = (int)(rs % kNS);
+      const int64_t u = rs / kNS;
+      const int nb = min(kRB, p.n_src - q0);
+      pf.start();
+      if (u >= 1) mbar_wait(p, B.rep_empty + s, (unsigned)((u - 1) & 1));
+      pf.stop(0);
+      mbar_expect_tx(B.rep_full + s, (unsigned)(nb * kTileBytes));
+      unsigned char* dst = sm + G::OFF_REP + s * kRB * kTileBytes;
+      for (int q = 0; q < nb; ++q)
+        bulk_load_stream(dst + q * kTileBytes, (const unsigned char*)s_src[q0 + q] + t0 * G::ESIZE, kTileBytes,
+                         B.rep_full + s, pol);
+    }
+    // (the partial last tile: compute warps read its replicas directly)
+    if (has_in) {
+      pf.start();
+      flag_wait(p, ready_in, j + 1, known);
+      pf.stop(1);
+      const int a = (int)(i & 1);
+      const int64_t ua = i >> 1;
+      pf.start();
+      if (ua >= 1) mbar_wait(p, B.acc_empty + a, (unsigned)((ua - 1) & 1));
+      pf.stop(2);
+      const unsigned bytes = round16(n * (int64_t)sizeof(typename G::Acc));
+      mbar_expect_tx(B.acc_full + a, bytes);
+      bulk_load(sm + G::OFF_ACC + a * G::ACC_BYTES, acc_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)), bytes,
+                B.acc_full + a);
+    }
+  }
+  pf.flush();
+}
+
+// COMPUTE warps: running sums (chain) or sum and mean (REDUCE) of the lane's tiles
+template <class D, bool REDUCE>
+__device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char* sm, const void** s_src,
+                             void** s_dst) {
+  using G = RingGeom<D>;
+  using Acc = typename G::Acc;
+  constexpr int KE = G::KE;
+  const Bars B = Bars::at<D>(sm);
+  const int tid = threadIdx.x;
+  const bool lead = (tid & 31) == 0;
+  const bool has_in = p.g > 0;
+  int64_t rs = 0;
+  Prof pf(p, threadIdx.x == 0 ? 4 : -1);
+  if (threadIdx.x) pf.out = nullptr;
+  for (int64_t i = 0; i < ln.steps; ++i) {
+    const int64_t t0 = tile_start<D>(p, ln, i);
+    const int64_t n = min((int64_t)G::TE, p.P - t0);
+    const int a = (int)(i & 1);
+    const int64_t ua = i >> 1;
+    const Acc* in = reinterpret_cast<const Acc*>(sm + G::OFF_ACC + a * G::ACC_BYTES);
+    const int o = (int)(i % kNO);
+    const int64_t uo = i / kNO;
+    unsigned char* out = sm + G::OFF_OUT + o * G::ACC_BYTES;
+    pf.start();
+    if (has_in) mbar_wait(p, B.acc_full + a, (unsigned)(ua & 1));
+    pf.stop(0);
+    pf.start();
+    if (uo >= 1) mbar_wait(p, B.out_empty + o, (unsigned)((uo - 1) & 1));
+    pf.stop(1);
+    if (n == G::TE) {
+      Acc acc[KE];
+#pragma unroll
+      for (int k = 0; k < KE; ++k) acc[k] = has_in ? in[tid * KE + k] : D::zero();
+      for (int q0 = 0; q0 < p.n_src; q0 += kRB, ++rs) {
+        const int s = (int)(rs % kNS);
+        const int nb = min(kRB, p.n_src - q0);
+        pf.start();
+        mbar_wait(p, B.rep_full + s, (unsigned)((rs / kNS) & 1));
+        pf.stop(2);
+        const unsigned char* st = sm + G::OFF_REP + s * kRB * kTileBytes + tid * 16;
+        for (int q = 0; q < nb; ++q) {  // ascending miner order (numpy's)
+          Acc x[KE];
+          unpack16<D>(*reinterpret_cast<const uint4*>(st + q * kTileBytes), x);
+#pragma unroll
+          for (int k = 0; k < KE; ++k) acc[k] = D::add(acc[k], x[k]);
+        }
+        __syncwarp();
+        if (lead) mbar_arrive(B.rep_empty + s);
+      }
+      if constexpr (REDUCE) {
+#pragma unroll
+        for (int k = 0; k < KE; ++k) acc[k] = D::mean(acc[k], p.n_div);
+        if (p.merged) {
+          double* m = p.merged + t0 + tid * KE;
+#pragma unroll
+          for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
+        }
+        *reinterpret_cast<uint4*>(out + tid * 16) = pack16<D>(acc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < KE; ++k) reinterpret_cast<Acc*>(out)[tid * KE + k] = acc[k];
+      }
+    } else {  // partial last tile: element by element from global memory
+      for (int64_t e = tid; e < n; e += kRingCompute) {
+        Acc v = has_in ? in[e] : D::zero();
+        for (int q = 0; q < p.n_src; ++q) v = D::add(v, D::load(s_src[q], t0 + e));
+        if constexpr (REDUCE) {
+          v = D::mean(v, p.n_div);
+          if (p.merged) p.merged[t0 + e] = D::widen(v);
+          for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], t0 + e, D::widen(v));
+          D::store(out, e, D::widen(v));
+        } else {
+          reinterpret_cast<Acc*>(out)[e] = v;
+        }
+      }
+    }
+    if (has_in) {  // the incoming sums have been read
+      __syncwarp();
+      if (lead) mbar_arrive(B.acc_empty + a);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // out stage -> TMA reads
+    __syncwarp();
+    if (lead) mbar_arrive(B.out_full + o);
+  }
+  pf.flush();
+}
+
+// STORER (lane 0 of warp kWStore): returns the inbox slot, bulk-stores the outgoing
+// tile (next rank's inbox; on the last rank also every local replica) and publishes
+// each step once its bytes have landed (one step later, so it never stalls the pipe)
+template <class D, bool REDUCE>
+__device__ void ring_storer(const RingParams& p, const Lane& ln, unsigned char* sm, void** s_dst) {
+  using G = RingGeom<D>;
+  using Acc = typename G::Acc;
+  const Bars B = Bars::at<D>(sm);
+  uint64_t* credit = p.g > 0 ? flag_at(p.prv, p, kFAccFree, ln.c) : nullptr;
+  uint64_t* free_out = REDUCE ? flag_at(p.my, p, kFFinFree, ln.c) : flag_at(p.my, p, kFAccFree, ln.c);
+  uint64_t* mail = reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL);  // published by the publisher warp
+  const uint64_t pol = policy_evict_first();
+  uint64_t known = 0;
+  Prof pf(p, 8);
+  for (int64_t i = 0; i < ln.steps; ++i) {
+    const uint64_t j = ln.base + (uint64_t)i;
+    const int slot = (int)(j % (uint64_t)p.NB);
+    const int64_t t0 = tile_start<D>(p, ln, i);
+    const int64_t n = min((int64_t)G::TE, p.P - t0);
+    const int o = (int)(i % kNO);
+    pf.start();
+    mbar_wait(p, B.out_full + o, (unsigned)((i / kNO) & 1));
+    pf.stop(0);
+    if (credit) st_relaxed_sys(credit, j + 1);  // our inbox slot has been loaded and used
+    pf.start();
+    if (j >= (uint64_t)p.NB) flag_wait(p, free_out, j + 1 - p.NB, known);
+    pf.stop(1);
+    const unsigned char* out = sm + G::OFF_OUT + o * G::ACC_BYTES;
+    if constexpr (REDUCE) {
+      if (n == G::TE)
+        for (int d = 0; d < p.n_dst; ++d)
+          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, out, kTileBytes, pol);
+      bulk_store(fin_slot<D>(p.nxt, p, ln.c, slot), out, round16(n * G::ESIZE));
+    } else {
+      bulk_store(acc_slot<D>(p.nxt, p, ln.c, slot), out, round16(n * (int64_t)sizeof(Acc)));
+    }
+    bulk_commit();
+    pf.start();
+    bulk_wait_read<1>();  // step i - 1's stage has been read out: hand it back
+    pf.stop(2);
+    if (i >= 1) mbar_arrive(B.out_empty + (int)((i - 1) % kNO));
+    if (i >= p.lag && (i % p.pub_every) == 0) {  // step i - lag has landed: publish it
+      pf.start();
+      bulk_wait_landed_n(p.lag);
+      pf.stop(3);
+      mail_post(mail, j + 1 - p.lag);
+    }
+  }
+  if (ln.steps > 0) {
+    bulk_wait_landed<0>();
+    mail_post(mail, ln.base + (uint64_t)ln.steps);
+  }
+  pf.flush();
+}
+
+// RELAY (ranks < last): lane 0 of warp kWRLoad loads the final tile from the inbox,
+// the warp after it bulk-stores the tile into every local replica and the successor
+template <class D>
+__device__ void ring_relay_loader(const RingParams& p, const Lane& ln, unsigned char* sm) {
+  using G = RingGeom<D>;
+  const Bars B = Bars::at<D>(sm);
+  uint64_t* ready_in = flag_at(p.my, p, kFFinReady, ln.c);
+  uint64_t known = 0;
+  Prof pf(p, 12);
+  for (int64_t i = 0; i < ln.steps; ++i) {
+    const uint64_t j = ln.base + (uint64_t)i;
+    const int64_t n = min((int64_t)G::TE, p.P - tile_start<D>(p, ln, i));
+    const int s = (int)(i % kNR);
+    const int64_t u = i / kNR;
+    pf.start();
+    flag_wait(p, ready_in, j + 1, known);
+    pf.stop(0);
+    pf.start();
+    if (u >= 1) mbar_wait(p, B.rel_empty + s, (unsigned)((u - 1) & 1));
+    pf.stop(1);
+    const unsigned bytes = round16(n * G::ESIZE);
+    mbar_expect_tx(B.rel_full + s, bytes);
+    bulk_load(sm + G::OFF_REL + s * G::FIN_BYTES, fin_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)), bytes,
+              B.rel_full + s);
+  }
+  pf.flush();
+}
+
+template <class D>
+__device__ void ring_relay_storer(const RingParams& p, const Lane& ln, unsigned char* sm, void** s_dst) {
+  using G = RingGeom<D>;
+  const Bars B = Bars::at<D>(sm);
+  const bool lead = (threadIdx.x & 31) == 0;
+  uint64_t* credit = flag_at(p.fpred, p, kFFinFree, ln.c);
+  uint64_t* free_out = p.fsucc ? flag_at(p.my, p, kFFinFree, ln.c) : nullptr;
+  uint64_t* mail = reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL) + 1;  // published by the publisher warp
+  const uint64_t pol = policy_evict_first();
+  uint64_t known = 0;
+  Prof pf(p, 16);
+  if (threadIdx.x & 31) pf.out = nullptr;
+  for (int64_t i = 0; i < ln.steps; ++i) {
+    const uint64_t j = ln.base + (uint64_t)i;
+    const int64_t t0 = tile_start<D>(p, ln, i);
+    const int64_t n = min((int64_t)G::TE, p.P - t0);
+    const int s = (int)(i % kNR);
+    const unsigned char* st = sm + G::OFF_REL + s * G::FIN_BYTES;
+    pf.start();
+    mbar_wait(p, B.rel_full + s, (unsigned)((i / kNR) & 1));
+    pf.stop(0);
+    if (n < G::TE) {  // partial last tile: the whole warp copies the bytes
+      const int64_t nb = n * G::ESIZE;
+      for (int d = 0; d < p.n_dst; ++d)
+        for (int64_t b = threadIdx.x & 31; b < nb; b += 32) ((unsigned char*)s_dst[d])[t0 * G::ESIZE + b] = st[b];
+      __syncwarp();
+    }
+    if (lead) {
+      st_relaxed_sys(credit, j + 1);  // the inbox slot has been loaded
+      if (n == G::TE)
+        for (int d = 0; d < p.n_dst; ++d)
+          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, st, kTileBytes, pol);
+      if (p.fsucc) {
+        pf.start();
+        if (j >= (uint64_t)p.NB) flag_wait(p, free_out, j + 1 - p.NB, known);
+        pf.stop(1);
+        bulk_store(fin_slot<D>(p.fsucc, p, ln.c, (int)(j % (uint64_t)p.NB)), st, round16(n * G::ESIZE));
+      }
+      bulk_commit();
+      pf.start();
+      bulk_wait_read<1>();
+      pf.stop(2);
+      if (i >= 1) mbar_arrive(B.rel_empty + (int)((i - 1) % kNR));
+      if (p.fsucc && i >= p.lag && (i % p.pub_every) == 0) {
+        pf.start();
+        bulk_wait_landed_n(p.lag);
+        pf.stop(3);
+        mail_post(mail, j + 1 - p.lag);
+      }
+    }
+    __syncwarp();
+  }
+  if (lead && ln.steps > 0) {
+    bulk_wait_landed<0>();  // the last replica stores have landed before the kernel ends
+    if (p.fsucc) mail_post(mail, ln.base + (uint64_t)ln.steps);
+  }
+  pf.flush();
+}
+
+// PUBLISHER (lane 0 of warp kWPub): forwards the storers' landed-step counts to the
+// consumers' ready flags with a system-scope release.  The release (a MEMBAR.SYS)
+// takes microseconds; in its own warp it overlaps the storers' work, and a slow
+// publication simply covers several steps at once.
+template <class D>
+__device__ void ring_publisher(const RingParams& p, const Lane& ln, unsigned char* sm) {
+  using G = RingGeom<D>;
+  const bool last = p.g == p.G - 1;
+  const uint64_t* mail = reinterpret_cast<const uint64_t*>(sm + G::OFF_MAIL);
+  uint64_t* out_c = last ? flag_at(p.nxt, p, kFFinReady, ln.c) : flag_at(p.nxt, p, kFAccReady, ln.c);
+  uint64_t* out_r = (!last && p.fsucc) ? flag_at(p.fsucc, p, kFFinReady, ln.c) : nullptr;
+  const uint64_t target = ln.base + (uint64_t)ln.steps;
+  uint64_t done_c = ln.base, done_r = out_r ? ln.base : target;
+  uint64_t t0 = global_ns();
+  const volatile uint64_t* abort_word = flag_at(p.my, p, kFAbort, 0);
+  while (done_c < target || done_r < target) {
+    bool moved = false;
+    const uint64_t vc = mail_read(mail);
+    if (vc > done_c) {
+      publish(p, out_c, vc);
+      done_c = vc;
+      moved = true;
+    }
+    if (out_r) {
+      const uint64_t vr = mail_read(mail + 1);
+      if (vr > done_r) {
+        publish(p, out_r, vr);
+        done_r = vr;
+        moved = true;
+      }
+    }
+    if (moved) {
+      t0 = global_ns();
+    } else {
+      __nanosleep(64);
+      if (*abort_word || global_ns() - t0 > kRingTimeoutNs) ring_abort(p);
+    }
+  }
+}
+
+template <class D>
+__global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  using G = RingGeom<D>;
+  const void** s_src = reinterpret_cast<const void**>(sm + G::OFF_PTR);
+  void** s_dst = const_cast<void**>(s_src + p.n_src);
+  for (int q = threadIdx.x; q < p.n_src; q += blockDim.x) s_src[q] = p.src[q];
+  for (int q = threadIdx.x; q < p.n_dst; q += blockDim.x) s_dst[q] = p.dst[q];
+  if (threadIdx.x == 0) {
+    const Bars B = Bars::at<D>(sm);
+    const unsigned warps = kRingCompute / 32;
+    for (int s = 0; s < kNS; ++s) {
+      mbar_init(B.rep_full + s, 1);       // the loader's expect_tx + the bytes
+      mbar_init(B.rep_empty + s, warps);  // every compute warp
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(B.acc_full + a, 1);
+      mbar_init(B.acc_empty + a, warps);
+    }
+    for (int o = 0; o < kNO; ++o) {
+      mbar_init(B.out_full + o, warps);
+      mbar_init(B.out_empty + o, 1);  // the storer
+    }
+    for (int s = 0; s < kNR; ++s) {
+      mbar_init(B.rel_full + s, 1);
+      mbar_init(B.rel_empty + s, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+  }
+  Lane ln;
+  ln.c = (int)blockIdx.x;
+  ln.steps = ln.c < p.T ? (p.T - ln.c + p.L - 1) / p.L : 0;
+  ln.base = p.round * (uint64_t)ln.steps;
+  if (threadIdx.x < 2) reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL)[threadIdx.x] = ln.base;
+  __syncthreads();
+  const bool last = p.g == p.G - 1;
+  const int w = (int)(threadIdx.x / 32);
+  const bool lead = (threadIdx.x & 31) == 0;
+  if (w < kWLoad) {
+    const long long t_start = clock64();
+    if (last)
+      ring_compute<D, true>(p, ln, sm, s_src, s_dst);
+    else
+      ring_compute<D, false>(p, ln, sm, s_src, s_dst);
+    if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 7] = (unsigned long long)(clock64() - t_start);
+  } else if (w == kWLoad) {
+    if (lead) ring_loader<D>(p, ln, sm, s_src);
+  } else if (w == kWStore) {
+    if (lead) {
+      if (last)
+        ring_storer<D, true>(p, ln, sm, s_dst);
+      else
+        ring_storer<D, false>(p, ln, sm, s_dst);
+    }
+  } else if (w == kWPub) {
+    if (lead && ln.steps > 0) ring_publisher<D>(p, ln, sm);
+  } else if (!last) {
+    if (w == kWRLoad) {
+      if (lead) ring_relay_loader<D>(p, ln, sm);
+    } else {
+      ring_relay_storer<D>(p, ln, sm, s_dst);
+    }
+  }
+}
+
+template <class D>
+static size_t ring_smem_bytes(int n_src, int n_dst) {
+  return (size_t)RingGeom<D>::OFF_PTR + sizeof(void*) * (size_t)(n_src + n_dst);
+}
+
+template <class D>
+static void ring_slot_bytes(int64_t* acc_b, int64_t* fin_b) {
+  *acc_b = RingGeom<D>::ACC_BYTES;
+  *fin_b = RingGeom<D>::FIN_BYTES;
+}
+
+constexpr int kRingMaxPtrs = 128;  // replica pointers a CTA stages (n_src + n_dst)
+
+template <class D>
+static int ring_lanes_for() {
+  int per_sm = 0;
+  const size_t smem = ring_smem_bytes<D>(kRingMaxPtrs, 0);
+  cudaFuncSetAttribute(k_ring<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring<D>, kRingThreads, smem) != cudaSuccess)
+    return 0;
+  return per_sm * sm_count();
+}
+
+template <class D>
+static int ring_launch(RingParams p, cudaStream_t st) {
+  if (p.n_src + p.n_dst > kRingMaxPtrs) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many local replicas");
+  p.T = (p.P + RingGeom<D>::TE - 1) / RingGeom<D>::TE;
+  const size_t smem = ring_smem_bytes<D>(p.n_src, p.n_dst);
+  cudaFuncSetAttribute(k_ring<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring<D>, kRingThreads, smem);
+  if ((int64_t)per_sm * sm_count() < p.L)
+    return fail(BFLY_E_UNSUPPORTED, "fused ring: " + std::to_string(p.L) + " CTAs cannot be co-resident");
+  void* args[] = {&p};
+  cudaError_t e =
+      cudaLaunchCooperativeKernel((const void*)k_ring<D>, dim3((unsigned)p.L), dim3(kRingThreads), args, smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_ring cooperative launch");
+  return BFLY_OK;
+}
+
+int ring_round_setup(const bfly_merge_args_t* a, void* stream);  // bfly_merge.cu
+
+static unsigned long long* g_prof = nullptr;  // diagnostics buffer (BFLY_RING_PROFILE)
+static int g_prof_n = 0;
+
+}  // namespace bfly
+
+using namespace bfly;
+
+extern "C" {
+
+int bfly_ring_fused_profile(unsigned long long* host_out, int32_t n) {
+  if (!g_prof) return fail(BFLY_E_INVALID_ARG, "no profile (set BFLY_RING_PROFILE)");
+  const int m = n < g_prof_n ? n : g_prof_n;
+  cudaError_t e = cudaMemcpy(host_out, g_prof, sizeof(unsigned long long) * (size_t)m, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? m : cuda_fail(e, "profile copy");
+}
+
+int32_t bfly_ring_fused_lanes(int32_t dtype) {
+  switch (dtype) {
+    case BFLY_F32: return ring_lanes_for<DF32>();
+    case BFLY_BF16: return ring_lanes_for<DBF16>();
+    case BFLY_F64WIRE: return ring_lanes_for<DF64W>();
+    default: return 0;
+  }
+}
+
+int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* off_fin, int64_t* off_flags,
+                           int64_t* total) {
+  if (lanes < 1 || nb < 2 || !off_fin || !off_flags || !total) return fail(BFLY_E_INVALID_ARG, "bad ring layout");
+  int64_t acc_b = 0, fin_b = 0;
+  switch (dtype) {
+    case BFLY_F32: ring_slot_bytes<DF32>(&acc_b, &fin_b); break;
+    case BFLY_BF16: ring_slot_bytes<DBF16>(&acc_b, &fin_b); break;
+    case BFLY_F64WIRE: ring_slot_bytes<DF64W>(&acc_b, &fin_b); break;
+    default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  }
+  auto align = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+  *off_fin = align((int64_t)lanes * nb * acc_b);
+  *off_flags = align(*off_fin + (int64_t)lanes * nb * fin_b);
+  *total = align(*off_flags + (int64_t)(kFAbort + 1) * lanes * 8);
+  return BFLY_OK;
+}
+
+int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
+  if (!d || d->world < 2 || d->rank < 0 || d->rank >= d->world || d->lanes < 1 || d->nb < 2 || !d->peer_base ||
+      d->payload_len < 1 || d->n_src < 0 || d->n_dst < 0 || (d->n_src > 0 && !d->d_src) ||
+      (d->n_dst > 0 && !d->d_dst))
+    return fail(BFLY_E_INVALID_ARG, "bad fused ring descriptor");
+  const int g = d->rank, G = d->world, Z = G - 1;
+  if (g == Z && d->n_div < 1) return fail(BFLY_E_INVALID_ARG, "fused ring: no alive miner");
+  int64_t off_fin = 0, off_flags = 0, total = 0;
+  int rc = bfly_ring_fused_layout(d->lanes, d->nb, d->dtype, &off_fin, &off_flags, &total);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (g == Z && d->merge_args) {
+    rc = ring_round_setup(d->merge_args, stream);
+    if (rc) return rc;
+  }
+  RingParams p{};
+  p.g = g;
+  p.G = G;
+  p.L = d->lanes;
+  p.NB = d->nb;
+  p.P = d->payload_len;
+  p.round = d->round_index;
+  auto region = [&](int r) { return reinterpret_cast<unsigned char*>((uintptr_t)d->peer_base[r]); };
+  p.my = region(g);
+  p.nxt = g == Z ? region(0) : region(g + 1);
+  p.prv = g > 0 ? region(g - 1) : nullptr;
+  p.fsucc = (g < Z && g + 1 < Z) ? region(g + 1) : nullptr;
+  p.fpred = g == 0 ? region(Z) : region(g - 1);
+  p.off_fin = off_fin;
+  p.off_flags = off_flags;
+  p.src = d->d_src;
+  p.n_src = d->n_src;
+  p.dst = d->d_dst;
+  p.n_dst = d->n_dst;
+  p.n_div = d->n_div;
+  p.merged = g == Z ? d->d_merged : nullptr;
+  p.pub_every = 1;
+  p.pub_relaxed = 0;
+  if (const char* e = getenv("BFLY_RING_PUB_EVERY")) p.pub_every = atoi(e) > 0 ? atoi(e) : 1;
+  if (const char* e = getenv("BFLY_RING_PUB_RELAXED")) p.pub_relaxed = atoi(e) != 0;
+  p.lag = 1;
+  if (const char* e = getenv("BFLY_RING_LAG")) p.lag = atoi(e) < 1 ? 1 : (atoi(e) > kMaxLag ? kMaxLag : atoi(e));
+  if (p.pub_every >= d->nb - p.lag) return fail(BFLY_E_INVALID_ARG, "fused ring: publication interval too long for nb");
+  if (getenv("BFLY_RING_PROFILE")) {
+    if (!g_prof || g_prof_n < p.L * kProfSlots) {
+      if (g_prof) cudaFree(g_prof);
+      g_prof_n = p.L * kProfSlots;
+      if (cudaMalloc(&g_prof, sizeof(unsigned long long) * g_prof_n) != cudaSuccess) return fail(BFLY_E_CUDA, "prof");
+    }
+    cudaMemsetAsync(g_prof, 0, sizeof(unsigned long long) * g_prof_n, st);
+    p.prof = g_prof;
+  }
+  switch (d->dtype) {
+    case BFLY_F32: return ring_launch<DF32>(p, st);
+    case BFLY_BF16: return ring_launch<DBF16>(p, st);
+    case BFLY_F64WIRE: return ring_launch<DF64W>(p, st);
+    default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  }
+}
+
+}  // extern "C"

@@ -271,6 +271,8 @@ class ButterflyMerge:
             self._args.d_host_copies = host_copies.data_ptr()
         if phase == L.PHASE_FINISH and not self.needs_finish():
             return self  # every shard is fast: nothing to compare, adopt or fall back
+        if phase == L.PHASE_ALL and not self.needs_finish():
+            phase = L.PHASE_REDUCE  # every shard fast: k_classify already wrote its results
         self._args.phase = phase
         self._args.d_acc_in = None
         self._args.elem_begin = self._args.elem_end = 0
@@ -294,7 +296,7 @@ class ButterflyMerge:
         side = torch.cuda.Stream(device=self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
         with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
-            self._args.phase = L.PHASE_ALL
+            self._args.phase = L.PHASE_ALL if self.needs_finish() else L.PHASE_REDUCE
             self._call(None)
         torch.cuda.current_stream(self.dev).wait_stream(side)
         self._graph = g
@@ -364,7 +366,8 @@ class ButterflyMerge:
         return self
 
     def needs_finish(self) -> bool:
-        return self.special or self.maybe_lost
+        # r = 3: a pair's entry is the minimum over the shards it shares (k_entries3)
+        return self.special or self.maybe_lost or self.r > 2
 
     # number of our kernels one run() launches (reported by bench.py as gpu_launches)
     def launches_per_run(self) -> int:

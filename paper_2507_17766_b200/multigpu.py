@@ -49,6 +49,7 @@ from .device import ButterflyMerge, _DTYPES, _stream_handle
 
 NB = int(os.environ.get("BFLY_RING_NB", "3"))  # inbox slots per ring
 WINDOW = 4  # chunks the host may run ahead of the GPUs per stream
+FUSED_NB = int(os.environ.get("BFLY_FUSED_NB", "10"))  # slots per lane of the persistent ring
 
 
 def special_ranges(assign: np.ndarray, P: int, failures: set, corrupted: set) -> list:
@@ -276,7 +277,19 @@ class ShardedButterflyMerge:
         self._src_table = self._table(self.local_alive) if self.local_alive else None
         self._local_table = self._table(self.local)
         self._fb_table = self._table([self._fb_buf]) if self._fb_buf is not None else None
-        if G > 1:
+        # every shard fast (no corrupted survivor, fewer than r failures, shards of >= 2
+        # elements, 16-byte aligned replicas on every rank for the TMA bulk copies): the
+        # whole round runs as one persistent kernel per GPU
+        self.fused = bool(G > 1 and not corrupted and len(failures) < self.plan_r
+                          and self.P // plan.n_shards >= 2 and os.environ.get("BFLY_RING_FUSED", "1") != "0")
+        if self.fused:
+            ok = torch.tensor([int(all(t.data_ptr() % 16 == 0 for t in self.local))], device=self.dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            self.fused = bool(ok.item())
+        if self.fused:
+            self._late_mode = False  # (r = 3) every shard's FINISH runs after the kernel
+            self._setup_fused()
+        elif G > 1:
             self._setup_ring()
 
     # -- late shards -------------------------------------------------------------
@@ -331,13 +344,13 @@ class ShardedButterflyMerge:
         self._tables.append(t)
         return t
 
-    def _setup_ring(self):
+    def _open_region(self, total: int):
+        """Allocate this rank's IPC region (zeroed) and map every other rank's."""
         lib = L.lib()
-        self.layout = lay = _Region(self.chunk, self.esize)
         base = ctypes.c_void_p()
         handle = (ctypes.c_uint8 * 64)()
         with torch.cuda.device(self.dev):
-            L.check(lib.bfly_ipc_alloc(lay.total, ctypes.byref(base), handle))
+            L.check(lib.bfly_ipc_alloc(total, ctypes.byref(base), handle))
         self._base = base.value
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(handle))
@@ -351,6 +364,34 @@ class ShardedButterflyMerge:
                 L.check(lib.bfly_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p)))
                 self._peer[r] = p.value
         dist.barrier()
+        self._peer_arr = (ctypes.c_uint64 * self.world)(*[self._peer[r] for r in range(self.world)])
+
+    def _setup_fused(self):
+        """The persistent single-kernel ring (bfly_ring_fused, csrc/bfly_ring.cu)."""
+        lib = L.lib()
+        lanes = torch.tensor([int(lib.bfly_ring_fused_lanes(self.dtype))], dtype=torch.int64, device=self.dev)
+        dist.all_reduce(lanes, op=dist.ReduceOp.MIN)  # every rank must deal tiles to the same lanes
+        self.lanes = int(lanes.item())
+        if self.lanes < 1:
+            raise RuntimeError("fused ring: no co-resident lanes on this device")
+        o = [ctypes.c_int64() for _ in range(3)]
+        L.check(lib.bfly_ring_fused_layout(self.lanes, FUSED_NB, self.dtype, *[ctypes.byref(x) for x in o]))
+        self._open_region(o[2].value)
+        d = L.RingFusedDesc()
+        d.rank, d.world, d.lanes, d.nb, d.dtype = self.rank, self.world, self.lanes, FUSED_NB, self.dtype
+        d.n_src, d.n_dst, d.n_div = len(self.local_alive), len(self.local), len(self.alive)
+        d.payload_len = self.P
+        d.peer_base = ctypes.cast(self._peer_arr, ctypes.c_void_p)
+        d.d_src = self._src_table.data_ptr() if self._src_table is not None else None
+        d.d_dst = self._local_table.data_ptr()
+        if self.is_last:
+            d.d_merged = self.job.merged.data_ptr() if self.job.merged is not None else None
+            d.merge_args = ctypes.pointer(self.job._args)
+        self._fdesc = d
+
+    def _setup_ring(self):
+        self.layout = lay = _Region(self.chunk, self.esize)
+        self._open_region(lay.total)
         self._relay = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("BFLY_RELAY_PRIORITY", "0")))
         # last rank: per-chunk late shards, high priority so a chunk's decision does not queue
         # behind the next chunk's reduce CTAs (the relay waits for it)
@@ -379,7 +420,6 @@ class ShardedButterflyMerge:
         d.payload_len, d.chunk, d.dtype, d.esize = self.P, self.chunk, self.dtype, self.esize
         self._edge_arr = (ctypes.c_int64 * (self.K + 1))(*self.edges)
         d.chunk_edges = ctypes.cast(self._edge_arr, ctypes.c_void_p)
-        self._peer_arr = (ctypes.c_uint64 * self.world)(*[self._peer[r] for r in range(self.world)])
         d.peer_base = ctypes.cast(self._peer_arr, ctypes.c_void_p)
         d.off_acc, d.off_fin, d.off_flags = lay.acc, lay.fin, lay.flags
         d.d_src_table = self._src_table.data_ptr() if self._src_table is not None else None
@@ -518,6 +558,10 @@ class ShardedButterflyMerge:
             for k in range(self.K):
                 b, e = self._bounds(k)
                 self.job.reduce_range(b, e)
+        elif self.fused:
+            self._fdesc.round_index = self._round
+            with torch.cuda.device(self.dev):
+                L.check(L.lib().bfly_ring_fused(ctypes.byref(self._fdesc), _stream_handle()))
         else:
             # fallback values (the lowest alive miner's replica) for the late shards: packed
             # before the relay overwrites that replica, sent while the ring runs
@@ -613,6 +657,8 @@ class ShardedButterflyMerge:
         fin = 3 + (1 if self.plan_r > 2 else 0)  # k_stats, k_decide, [k_entries3], k_apply
         if self.world == 1:
             return 2 + self.K + (fin if self.job.needs_finish() else 0)
+        if self.fused:  # k_ring (+ k_fill_nan, k_classify [, FINISH for r = 3] on the last rank)
+            return 3 + (fin if self.job.needs_finish() else 0) if self.is_last else 1
         if self.is_last:
             n = 2 + self.K  # k_fill_nan + k_classify, then one k_reduce per chunk
             if self._late_mode:

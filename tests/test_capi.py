@@ -46,6 +46,10 @@ def test_struct_layout_matches_header(tmp_path):
     body = "\n".join(f'  printf("{f} %zu\\n", offsetof(bfly_merge_args_t, {f}));' for f in fields)
     body += "\n" + "\n".join(f'  printf("ring.{f} %zu\\n", offsetof(bfly_ring_desc_t, {f}));' for f in rfields)
     body += '\n  printf("rsize %zu\\n", sizeof(bfly_ring_desc_t));'
+    ffields = [f for f, _ in _lib.RingFusedDesc._fields_]
+    body += "\n" + "\n".join(f'  printf("fused.{f} %zu\\n", offsetof(bfly_ring_fused_desc_t, {f}));'
+                             for f in ffields)
+    body += '\n  printf("fsize %zu\\n", sizeof(bfly_ring_fused_desc_t));'
     src.write_text(f"""#include <stdio.h>
 #include <stddef.h>
 #include "bfly.h"
@@ -66,6 +70,29 @@ int main(void) {{
     assert int(out["rsize"]) == ctypes.sizeof(_lib.RingDesc)
     for f in rfields:
         assert int(out["ring." + f]) == getattr(_lib.RingDesc, f).offset, f
+    assert int(out["fsize"]) == ctypes.sizeof(_lib.RingFusedDesc)
+    for f in ffields:
+        assert int(out["fused." + f]) == getattr(_lib.RingFusedDesc, f).offset, f
+
+
+def test_fused_ring_layout():
+    """Region of the persistent ring (bfly_ring_fused_layout): per lane NB running-sum
+    slots (one tile at accumulator width), NB final-vector slots (one tile at replica
+    width), then the five 64-bit flag arrays; every part 256-byte aligned."""
+    from paper_2507_17766_b200 import _lib
+
+    lib = _lib.lib()
+    # a tile is 4 KB of every replica: 1024 fp32 / 2048 bf16 / 512 fp64 elements
+    for dtype, acc_b, fin_b in ((_lib.F32, 1024 * 8, 4096), (_lib.BF16, 2048 * 4, 4096),
+                                (_lib.F64WIRE, 512 * 8, 4096)):
+        o = [ctypes.c_int64() for _ in range(3)]
+        _lib.check(lib.bfly_ring_fused_layout(148, 4, dtype, *[ctypes.byref(x) for x in o]))
+        off_fin, off_flags, total = (x.value for x in o)
+        assert off_fin == 148 * 4 * acc_b
+        assert off_flags == off_fin + 148 * 4 * fin_b
+        assert total == (off_flags + 5 * 148 * 8 + 255) // 256 * 256
+    with pytest.raises(Exception):
+        _lib.check(lib.bfly_ring_fused_layout(148, 1, _lib.F32, *[ctypes.byref(ctypes.c_int64()) for _ in range(3)]))
 
 
 @pytest.mark.parametrize("seed", [0, 1, 24, 2**63 - 1, 2**64 + 5, -7, 10**30])

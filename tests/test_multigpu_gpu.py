@@ -52,20 +52,27 @@ corr = {m: Corruption(kinds[s[0]], s[1], (s[2], s[3]) if len(s) > 2 else (0, 0))
 job = ShardedButterflyMerge(local, plan, failures=fails, corruptions=corr,
                             fallback=None if fb is None else torch.from_numpy(fb).to(dev),
                             chunk=case["chunk"], want_merged=True)
-job.run()
-torch.cuda.synchronize()
-assert_same_floats(job.merged.cpu().numpy(), want["merged"])
-if not bf16:
-    for t in local:
-        assert_same_floats(t.cpu().numpy(), want["merged"].astype(np.float32))
-else:
-    bits = np.array([orc.lib().orc_f32_to_bf16(float(v)) for v in want["merged"][:4099].astype(np.float32)],
-                    dtype=np.uint16)
-    for t in local:
-        assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16)[:4099], bits)
-assert np.array_equal(job.status.cpu().numpy(), want["status"])
-assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
-assert_entries_close(job.entries.cpu().numpy(), want["entries"])
+if "fused" in case:
+    assert job.fused == case["fused"], (job.fused, case["fused"])
+orig = [t.clone() for t in local]
+for rnd in range(case.get("rounds", 1)):
+    if rnd:  # refill the replicas in place: the next round reuses slots and flags
+        for t, o in zip(local, orig):
+            t.copy_(o)
+    job.run()
+    torch.cuda.synchronize()
+    assert_same_floats(job.merged.cpu().numpy(), want["merged"])
+    if not bf16:
+        for t in local:
+            assert_same_floats(t.cpu().numpy(), want["merged"].astype(np.float32))
+    else:
+        bits = np.array([orc.lib().orc_f32_to_bf16(float(v)) for v in want["merged"][:4099].astype(np.float32)],
+                        dtype=np.uint16)
+        for t in local:
+            assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16)[:4099], bits)
+    assert np.array_equal(job.status.cpu().numpy(), want["status"])
+    assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
+    assert_entries_close(job.entries.cpu().numpy(), want["entries"])
 dist.barrier()
 dist.destroy_process_group()
 print("rank", rank, "ok")
@@ -88,6 +95,22 @@ CASES = [
      "fallback": False, "chunk": 1 << 20},
     {"counts": [2, 2, 2, 2], "P": 6_000_007, "seed": 13, "failures": [], "corr": {"3": [3, 1.0, 2, 3]},
      "fallback": False, "chunk": 1 << 20},
+    # persistent single-kernel ring (bfly_ring_fused): every shard fast; several rounds
+    # reuse the slot rings and the monotonic flags; partial last tiles; uneven lanes
+    {"counts": [4, 4], "P": 3_000_017, "seed": 21, "failures": [], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "rounds": 8},
+    {"counts": [3, 5], "P": 2_345_679, "seed": 22, "failures": [6], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "rounds": 2},
+    {"counts": [2, 3, 2], "P": 1_234_567, "seed": 23, "failures": [0], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "rounds": 2},
+    {"counts": [2, 2, 2, 2], "P": 4_000_037, "seed": 24, "failures": [], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "rounds": 8},
+    {"counts": [3, 3], "P": 1_500_007, "seed": 25, "failures": [1], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "bf16": True, "fused": True, "rounds": 2},
+    {"counts": [2, 3], "P": 10 * 3000 + 7, "seed": 26, "failures": [3, 4], "corr": {}, "fallback": False,
+     "chunk": 8192, "r": 3, "fused": True, "rounds": 2},
+    {"counts": [1, 2], "P": 9_001, "seed": 27, "failures": [], "corr": {}, "fallback": False,
+     "chunk": 8192, "fused": True, "rounds": 4},
 ]
 
 

@@ -1,0 +1,79 @@
+"""Diagnostics of the persistent multi-GPU ring (k_ring, csrc/bfly_ring.cu).
+
+    BFLY_RING_PROFILE=1 torchrun --nproc-per-node G tools/ring_fused_probe.py [P] [miners_per_gpu]
+
+Times a few rounds with CUDA events (max over ranks) and prints, per rank, the
+share of the kernel's cycles each role spent waiting (mean over CTAs):
+loader (replica stage free, upstream ready flag, acc stage free), compute (acc
+tile, out stage free, replica stage full), storer (out tile, downstream free
+flag, stage read-out, landing), relay loader (ready flag, stage free), relay
+storer (stage full, downstream free flag, read-out, landing).
+"""
+
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+
+from paper_2507_17766_b200 import _lib as L  # noqa: E402
+from paper_2507_17766_b200.device import DevicePlan  # noqa: E402
+from paper_2507_17766_b200.multigpu import ShardedButterflyMerge  # noqa: E402
+
+NAMES = ["ld.rep_empty", "ld.ready_flag", "ld.acc_empty", "-", "cmp.acc_full", "cmp.out_empty", "cmp.rep_full",
+         "total_cycles", "st.out_full", "st.free_flag", "st.read", "st.landed", "rl.ready_flag", "rl.rel_empty", "-",
+         "-", "rs.rel_full", "rs.free_flag", "rs.read", "rs.landed"]
+
+
+def main():
+    P = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000_000
+    n_local = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", rank)))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    g = torch.Generator(device=dev)
+    reps = []
+    for i in range(n_local):
+        g.manual_seed(rank * n_local + i)
+        reps.append(torch.empty(P, dtype=torch.float32, device=dev).uniform_(-1, 1, generator=g))
+    plan = DevicePlan(n_local * world, P, 0, device=dev)
+    job = ShardedButterflyMerge(reps, plan)
+    assert job.fused
+    for _ in range(2):
+        job.run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    rounds = 3
+    ev[0].record()
+    for _ in range(rounds):
+        job.run()
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([ev[0].elapsed_time(ev[1]) / rounds], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    out = {"rank": rank, "round_ms": round(float(ms.item()), 3), "lanes": job.lanes}
+    if os.environ.get("BFLY_RING_PROFILE"):
+        n = job.lanes * 20
+        buf = (ctypes.c_ulonglong * n)()
+        L.lib().bfly_ring_fused_profile(buf, n)
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(job.lanes, 20).astype(np.float64)
+        tot = a[:, 7].mean()
+        out["kernel_ms_at_1.9GHz"] = round(tot / 1.9e6, 3)
+        out["wait_share"] = {NAMES[k]: round(a[:, k].mean() / tot, 3) for k in range(20) if NAMES[k] not in ("-", "total_cycles")}
+    for r in range(world):
+        if r == rank:
+            print(json.dumps(out), flush=True)
+        dist.barrier()
+    job.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
