@@ -368,15 +368,20 @@ def run_multi(cfg, args, rank, world):
             "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
             "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "miners_per_gpu": n_local,
                        "params": P, "replica_dtype": dtype, "redundancy": r, "deceptive": len(bad),
-                       "parallelism": f"miners in contiguous blocks over {world} GPUs; fp64 running sums chained "
-                                      f"rank to rank (TMA bulk stores into IPC-mapped peer inboxes over NVLink, "
-                                      f"up to {args.chunk}-element chunks), final vector relayed round the ring",
+                       "parallelism": (f"miners in contiguous blocks over {world} GPUs; one persistent kernel per "
+                                       f"GPU (k_ring): fp64 running sums chained rank to rank tile by tile through "
+                                       f"TMA bulk stores into IPC-mapped peer inboxes over NVLink, final values "
+                                       f"relayed round the ring" if job.fused else
+                                       f"miners in contiguous blocks over {world} GPUs; chunked ring: fp64 running "
+                                       f"sums chained rank to rank (TMA bulk stores into IPC-mapped peer inboxes, "
+                                       f"up to {args.chunk}-element chunks), final vector relayed round the ring"),
                        "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
             "params_merged_per_s": P / t_step,
             "roofline": {"bound": "hbm" if per_gpu_hbm / hbm_peak > float(nvl.item()) / nvl_peak else "nvlink",
                          "achieved": per_gpu_hbm / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
                          "frac": t_roof / t_step, "traffic": None,
-                         "kernel": "whole round per GPU (chain / reduce / fan-out kernels + NVLink ring)",
+                         "kernel": ("whole round per GPU (k_ring: one persistent kernel)" if job.fused else
+                                    "whole round per GPU (chain / reduce / fan-out kernels + NVLink ring)"),
                          "t_roof_ms": t_roof * 1e3, "hbm_bytes_per_gpu": per_gpu_hbm,
                          "nvlink_bytes_in_per_gpu": float(nvl.item()),
                          "peaks": {"hbm_GBps": hbm_peak, "nvlink_GBps_per_direction": nvl_peak,
