@@ -279,7 +279,7 @@ int32_t bfly_ring_fused_lanes(int32_t dtype);
 int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* off_fin, int64_t* off_flags,
                            int64_t* total);
 int bfly_ring_fused(const bfly_ring_fused_desc_t* desc, void* stream);
-/* Diagnostics: with BFLY_RING_PROFILE set, per CTA 20 counters of the last k_ring
+/* Diagnostics: with BFLY_RING_PROFILE set, per CTA 24 counters of the last k_ring
  * launch (cycles spent in each wait, per role); copies n of them, returns the count. */
 int bfly_ring_fused_profile(unsigned long long* host_out, int32_t n);
 

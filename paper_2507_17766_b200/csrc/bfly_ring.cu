@@ -146,7 +146,7 @@ __device__ __forceinline__ uint64_t mail_read(const uint64_t* box) {
 }
 
 // Wait-cycle counters of one role (diagnostics only; p.prof == null in production).
-constexpr int kProfSlots = 20;
+constexpr int kProfSlots = 24;  // 5 roles x 4 counters, then CTA start / end (globaltimer)
 struct Prof {
   unsigned long long* out;
   unsigned long long acc[4] = {0, 0, 0, 0};
@@ -701,13 +701,17 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
   const bool last = p.g == p.G - 1;
   const int w = (int)(threadIdx.x / 32);
   const bool lead = (threadIdx.x & 31) == 0;
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 20] = global_ns();
   if (w < kWLoad) {
     const long long t_start = clock64();
     if (last)
       ring_compute<D, true>(p, ln, sm, s_src, s_dst);
     else
       ring_compute<D, false>(p, ln, sm, s_src, s_dst);
-    if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 7] = (unsigned long long)(clock64() - t_start);
+    if (p.prof && threadIdx.x == 0) {
+      p.prof[blockIdx.x * kProfSlots + 7] = (unsigned long long)(clock64() - t_start);
+      p.prof[blockIdx.x * kProfSlots + 21] = global_ns();
+    }
   } else if (w == kWLoad) {
     if (lead) ring_loader<D>(p, ln, sm, s_src);
   } else if (w == kWStore) {

@@ -27,7 +27,7 @@ from paper_2507_17766_b200.multigpu import ShardedButterflyMerge  # noqa: E402
 
 NAMES = ["ld.rep_empty", "ld.ready_flag", "ld.acc_empty", "-", "cmp.acc_full", "cmp.out_empty", "cmp.rep_full",
          "total_cycles", "st.out_full", "st.free_flag", "st.read", "st.landed", "rl.ready_flag", "rl.rel_empty", "-",
-         "-", "rs.rel_full", "rs.free_flag", "rs.read", "rs.landed"]
+         "-", "rs.rel_full", "rs.free_flag", "rs.read", "rs.landed", "t_start", "t_end", "-", "-"]
 
 
 def main():
@@ -60,13 +60,19 @@ def main():
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     out = {"rank": rank, "round_ms": round(float(ms.item()), 3), "lanes": job.lanes}
     if os.environ.get("BFLY_RING_PROFILE"):
-        n = job.lanes * 20
+        n = job.lanes * 24
         buf = (ctypes.c_ulonglong * n)()
         L.lib().bfly_ring_fused_profile(buf, n)
-        a = np.frombuffer(buf, dtype=np.uint64).reshape(job.lanes, 20).astype(np.float64)
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(job.lanes, 24).astype(np.float64)
         tot = a[:, 7].mean()
         out["kernel_ms_at_1.9GHz"] = round(tot / 1.9e6, 3)
-        out["wait_share"] = {NAMES[k]: round(a[:, k].mean() / tot, 3) for k in range(20) if NAMES[k] not in ("-", "total_cycles")}
+        out["wait_share"] = {NAMES[k]: round(a[:, k].mean() / tot, 3) for k in range(24)
+                             if NAMES[k] not in ("-", "total_cycles", "t_start", "t_end")}
+        ts, te = a[:, 20], a[:, 21]
+        out["cta_ms"] = {"start_skew": round((ts.max() - ts.min()) / 1e6, 3),
+                         "span": round((te.max() - ts.min()) / 1e6, 3),
+                         "mean_dur": round((te - ts).mean() / 1e6, 3), "max_dur": round((te - ts).max() / 1e6, 3),
+                         "end_skew": round((te.max() - te.min()) / 1e6, 3)}
     for r in range(world):
         if r == rank:
             print(json.dumps(out), flush=True)
