@@ -1096,7 +1096,8 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   if (!a->d_assign || !a->d_failed || !a->d_corr || !a->d_status || !a->d_entries || !a->d_flagged)
     return fail(BFLY_E_INVALID_ARG, "missing required device array");
   if (a->n_alive > 0 && !a->d_src) return fail(BFLY_E_INVALID_ARG, "missing replicas");
-  if (a->n_alive == 0 && a->n_div > 0 && !a->d_acc_in) return fail(BFLY_E_INVALID_ARG, "n_div without replicas");
+  if (a->n_alive == 0 && a->n_div > 0 && !a->d_acc_in && a->phase != BFLY_PHASE_FINISH)
+    return fail(BFLY_E_INVALID_ARG, "n_div without replicas");  // (FINISH reads no replica sums)
   if (a->n_dst > 0 && !a->d_dst) return fail(BFLY_E_INVALID_ARG, "missing scatter-back targets");
   if (!a->d_merged && !a->d_ws) return fail(BFLY_E_INVALID_ARG, "need d_merged or d_ws");
   ScratchLayout L;
@@ -1162,7 +1163,9 @@ namespace bfly {
 // bfly_ring.cu, reduces inside its own kernel): entries NaN, flags cleared, classify.
 int ring_round_setup(const bfly_merge_args_t* a, void* stream) {
   Params p;
-  int rc = build_params(a, p);
+  bfly_merge_args_t b = *a;
+  b.phase = BFLY_PHASE_FINISH;  // no reduce here: the last rank may hold no alive replica
+  int rc = build_params(&b, p);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nn = (int64_t)p.n * p.n;
