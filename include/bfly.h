@@ -254,10 +254,11 @@ int bfly_ring_ops(int32_t rank, int32_t world, int32_t k_chunks, int32_t nb, uin
  * the neighbouring rank through a slot ring in the neighbour's IPC region, with
  * 64-bit monotonic flags stored / polled by the SMs (st.release.sys / ld.acquire.sys)
  * — the transfer of tile i overlaps the reduction of tile i+1.  Same values as
- * bfly_ring_round (running fp64 sums in ascending miner order); only for rounds in
- * which every shard is fast (no corrupted survivor, fewer than r failures) and every
- * shard has >= 2 elements.  Replaces, for those rounds, the chunked ring of
- * bfly_ring_round (which stays for rounds with corrupted / lost shards).          */
+ * bfly_ring_round (running fp64 sums in ascending miner order); every shard must have
+ * >= 2 elements and the replicas must be 16-byte aligned.  Rounds with corrupted / lost shards run it too (desc.special):
+ * the relayed tiles then carry k_classify's predicted outcome and FINISH on the last rank
+ * decides the special shards after the kernel (the caller re-broadcasts the few whose
+ * decision differs from the prediction).                                          */
 typedef struct bfly_ring_fused_desc {
   int32_t rank, world;           /* this process's rank and the ring size            */
   int32_t lanes, nb;             /* lanes (equal on every rank), slots per lane      */
@@ -271,6 +272,10 @@ typedef struct bfly_ring_fused_desc {
   double* d_merged;              /* last rank, optional: fp64 merged vector            */
   const bfly_merge_args_t* merge_args; /* last rank, optional: the round's per-shard
                                     setup (status / entries / flags) runs first       */
+  int32_t special;               /* last rank: some shard may be corrupted or lost — its
+                                    tiles get k_classify's predicted outcome (and the means
+                                    go to the workspace); FINISH runs after the kernel  */
+  int32_t pad;
 } bfly_ring_fused_desc_t;
 /* Lanes this device runs (all CTAs co-resident: cooperative launch). */
 int32_t bfly_ring_fused_lanes(int32_t dtype);

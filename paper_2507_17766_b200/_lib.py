@@ -159,6 +159,8 @@ class RingFusedDesc(ctypes.Structure):
         ("d_dst", ctypes.c_void_p),
         ("d_merged", ctypes.c_void_p),
         ("merge_args", ctypes.POINTER(MergeArgs)),
+        ("special", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
     ]
 
 

@@ -77,4 +77,17 @@ struct ScratchLayout {
   }
 };
 
+// What the persistent ring's last rank needs to write predicted outcomes for special /
+// lost shards (filled by ring_round_setup from the merge arguments).
+struct RingSpecial {
+  const uint8_t* cls = nullptr;   // ShardClass per shard
+  const uint8_t* pred = nullptr;  // ShardPred per shard
+  Bounds bnd{};
+  double* ws = nullptr;           // means of special shards (may alias merged)
+  const double* fallback = nullptr;
+  const void* fb_src = nullptr;   // replica supplying fallback values
+  bool merged_apart = false;      // merged is not the workspace
+};
+int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out);
+
 }  // namespace bfly

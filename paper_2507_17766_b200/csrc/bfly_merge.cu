@@ -1161,12 +1161,25 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
 namespace bfly {
 // Per-round setup of the shard results without a reduce (the fused multi-GPU ring,
 // bfly_ring.cu, reduces inside its own kernel): entries NaN, flags cleared, classify.
-int ring_round_setup(const bfly_merge_args_t* a, void* stream) {
+int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out) {
   Params p;
   bfly_merge_args_t b = *a;
   b.phase = BFLY_PHASE_FINISH;  // no reduce here: the last rank may hold no alive replica
   int rc = build_params(&b, p);
   if (rc) return rc;
+  // the kernel reduces every element (from the chained sums), so k_classify predicts the
+  // outcomes as for a chained reduce even when this rank holds no alive replica
+  static const double kChained = 0.0;
+  p.acc_in = &kChained;
+  if (out) {
+    out->cls = p.cls;
+    out->pred = p.pred;
+    out->bnd = p.bnd;
+    out->ws = p.ws;
+    out->fallback = p.fallback;
+    out->fb_src = p.fb_src;  // the multi-GPU last rank always names it (the lowest alive miner's replica)
+    out->merged_apart = p.merged && p.merged != p.ws;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nn = (int64_t)p.n * p.n;
   k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);

@@ -80,6 +80,8 @@ struct RingParams {
   int pub_every;             // publish every pub_every-th step (each publication covers the ones before)
   int pub_relaxed;           // 1: after wait_group the flag is a relaxed store (no MEMBAR.SYS)
   int lag;                   // publication lag in steps (1..kMaxLag)
+  int special;               // last rank: some shard is corrupted or lost (see RingSpecial)
+  RingSpecial sp;
 };
 
 template <class D>
@@ -312,6 +314,49 @@ __device__ __forceinline__ uint4 pack16(const typename D::Acc* x) {
   return make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
 }
 
+// 16 bytes from KE doubles, rounded as the replicas store them
+template <class D>
+__device__ __forceinline__ uint4 pack16d(const double* v) {
+  double t[D::K];
+#pragma unroll
+  for (int k = 0; k < D::K; ++k) t[k] = k < RingGeom<D>::KE ? v[k] : 0.0;
+  const V8 w = D::pack_d(t);
+  return make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
+}
+
+// Special / lost shards on the last rank (p.special): does the tile at t0 lie in fast
+// shards only?  (Shards are far longer than a tile: one or two lookups.)
+__device__ __forceinline__ bool tile_fast(const RingParams& p, int64_t t0, int64_t te) {
+  const int64_t s_lo = p.sp.bnd.shard_of(t0), s_hi = p.sp.bnd.shard_of(min(t0 + te - 1, p.P - 1));
+  for (int64_t s = s_lo; s <= s_hi; ++s)
+    if (p.sp.cls[s] != kFast) return false;
+  return true;
+}
+
+// The value element e leaves the last rank with, as k_reduce writes it (emit_predicted,
+// bfly_merge.cu): the mean for fast shards and for shards predicted to adopt it, the
+// fallback for shards predicted to fall back; a shard without a prediction carries the
+// mean until FINISH rewrites it.  Means of special shards go to the workspace.
+template <class D>
+__device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean) {
+  const int64_t s = p.sp.bnd.shard_of(e);
+  const uint8_t c = p.sp.cls[s];
+  if (c == kFast) {
+    if (p.merged) p.merged[e] = mean;
+    return mean;
+  }
+  if (c == kSpecial) p.sp.ws[e] = mean;
+  const uint8_t pr = p.sp.pred[s] & kPredMask;
+  if (pr == kPredFallback) {
+    const double v = p.sp.fallback ? p.sp.fallback[e]
+                                   : (p.sp.fb_src ? D::raw(p.sp.fb_src, e) : __longlong_as_double(0x7ff8000000000000LL));
+    if (p.merged && (c == kLost || p.sp.merged_apart)) p.merged[e] = v;
+    return v;
+  }
+  if (pr == kPredMean && p.sp.merged_apart) p.merged[e] = mean;
+  return mean;
+}
+
 // ---------------------------------------------------------------------------
 // the roles
 // ---------------------------------------------------------------------------
@@ -446,12 +491,19 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
       if constexpr (REDUCE) {
 #pragma unroll
         for (int k = 0; k < KE; ++k) acc[k] = D::mean(acc[k], p.n_div);
-        if (p.merged) {
-          double* m = p.merged + t0 + tid * KE;
+        if (p.special && !tile_fast(p, t0, G::TE)) {  // predicted outcomes (k_classify) of special / lost shards
+          double v[KE];
 #pragma unroll
-          for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
+          for (int k = 0; k < KE; ++k) v[k] = final_value<D>(p, t0 + tid * KE + k, D::widen(acc[k]));
+          *reinterpret_cast<uint4*>(out + tid * 16) = pack16d<D>(v);
+        } else {
+          if (p.merged) {
+            double* m = p.merged + t0 + tid * KE;
+#pragma unroll
+            for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
+          }
+          *reinterpret_cast<uint4*>(out + tid * 16) = pack16<D>(acc);
         }
-        *reinterpret_cast<uint4*>(out + tid * 16) = pack16<D>(acc);
       } else {
 #pragma unroll
         for (int k = 0; k < KE; ++k) reinterpret_cast<Acc*>(out)[tid * KE + k] = acc[k];
@@ -462,9 +514,15 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
         for (int q = 0; q < p.n_src; ++q) v = D::add(v, D::load(s_src[q], t0 + e));
         if constexpr (REDUCE) {
           v = D::mean(v, p.n_div);
-          if (p.merged) p.merged[t0 + e] = D::widen(v);
-          for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], t0 + e, D::widen(v));
-          D::store(out, e, D::widen(v));
+          double f;
+          if (p.special) {
+            f = final_value<D>(p, t0 + e, D::widen(v));
+          } else {
+            f = D::widen(v);
+            if (p.merged) p.merged[t0 + e] = f;
+          }
+          for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], t0 + e, f);
+          D::store(out, e, f);
         } else {
           reinterpret_cast<Acc*>(out)[e] = v;
         }
@@ -772,7 +830,6 @@ static int ring_launch(RingParams p, cudaStream_t st) {
   return BFLY_OK;
 }
 
-int ring_round_setup(const bfly_merge_args_t* a, void* stream);  // bfly_merge.cu
 
 static unsigned long long* g_prof = nullptr;  // diagnostics buffer (BFLY_RING_PROFILE)
 static int g_prof_n = 0;
@@ -827,11 +884,13 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   int rc = bfly_ring_fused_layout(d->lanes, d->nb, d->dtype, &off_fin, &off_flags, &total);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (g == Z && d->merge_args) {
-    rc = ring_round_setup(d->merge_args, stream);
-    if (rc) return rc;
-  }
   RingParams p{};
+  if (g == Z && d->merge_args) {
+    rc = ring_round_setup(d->merge_args, stream, &p.sp);
+    if (rc) return rc;
+    p.special = d->special != 0;
+  }
+  if (p.special && !d->merge_args) return fail(BFLY_E_INVALID_ARG, "fused ring: special shards need merge_args");
   p.g = g;
   p.G = G;
   p.L = d->lanes;

@@ -71,6 +71,29 @@ def special_ranges(assign: np.ndarray, P: int, failures: set, corrupted: set) ->
     return runs
 
 
+CLS_FAST, CLS_SPECIAL, CLS_LOST = 0, 1, 2
+PRED_NONE, PRED_MEAN, PRED_FALLBACK = 0, 1, 2
+
+
+def classify_host(assign: np.ndarray, failures: set, corrupted: set, n_alive: int):
+    """Host restatement of k_classify (csrc/bfly_merge.cu) for a chained reduce: per shard
+    the class (fast / special / lost) and the predicted outcome of special and lost shards
+    (an honest majority adopts the mean; no majority among >= 2 survivors falls back; a
+    lone corrupted survivor has no prediction)."""
+    S = assign.shape[0]
+    cls = np.zeros(S, dtype=np.uint8)
+    pred = np.zeros(S, dtype=np.uint8)
+    for s in range(S):
+        surv = [int(m) for m in assign[s] if int(m) not in failures]
+        if not surv or n_alive == 0:
+            cls[s], pred[s] = CLS_LOST, PRED_FALLBACK
+        elif any(m in corrupted for m in surv):
+            cls[s] = CLS_SPECIAL
+            nh = sum(1 for m in surv if m not in corrupted)
+            pred[s] = PRED_MEAN if 2 * nh > len(surv) else (PRED_FALLBACK if len(surv) >= 2 else PRED_NONE)
+    return cls, pred
+
+
 def pack_results(entries, source, status, flagged, out):
     """entries | source | status | flagged into one byte buffer (8-byte aligned parts first)."""
     parts = [entries.reshape(-1).view(torch.uint8), source.view(torch.uint8), status.view(torch.uint8),
@@ -229,11 +252,6 @@ class ShardedButterflyMerge:
         self._straddle_dev = torch.tensor(straddlers, dtype=torch.int32, device=self.dev)
         # BFLY_RING_LATE=0 (diagnostics): no per-chunk finishing, every special shard after the ring
         self._per_chunk_finish = os.environ.get("BFLY_RING_LATE", "1") != "0"
-        late = ([r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())]
-                if G > 1 and self._per_chunk_finish else runs)
-        self.late_runs = late
-        self.special_runs = late  # kept name: ranges broadcast after the ring
-        self._late_set = self._range_set(late) if late else None
         # fallback values come from the lowest alive miner when no fallback is given; when
         # that replica lives on another rank the last rank reads it in place over NVLink
         # (IPC-mapped): chunk k of it is only overwritten by the relay, which starts after
@@ -243,6 +261,31 @@ class ShardedButterflyMerge:
         if self._needs_fb:
             m0 = self.alive[0]
             self.fb_owner = next(r for r in range(G) if sum(self.counts[: r + 1]) > m0)
+        # The persistent ring (one kernel per GPU, csrc/bfly_ring.cu) runs every round whose
+        # shards are >= 2 elements long and whose replicas are 16-byte aligned on every rank.
+        # Corrupted / lost shards ride along with k_classify's predicted outcome and are
+        # decided after the kernel; it needs that no decision can end in fallback values
+        # the relay has already overwritten: the fallback is given, or the lowest alive
+        # replica is not on the last rank and no special shard has an honest majority
+        # (only such a shard could, with non-finite means, fall back unpredicted).
+        self._cls, self._pred = classify_host(assign, failures, corrupted, len(self.alive))
+        self._special_ids = np.flatnonzero(self._cls != CLS_FAST)
+        honest_major = bool(np.any((self._cls == CLS_SPECIAL) & (self._pred == PRED_MEAN)))
+        self.fused = bool(G > 1 and self.P // plan.n_shards >= 2 and os.environ.get("BFLY_RING_FUSED", "1") != "0"
+                          and not (self._needs_fb and (self.fb_owner == G - 1 or honest_major)))
+        if self.fused:
+            ok = torch.tensor([int(all(t.data_ptr() % 16 == 0 for t in self.local))], device=self.dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            self.fused = bool(ok.item())
+        self._corr_kind = np.zeros(self.n, dtype=np.int32)
+        for m, c in (corruptions or {}).items():
+            self._corr_kind[int(m)] = int(c.code()) if hasattr(c, "code") else 1
+        late = ([] if self.fused else
+                [r for r in runs if any(r[0] < b < r[1] for b in self._chunk_starts())]
+                if G > 1 and self._per_chunk_finish else runs)
+        self.late_runs = late
+        self.special_runs = late  # kept name: ranges broadcast after the ring
+        self._late_set = self._range_set(late) if late else None
         if G > 1 and self._needs_fb and self.fb_owner != G - 1:
             info = _ipc_export(local[m0 - self.offset]) if self.rank == self.fb_owner else None
             infos = [None] * G
@@ -277,15 +320,6 @@ class ShardedButterflyMerge:
         self._src_table = self._table(self.local_alive) if self.local_alive else None
         self._local_table = self._table(self.local)
         self._fb_table = self._table([self._fb_buf]) if self._fb_buf is not None else None
-        # every shard fast (no corrupted survivor, fewer than r failures, shards of >= 2
-        # elements, 16-byte aligned replicas on every rank for the TMA bulk copies): the
-        # whole round runs as one persistent kernel per GPU
-        self.fused = bool(G > 1 and not corrupted and len(failures) < self.plan_r
-                          and self.P // plan.n_shards >= 2 and os.environ.get("BFLY_RING_FUSED", "1") != "0")
-        if self.fused:
-            ok = torch.tensor([int(all(t.data_ptr() % 16 == 0 for t in self.local))], device=self.dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            self.fused = bool(ok.item())
         if self.fused:
             self._late_mode = False  # (r = 3) every shard's FINISH runs after the kernel
             self._setup_fused()
@@ -387,6 +421,7 @@ class ShardedButterflyMerge:
         if self.is_last:
             d.d_merged = self.job.merged.data_ptr() if self.job.merged is not None else None
             d.merge_args = ctypes.pointer(self.job._args)
+            d.special = int(len(self._special_ids) > 0)
         self._fdesc = d
 
     def _setup_ring(self):
@@ -638,6 +673,8 @@ class ShardedButterflyMerge:
         elif self.want_merged:
             self.merged.copy_(self.job.merged)
         unpack_results(self._res, self.entries, self.source, self.status, self.flagged)
+        if G > 1 and self.fused and len(self._special_ids):
+            self._rebroadcast_mispredicted()
         mark("end")
         if tm is not None:
             torch.cuda.synchronize(self.dev)
@@ -645,6 +682,36 @@ class ShardedButterflyMerge:
         if self.debug == 2 and G > 1:
             self._watch(self._marks)
         return self
+
+    def _rebroadcast_mispredicted(self):
+        """Persistent ring: the relayed tiles of special / lost shards carried the predicted
+        outcome; the shards FINISH decided otherwise (k_apply rewrote them on the last rank)
+        are sent to the other ranks and scattered into their replicas."""
+        src = self.source.cpu().numpy()
+        ids = self._special_ids
+        pred = self._pred[ids]
+        srcs = src[ids]
+        honest_src = self._corr_kind[np.maximum(srcs, 0)] == 0
+        as_pred = np.where(srcs < 0, pred == PRED_FALLBACK, (pred == PRED_MEAN) & honest_src)
+        mis = ids[~as_pred]
+        self.mispredicted = len(mis)
+        if not len(mis):
+            return
+        base, rem = divmod(self.P, self.plan.n_shards)
+        runs = []
+        for sh in mis.tolist():
+            lo = sh * base + min(sh, rem)
+            hi = lo + base + (1 if sh < rem else 0)
+            if runs and runs[-1][1] == lo:
+                runs[-1][1] = hi
+            else:
+                runs.append([lo, hi])
+        rset = self._range_set(runs)
+        if self.is_last:
+            self._copy_ranges(rset, self.local[0].data_ptr(), None, 0, 0)
+        dist.broadcast(rset[1], src=self.world - 1)
+        if not self.is_last:
+            self._copy_ranges(rset, None, self._local_table.data_ptr(), len(self.local), 1)
 
     def timeline(self) -> list:
         """BFLY_DEBUG_RING=3: (op, ms after the round started) for every op of the last
