@@ -248,17 +248,23 @@ int bfly_ring_round(const bfly_ring_desc_t* desc, uint32_t round_index);
 int bfly_ring_ops(int32_t rank, int32_t world, int32_t k_chunks, int32_t nb, uint32_t round_index,
                   int32_t late, int32_t* out, int32_t cap);
 
-/* The whole multi-GPU round in ONE persistent kernel per GPU (k_ring): the payload is
- * cut into tiles dealt round-robin to `lanes` lanes; lane c of every rank is a CTA
- * (a CTA pair on ranks < last: chain + relay) that hands tile after tile to lane c of
- * the neighbouring rank through a slot ring in the neighbour's IPC region, with
- * 64-bit monotonic flags stored / polled by the SMs (st.release.sys / ld.acquire.sys)
- * — the transfer of tile i overlaps the reduction of tile i+1.  Same values as
- * bfly_ring_round (running fp64 sums in ascending miner order); every shard must have
- * >= 2 elements and the replicas must be 16-byte aligned.  Rounds with corrupted / lost shards run it too (desc.special):
- * the relayed tiles then carry k_classify's predicted outcome and FINISH on the last rank
- * decides the special shards after the kernel (the caller re-broadcasts the few whose
- * decision differs from the prediction).                                          */
+/* The whole multi-GPU round in ONE persistent kernel per GPU (k_ring,
+ * csrc/bfly_ring.cu): the payload is cut into tiles (4 KB of each replica) dealt
+ * round-robin to `lanes` lanes, one CTA per SM; lane c of every rank hands tile after
+ * tile to lane c of the neighbouring rank through a slot ring in the neighbour's IPC
+ * region.  Warp-specialised: a loader warp bulk-loads replica tiles and incoming sums
+ * (TMA, mbarrier stage ring), compute warps add in ascending miner order, a storer
+ * warp bulk-stores into the next rank's inbox, relay warps move the final tiles into
+ * every replica, a publisher warp releases 64-bit monotonic flags (st.release.sys;
+ * consumers poll with ld.acquire.sys) — the NVLink transfer of tile i overlaps the
+ * HBM stream of tile i+1.  Same values as bfly_ring_round (running fp64 sums in
+ * ascending miner order).  Needs shards of >= 2 elements and 16-byte aligned
+ * replicas.  Rounds with corrupted / lost shards (desc.special on the last rank):
+ * the relayed tiles carry k_classify's predicted outcome, FINISH on the last rank
+ * decides those shards after the kernel, and the caller re-broadcasts the few whose
+ * decision differs from the prediction.
+ * Replaces, for these rounds, the chunked exchange of bfly_ring_round; the reference
+ * has no multi-GPU path (run_all_reduce, butterfly.py:161-295, is one process).     */
 typedef struct bfly_ring_fused_desc {
   int32_t rank, world;           /* this process's rank and the ring size            */
   int32_t lanes, nb;             /* lanes (equal on every rank), slots per lane      */
