@@ -759,7 +759,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
   const bool last = p.g == p.G - 1;
   const int w = (int)(threadIdx.x / 32);
   const bool lead = (threadIdx.x & 31) == 0;
-  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 20] = global_ns();
+  if (p.prof && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.prof[blockIdx.x * kProfSlots + 20] = global_ns();
+    p.prof[blockIdx.x * kProfSlots + 22] = smid;
+  }
   if (w < kWLoad) {
     const long long t_start = clock64();
     if (last)

@@ -73,6 +73,11 @@ def main():
                          "span": round((te.max() - ts.min()) / 1e6, 3),
                          "mean_dur": round((te - ts).mean() / 1e6, 3), "max_dur": round((te - ts).max() / 1e6, 3),
                          "end_skew": round((te.max() - te.min()) / 1e6, 3)}
+        dur = (te - ts) / 1e6
+        order = np.argsort(dur)
+        out["lane_ms_pct"] = [round(float(np.percentile(dur, q)), 2) for q in (0, 10, 50, 90, 100)]
+        out["slowest_lanes"] = [(int(c), int(a[c, 22]), round(float(dur[c]), 2)) for c in order[-6:]]
+        out["fastest_lanes"] = [(int(c), int(a[c, 22]), round(float(dur[c]), 2)) for c in order[:4]]
     for r in range(world):
         if r == rank:
             print(json.dumps(out), flush=True)
