@@ -271,7 +271,8 @@ typedef struct bfly_ring_fused_desc {
   int32_t dtype;                 /* BFLY_* element type of the replicas              */
   int32_t n_src, n_dst, n_div;   /* alive local replicas, all local replicas, divisor */
   int64_t payload_len;           /* P                                                */
-  uint64_t round_index;          /* rounds already run on this region (flags are monotonic) */
+  uint64_t round_index;          /* informational: the flags are monotonic step counts the
+                                    kernel persists per lane in the region itself      */
   const uint64_t* peer_base;     /* [world] region base of every rank as mapped here  */
   const void* const* d_src;      /* device table of the alive local replicas          */
   void* const* d_dst;            /* device table of every local replica (scatter-back) */

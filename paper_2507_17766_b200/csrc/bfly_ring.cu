@@ -57,19 +57,20 @@ constexpr int kNS = 4;            // replica stages
 constexpr int kRB = 8;            // replica tiles per stage
 constexpr int kNR = 4;            // relay stages
 constexpr int kNO = 4;            // outgoing-tile stages
+constexpr int kNT = 8;            // chain steps the loader may lead the storer by (tile-id ring)
 constexpr int kMaxLag = 3;        // a step is published p.lag (1..3) steps later, when its bytes have landed
 constexpr int kTileBytes = 4096;  // one replica's share of a tile
 
 struct RingParams {
   int g, G, L, NB;
   int64_t P, T;  // elements, tiles
-  uint64_t round;
   unsigned char* my;     // own region
   unsigned char* nxt;    // chain target (g + 1), or rank 0 for the last rank
   unsigned char* prv;    // acc credits go here (g - 1); null on rank 0
   unsigned char* fsucc;  // relay successor (g + 1 < last), else null
   unsigned char* fpred;  // relay predecessor (last for rank 0, else g - 1)
-  int64_t off_fin, off_flags;
+  int64_t off_fin, off_flags, off_steps;
+  unsigned long long* tile_ctr;  // rank 0: next tile of the round (zeroed before the launch)
   const void* const* src;
   int n_src;
   void* const* dst;
@@ -92,15 +93,19 @@ struct RingGeom {
   using Acc = typename D::Acc;                  // running sums travel at accumulator width
   static constexpr int ACC_BYTES = TE * (int)sizeof(Acc);
   static constexpr int FIN_BYTES = TE * ESIZE;  // == kTileBytes
-  // shared memory: replica stages | 2 acc stages | 2 out stages | relay stages | barriers | pointers
+  // an inbox slot / outgoing stage: a 16-byte header (the tile id) + the tile
+  static constexpr int ACC_SLOT = 16 + ACC_BYTES;
+  static constexpr int FIN_SLOT = 16 + FIN_BYTES;
+  static constexpr int OUT_SLOT = ACC_SLOT;  // >= FIN_SLOT
+  // shared memory: replica stages | 2 acc stages | out stages | relay stages | barriers,
+  // tile rings, mailbox | pointers
   static constexpr int OFF_REP = 0;
   static constexpr int OFF_ACC = OFF_REP + kNS * kRB * kTileBytes;
   static constexpr int OFF_OUT = OFF_ACC + 2 * ACC_BYTES;
-  static constexpr int OFF_REL = OFF_OUT + kNO * ACC_BYTES;
-  static constexpr int OFF_BAR = OFF_REL + kNR * FIN_BYTES;
-  static constexpr int N_BAR = 2 * kNS + 4 + 2 * kNO + 2 * kNR;
-  static constexpr int OFF_MAIL = OFF_BAR + 8 * N_BAR;  // landed-step counters: [0] chain / reduce, [1] relay
-  static constexpr int OFF_PTR = OFF_MAIL + 16;
+  static constexpr int OFF_REL = OFF_OUT + kNO * OUT_SLOT;
+  static constexpr int OFF_BAR = OFF_REL + kNR * FIN_SLOT;
+  static constexpr int N_BAR = 2 * kNS + 4 + 2 * kNO + 2 * kNR + 2 * kNT;
+  static constexpr int OFF_PTR = OFF_BAR + 8 * (N_BAR + kNT + kNR + 4);
 };
 
 // ---------------------------------------------------------------------------
@@ -286,11 +291,11 @@ __device__ __forceinline__ unsigned round16(int64_t b) { return (unsigned)((b + 
 
 template <class D>
 __device__ __forceinline__ typename D::Acc* acc_slot(unsigned char* region, const RingParams& p, int lane, int slot) {
-  return reinterpret_cast<typename D::Acc*>(region) + ((int64_t)lane * p.NB + slot) * RingGeom<D>::TE;
+  return reinterpret_cast<typename D::Acc*>(region + ((int64_t)lane * p.NB + slot) * RingGeom<D>::ACC_SLOT);
 }
 template <class D>
 __device__ __forceinline__ unsigned char* fin_slot(unsigned char* region, const RingParams& p, int lane, int slot) {
-  return region + p.off_fin + ((int64_t)lane * p.NB + slot) * RingGeom<D>::FIN_BYTES;
+  return region + p.off_fin + ((int64_t)lane * p.NB + slot) * RingGeom<D>::FIN_SLOT;
 }
 
 // 16 bytes of one replica -> KE values / KE values -> 16 bytes (through the 32-byte
@@ -363,18 +368,15 @@ __device__ __forceinline__ double final_value(const RingParams& p, int64_t e, do
 
 struct Lane {
   int c;
-  int64_t steps;
-  uint64_t base;  // monotonic flags: the steps of earlier rounds on this region
+  uint64_t base_c, base_r;  // steps of earlier rounds on this lane (chain side, relay side)
 };
 
-template <class D>
-__device__ __forceinline__ int64_t tile_start(const RingParams& p, const Lane& ln, int64_t i) {
-  return (ln.c + i * p.L) * (int64_t)RingGeom<D>::TE;
-}
-
-// barriers (in shared memory, after the stages)
+// barriers and small rings (in shared memory, after the stages)
 struct Bars {
-  uint64_t *rep_full, *rep_empty, *acc_full, *acc_empty, *out_full, *out_empty, *rel_full, *rel_empty;
+  uint64_t *rep_full, *rep_empty, *acc_full, *acc_empty, *out_full, *out_empty, *rel_full, *rel_empty, *tile_full,
+      *tile_empty;
+  volatile int64_t *tile_of, *rtile_of;  // tile of chain step i (ring kNT), of relay step i (ring kNR)
+  uint64_t* mail;                        // [0] chain landed, [1] relay landed, [2] chain done, [3] relay done
   template <class D>
   __device__ static Bars at(unsigned char* sm) {
     uint64_t* b = reinterpret_cast<uint64_t*>(sm + RingGeom<D>::OFF_BAR);
@@ -387,11 +389,27 @@ struct Bars {
     r.out_empty = b + 2 * kNS + 4 + kNO;
     r.rel_full = b + 2 * kNS + 4 + 2 * kNO;
     r.rel_empty = b + 2 * kNS + 4 + 2 * kNO + kNR;
+    r.tile_full = b + 2 * kNS + 4 + 2 * kNO + 2 * kNR;
+    r.tile_empty = r.tile_full + kNT;
+    r.tile_of = reinterpret_cast<volatile int64_t*>(r.tile_empty + kNT);
+    r.rtile_of = r.tile_of + kNT;
+    r.mail = reinterpret_cast<uint64_t*>(const_cast<int64_t*>(r.rtile_of + kNR));
     return r;
   }
 };
 
-// LOADER (lane 0 of warp kWLoad): incoming sums and replica tiles into the stages
+// the tile id a slot carries in its 16-byte header (-1: the lane's last step)
+__device__ __forceinline__ int64_t slot_tile(const void* slot) {
+  int64_t v;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+  return v;
+}
+
+// LOADER (lane 0 of warp kWLoad).  Rank 0 deals the tiles: each step takes the next
+// tile of the round from a counter shared by its lanes (a lane on a slower SM simply
+// takes fewer), and the tile id travels in every slot header, so lane c of every later
+// rank processes exactly the tiles lane c of rank 0 took.  Then: replica tiles into
+// the stages, the incoming running sums into an acc stage.
 template <class D>
 __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* sm, const void** s_src) {
   using G = RingGeom<D>;
@@ -402,11 +420,26 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
   uint64_t known = 0;
   int64_t rs = 0;  // replica stage uses so far
   Prof pf(p, 0);
-  for (int64_t i = 0; i < ln.steps; ++i) {
-    const uint64_t j = ln.base + (uint64_t)i;
-    const int64_t t0 = tile_start<D>(p, ln, i);
+  for (int64_t i = 0;; ++i) {
+    const uint64_t j = ln.base_c + (uint64_t)i;
+    const int k = (int)(i % kNT);
+    if (i >= kNT) mbar_wait(p, B.tile_empty + k, (unsigned)((i / kNT - 1) & 1));
+    int64_t tile;
+    const unsigned char* in = reinterpret_cast<const unsigned char*>(acc_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)));
+    if (has_in) {
+      pf.start();
+      flag_wait(p, ready_in, j + 1, known);
+      pf.stop(1);
+      tile = slot_tile(in);
+    } else {
+      tile = (int64_t)atomicAdd(p.tile_ctr, 1ull);
+      if (tile >= p.T) tile = -1;
+    }
+    B.tile_of[k] = tile;
+    mbar_arrive(B.tile_full + k);
+    if (tile < 0) break;
+    const int64_t t0 = tile * G::TE;
     const int64_t n = min((int64_t)G::TE, p.P - t0);
-    // the replica tiles first: they do not wait for the upstream rank
     for (int q0 = 0; n == G::TE && q0 < p.n_src; q0 += kRB, ++rs) {
       const int s = (int)(rs % kNS);
       const int64_t u = rs / kNS;
@@ -422,9 +455,6 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
     }
     // (the partial last tile: compute warps read its replicas directly)
     if (has_in) {
-      pf.start();
-      flag_wait(p, ready_in, j + 1, known);
-      pf.stop(1);
       const int a = (int)(i & 1);
       const int64_t ua = i >> 1;
       pf.start();
@@ -432,8 +462,7 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
       pf.stop(2);
       const unsigned bytes = round16(n * (int64_t)sizeof(typename G::Acc));
       mbar_expect_tx(B.acc_full + a, bytes);
-      bulk_load(sm + G::OFF_ACC + a * G::ACC_BYTES, acc_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)), bytes,
-                B.acc_full + a);
+      bulk_load(sm + G::OFF_ACC + a * G::ACC_BYTES, in + 16, bytes, B.acc_full + a);
     }
   }
   pf.flush();
@@ -453,15 +482,18 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
   int64_t rs = 0;
   Prof pf(p, threadIdx.x == 0 ? 4 : -1);
   if (threadIdx.x) pf.out = nullptr;
-  for (int64_t i = 0; i < ln.steps; ++i) {
-    const int64_t t0 = tile_start<D>(p, ln, i);
+  for (int64_t i = 0;; ++i) {
+    mbar_wait(p, B.tile_full + (int)(i % kNT), (unsigned)((i / kNT) & 1));
+    const int64_t tile = B.tile_of[i % kNT];
+    if (tile < 0) break;
+    const int64_t t0 = tile * G::TE;
     const int64_t n = min((int64_t)G::TE, p.P - t0);
     const int a = (int)(i & 1);
     const int64_t ua = i >> 1;
     const Acc* in = reinterpret_cast<const Acc*>(sm + G::OFF_ACC + a * G::ACC_BYTES);
     const int o = (int)(i % kNO);
     const int64_t uo = i / kNO;
-    unsigned char* out = sm + G::OFF_OUT + o * G::ACC_BYTES;
+    unsigned char* out = sm + G::OFF_OUT + o * G::OUT_SLOT + 16;  // after the header
     pf.start();
     if (has_in) mbar_wait(p, B.acc_full + a, (unsigned)(ua & 1));
     pf.stop(0);
@@ -539,9 +571,15 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
   pf.flush();
 }
 
+// Persisted step count of a lane side (the next round's base), in the own region.
+__device__ __forceinline__ uint64_t* steps_at(const RingParams& p, int side, int lane) {
+  return reinterpret_cast<uint64_t*>(p.my + p.off_steps) + (int64_t)side * p.L + lane;
+}
+
 // STORER (lane 0 of warp kWStore): returns the inbox slot, bulk-stores the outgoing
-// tile (next rank's inbox; on the last rank also every local replica) and publishes
-// each step once its bytes have landed (one step later, so it never stalls the pipe)
+// tile with its header (next rank's inbox; on the last rank also every local replica)
+// and posts the steps that have landed to the publisher (p.lag steps later, so it
+// never stalls the pipe).  The lane's last step sends the end marker (tile -1).
 template <class D, bool REDUCE>
 __device__ void ring_storer(const RingParams& p, const Lane& ln, unsigned char* sm, void** s_dst) {
   using G = RingGeom<D>;
@@ -549,48 +587,61 @@ __device__ void ring_storer(const RingParams& p, const Lane& ln, unsigned char* 
   const Bars B = Bars::at<D>(sm);
   uint64_t* credit = p.g > 0 ? flag_at(p.prv, p, kFAccFree, ln.c) : nullptr;
   uint64_t* free_out = REDUCE ? flag_at(p.my, p, kFFinFree, ln.c) : flag_at(p.my, p, kFAccFree, ln.c);
-  uint64_t* mail = reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL);  // published by the publisher warp
   const uint64_t pol = policy_evict_first();
   uint64_t known = 0;
   Prof pf(p, 8);
-  for (int64_t i = 0; i < ln.steps; ++i) {
-    const uint64_t j = ln.base + (uint64_t)i;
+  int64_t i = 0;
+  for (;; ++i) {
+    const uint64_t j = ln.base_c + (uint64_t)i;
     const int slot = (int)(j % (uint64_t)p.NB);
-    const int64_t t0 = tile_start<D>(p, ln, i);
-    const int64_t n = min((int64_t)G::TE, p.P - t0);
+    const int k = (int)(i % kNT);
+    mbar_wait(p, B.tile_full + k, (unsigned)((i / kNT) & 1));
+    const int64_t tile = B.tile_of[k];
     const int o = (int)(i % kNO);
     pf.start();
-    mbar_wait(p, B.out_full + o, (unsigned)((i / kNO) & 1));
+    if (tile >= 0) mbar_wait(p, B.out_full + o, (unsigned)((i / kNO) & 1));
     pf.stop(0);
-    if (credit) st_relaxed_sys(credit, j + 1);  // our inbox slot has been loaded and used
+    if (credit) st_relaxed_sys(credit, j + 1);  // our inbox slot has been read
     pf.start();
     if (j >= (uint64_t)p.NB) flag_wait(p, free_out, j + 1 - p.NB, known);
     pf.stop(1);
-    const unsigned char* out = sm + G::OFF_OUT + o * G::ACC_BYTES;
+    unsigned char* out = sm + G::OFF_OUT + o * G::OUT_SLOT;
+    *reinterpret_cast<volatile int64_t*>(out) = tile;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    unsigned bytes = 16;
+    int64_t t0 = 0, n = 0;
+    if (tile >= 0) {
+      t0 = tile * G::TE;
+      n = min((int64_t)G::TE, p.P - t0);
+      bytes += REDUCE ? round16(n * G::ESIZE) : round16(n * (int64_t)sizeof(Acc));
+    }
     if constexpr (REDUCE) {
       if (n == G::TE)
         for (int d = 0; d < p.n_dst; ++d)
-          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, out, kTileBytes, pol);
-      bulk_store(fin_slot<D>(p.nxt, p, ln.c, slot), out, round16(n * G::ESIZE));
+          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, out + 16, kTileBytes, pol);
+      bulk_store(fin_slot<D>(p.nxt, p, ln.c, slot), out, bytes);
     } else {
-      bulk_store(acc_slot<D>(p.nxt, p, ln.c, slot), out, round16(n * (int64_t)sizeof(Acc)));
+      bulk_store(acc_slot<D>(p.nxt, p, ln.c, slot), out, bytes);
     }
     bulk_commit();
     pf.start();
     bulk_wait_read<1>();  // step i - 1's stage has been read out: hand it back
     pf.stop(2);
     if (i >= 1) mbar_arrive(B.out_empty + (int)((i - 1) % kNO));
-    if (i >= p.lag && (i % p.pub_every) == 0) {  // step i - lag has landed: publish it
+    mbar_arrive(B.tile_empty + k);
+    if (tile < 0) break;
+    if (i >= p.lag && (i % p.pub_every) == 0) {  // step i - lag has landed: post it
       pf.start();
       bulk_wait_landed_n(p.lag);
       pf.stop(3);
-      mail_post(mail, j + 1 - p.lag);
+      mail_post(B.mail, j + 1 - p.lag);
     }
   }
-  if (ln.steps > 0) {
-    bulk_wait_landed<0>();
-    mail_post(mail, ln.base + (uint64_t)ln.steps);
-  }
+  bulk_wait_landed<0>();
+  const uint64_t total = ln.base_c + (uint64_t)i + 1;
+  *steps_at(p, 0, ln.c) = total;
+  mail_post(B.mail, total);
+  mail_post(B.mail + 2, 1);
   pf.flush();
 }
 
@@ -603,9 +654,8 @@ __device__ void ring_relay_loader(const RingParams& p, const Lane& ln, unsigned 
   uint64_t* ready_in = flag_at(p.my, p, kFFinReady, ln.c);
   uint64_t known = 0;
   Prof pf(p, 12);
-  for (int64_t i = 0; i < ln.steps; ++i) {
-    const uint64_t j = ln.base + (uint64_t)i;
-    const int64_t n = min((int64_t)G::TE, p.P - tile_start<D>(p, ln, i));
+  for (int64_t i = 0;; ++i) {
+    const uint64_t j = ln.base_r + (uint64_t)i;
     const int s = (int)(i % kNR);
     const int64_t u = i / kNR;
     pf.start();
@@ -614,10 +664,17 @@ __device__ void ring_relay_loader(const RingParams& p, const Lane& ln, unsigned 
     pf.start();
     if (u >= 1) mbar_wait(p, B.rel_empty + s, (unsigned)((u - 1) & 1));
     pf.stop(1);
+    const unsigned char* in = fin_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB));
+    const int64_t tile = slot_tile(in);
+    B.rtile_of[s] = tile;
+    if (tile < 0) {
+      mbar_arrive(B.rel_full + s);
+      break;
+    }
+    const int64_t n = min((int64_t)G::TE, p.P - tile * G::TE);
     const unsigned bytes = round16(n * G::ESIZE);
     mbar_expect_tx(B.rel_full + s, bytes);
-    bulk_load(sm + G::OFF_REL + s * G::FIN_BYTES, fin_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)), bytes,
-              B.rel_full + s);
+    bulk_load(sm + G::OFF_REL + s * G::FIN_SLOT + 16, in + 16, bytes, B.rel_full + s);
   }
   pf.flush();
 }
@@ -629,54 +686,61 @@ __device__ void ring_relay_storer(const RingParams& p, const Lane& ln, unsigned 
   const bool lead = (threadIdx.x & 31) == 0;
   uint64_t* credit = flag_at(p.fpred, p, kFFinFree, ln.c);
   uint64_t* free_out = p.fsucc ? flag_at(p.my, p, kFFinFree, ln.c) : nullptr;
-  uint64_t* mail = reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL) + 1;  // published by the publisher warp
   const uint64_t pol = policy_evict_first();
   uint64_t known = 0;
   Prof pf(p, 16);
-  if (threadIdx.x & 31) pf.out = nullptr;
-  for (int64_t i = 0; i < ln.steps; ++i) {
-    const uint64_t j = ln.base + (uint64_t)i;
-    const int64_t t0 = tile_start<D>(p, ln, i);
-    const int64_t n = min((int64_t)G::TE, p.P - t0);
+  if (!lead) pf.out = nullptr;
+  int64_t i = 0;
+  for (;; ++i) {
+    const uint64_t j = ln.base_r + (uint64_t)i;
     const int s = (int)(i % kNR);
-    const unsigned char* st = sm + G::OFF_REL + s * G::FIN_BYTES;
+    unsigned char* st = sm + G::OFF_REL + s * G::FIN_SLOT;
     pf.start();
     mbar_wait(p, B.rel_full + s, (unsigned)((i / kNR) & 1));
     pf.stop(0);
-    if (n < G::TE) {  // partial last tile: the whole warp copies the bytes
+    const int64_t tile = B.rtile_of[s];
+    const int64_t t0 = tile >= 0 ? tile * G::TE : 0;
+    const int64_t n = tile >= 0 ? min((int64_t)G::TE, p.P - t0) : 0;
+    if (tile >= 0 && n < G::TE) {  // partial last tile: the whole warp copies the bytes
       const int64_t nb = n * G::ESIZE;
       for (int d = 0; d < p.n_dst; ++d)
-        for (int64_t b = threadIdx.x & 31; b < nb; b += 32) ((unsigned char*)s_dst[d])[t0 * G::ESIZE + b] = st[b];
+        for (int64_t b = threadIdx.x & 31; b < nb; b += 32) ((unsigned char*)s_dst[d])[t0 * G::ESIZE + b] = st[16 + b];
       __syncwarp();
     }
     if (lead) {
-      st_relaxed_sys(credit, j + 1);  // the inbox slot has been loaded
+      st_relaxed_sys(credit, j + 1);  // the inbox slot has been read
       if (n == G::TE)
         for (int d = 0; d < p.n_dst; ++d)
-          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, st, kTileBytes, pol);
+          bulk_store_stream((unsigned char*)s_dst[d] + t0 * G::ESIZE, st + 16, kTileBytes, pol);
       if (p.fsucc) {
         pf.start();
         if (j >= (uint64_t)p.NB) flag_wait(p, free_out, j + 1 - p.NB, known);
         pf.stop(1);
-        bulk_store(fin_slot<D>(p.fsucc, p, ln.c, (int)(j % (uint64_t)p.NB)), st, round16(n * G::ESIZE));
+        *reinterpret_cast<volatile int64_t*>(st) = tile;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_store(fin_slot<D>(p.fsucc, p, ln.c, (int)(j % (uint64_t)p.NB)), st, 16 + round16(n * G::ESIZE));
       }
       bulk_commit();
       pf.start();
       bulk_wait_read<1>();
       pf.stop(2);
       if (i >= 1) mbar_arrive(B.rel_empty + (int)((i - 1) % kNR));
-      if (p.fsucc && i >= p.lag && (i % p.pub_every) == 0) {
+      if (p.fsucc && tile >= 0 && i >= p.lag && (i % p.pub_every) == 0) {
         pf.start();
         bulk_wait_landed_n(p.lag);
         pf.stop(3);
-        mail_post(mail, j + 1 - p.lag);
+        mail_post(B.mail + 1, j + 1 - p.lag);
       }
     }
     __syncwarp();
+    if (tile < 0) break;
   }
-  if (lead && ln.steps > 0) {
+  if (lead) {
     bulk_wait_landed<0>();  // the last replica stores have landed before the kernel ends
-    if (p.fsucc) mail_post(mail, ln.base + (uint64_t)ln.steps);
+    const uint64_t total = ln.base_r + (uint64_t)i + 1;
+    *steps_at(p, 1, ln.c) = total;
+    if (p.fsucc) mail_post(B.mail + 1, total);
+    mail_post(B.mail + 3, 1);
   }
   pf.flush();
 }
@@ -684,34 +748,36 @@ __device__ void ring_relay_storer(const RingParams& p, const Lane& ln, unsigned 
 // PUBLISHER (lane 0 of warp kWPub): forwards the storers' landed-step counts to the
 // consumers' ready flags with a system-scope release.  The release (a MEMBAR.SYS)
 // takes microseconds; in its own warp it overlaps the storers' work, and a slow
-// publication simply covers several steps at once.
+// publication simply covers several steps at once.  Runs until both storers are done.
 template <class D>
 __device__ void ring_publisher(const RingParams& p, const Lane& ln, unsigned char* sm) {
-  using G = RingGeom<D>;
+  const Bars B = Bars::at<D>(sm);
   const bool last = p.g == p.G - 1;
-  const uint64_t* mail = reinterpret_cast<const uint64_t*>(sm + G::OFF_MAIL);
   uint64_t* out_c = last ? flag_at(p.nxt, p, kFFinReady, ln.c) : flag_at(p.nxt, p, kFAccReady, ln.c);
   uint64_t* out_r = (!last && p.fsucc) ? flag_at(p.fsucc, p, kFFinReady, ln.c) : nullptr;
-  const uint64_t target = ln.base + (uint64_t)ln.steps;
-  uint64_t done_c = ln.base, done_r = out_r ? ln.base : target;
+  uint64_t done_c = ln.base_c, done_r = ln.base_r;
+  bool fin_c = false, fin_r = last;  // the last rank has no relay
   uint64_t t0 = global_ns();
   const volatile uint64_t* abort_word = flag_at(p.my, p, kFAbort, 0);
-  while (done_c < target || done_r < target) {
+  while (!(fin_c && fin_r)) {
+    const bool end_c = mail_read(B.mail + 2) != 0, end_r = last || mail_read(B.mail + 3) != 0;
     bool moved = false;
-    const uint64_t vc = mail_read(mail);
+    const uint64_t vc = mail_read(B.mail);
     if (vc > done_c) {
       publish(p, out_c, vc);
       done_c = vc;
       moved = true;
     }
     if (out_r) {
-      const uint64_t vr = mail_read(mail + 1);
+      const uint64_t vr = mail_read(B.mail + 1);
       if (vr > done_r) {
         publish(p, out_r, vr);
         done_r = vr;
         moved = true;
       }
     }
+    fin_c = end_c && mail_read(B.mail) == done_c;
+    fin_r = end_r && (!out_r || mail_read(B.mail + 1) == done_r);
     if (moved) {
       t0 = global_ns();
     } else {
@@ -729,8 +795,12 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
   void** s_dst = const_cast<void**>(s_src + p.n_src);
   for (int q = threadIdx.x; q < p.n_src; q += blockDim.x) s_src[q] = p.src[q];
   for (int q = threadIdx.x; q < p.n_dst; q += blockDim.x) s_dst[q] = p.dst[q];
+  Lane ln;
+  ln.c = (int)blockIdx.x;
+  ln.base_c = *steps_at(p, 0, ln.c);
+  ln.base_r = *steps_at(p, 1, ln.c);
+  const Bars B = Bars::at<D>(sm);
   if (threadIdx.x == 0) {
-    const Bars B = Bars::at<D>(sm);
     const unsigned warps = kRingCompute / 32;
     for (int s = 0; s < kNS; ++s) {
       mbar_init(B.rep_full + s, 1);       // the loader's expect_tx + the bytes
@@ -748,13 +818,15 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
       mbar_init(B.rel_full + s, 1);
       mbar_init(B.rel_empty + s, 1);
     }
+    for (int k = 0; k < kNT; ++k) {
+      mbar_init(B.tile_full + k, 1);   // the loader
+      mbar_init(B.tile_empty + k, 1);  // the storer
+    }
+    B.mail[0] = ln.base_c;
+    B.mail[1] = ln.base_r;
+    B.mail[2] = B.mail[3] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
   }
-  Lane ln;
-  ln.c = (int)blockIdx.x;
-  ln.steps = ln.c < p.T ? (p.T - ln.c + p.L - 1) / p.L : 0;
-  ln.base = p.round * (uint64_t)ln.steps;
-  if (threadIdx.x < 2) reinterpret_cast<uint64_t*>(sm + G::OFF_MAIL)[threadIdx.x] = ln.base;
   __syncthreads();
   const bool last = p.g == p.G - 1;
   const int w = (int)(threadIdx.x / 32);
@@ -785,7 +857,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
         ring_storer<D, false>(p, ln, sm, s_dst);
     }
   } else if (w == kWPub) {
-    if (lead && ln.steps > 0) ring_publisher<D>(p, ln, sm);
+    if (lead) ring_publisher<D>(p, ln, sm);
   } else if (!last) {
     if (w == kWRLoad) {
       if (lead) ring_relay_loader<D>(p, ln, sm);
@@ -802,8 +874,8 @@ static size_t ring_smem_bytes(int n_src, int n_dst) {
 
 template <class D>
 static void ring_slot_bytes(int64_t* acc_b, int64_t* fin_b) {
-  *acc_b = RingGeom<D>::ACC_BYTES;
-  *fin_b = RingGeom<D>::FIN_BYTES;
+  *acc_b = RingGeom<D>::ACC_SLOT;
+  *fin_b = RingGeom<D>::FIN_SLOT;
 }
 
 constexpr int kRingMaxPtrs = 128;  // replica pointers a CTA stages (n_src + n_dst)
@@ -874,7 +946,8 @@ int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* of
   auto align = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
   *off_fin = align((int64_t)lanes * nb * acc_b);
   *off_flags = align(*off_fin + (int64_t)lanes * nb * fin_b);
-  *total = align(*off_flags + (int64_t)(kFAbort + 1) * lanes * 8);
+  // then the persisted step counts (2 x lanes) and rank 0's tile counter
+  *total = align(align(align(*off_flags + (int64_t)(kFAbort + 1) * lanes * 8) + 2 * (int64_t)lanes * 8) + 8);
   return BFLY_OK;
 }
 
@@ -901,7 +974,6 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.L = d->lanes;
   p.NB = d->nb;
   p.P = d->payload_len;
-  p.round = d->round_index;
   auto region = [&](int r) { return reinterpret_cast<unsigned char*>((uintptr_t)d->peer_base[r]); };
   p.my = region(g);
   p.nxt = g == Z ? region(0) : region(g + 1);
@@ -910,6 +982,13 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.fpred = g == 0 ? region(Z) : region(g - 1);
   p.off_fin = off_fin;
   p.off_flags = off_flags;
+  auto align = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
+  p.off_steps = align(off_flags + (int64_t)(kFAbort + 1) * p.L * 8);
+  p.tile_ctr = reinterpret_cast<unsigned long long*>(p.my + align(p.off_steps + 2 * (int64_t)p.L * 8));
+  if (g == 0) {  // the tiles of this round are dealt from 0 again
+    cudaError_t e = cudaMemsetAsync(p.tile_ctr, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused ring: tile counter");
+  }
   p.src = d->d_src;
   p.n_src = d->n_src;
   p.dst = d->d_dst;

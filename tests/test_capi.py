@@ -78,19 +78,25 @@ int main(void) {{
 def test_fused_ring_layout():
     """Region of the persistent ring (bfly_ring_fused_layout): per lane NB running-sum
     slots (one tile at accumulator width), NB final-vector slots (one tile at replica
-    width), then the five 64-bit flag arrays; every part 256-byte aligned."""
+    width), the five 64-bit flag arrays, the step counts and the tile counter; every part
+    256-byte aligned."""
     from paper_2507_17766_b200 import _lib
 
     lib = _lib.lib()
-    # a tile is 4 KB of every replica: 1024 fp32 / 2048 bf16 / 512 fp64 elements
-    for dtype, acc_b, fin_b in ((_lib.F32, 1024 * 8, 4096), (_lib.BF16, 2048 * 4, 4096),
-                                (_lib.F64WIRE, 512 * 8, 4096)):
+    # a tile is 4 KB of every replica: 1024 fp32 / 2048 bf16 / 512 fp64 elements; every
+    # slot starts with a 16-byte header (the tile id, -1 = the lane's last step)
+    def align(x):
+        return (x + 255) // 256 * 256
+
+    for dtype, acc_b, fin_b in ((_lib.F32, 16 + 1024 * 8, 16 + 4096), (_lib.BF16, 16 + 2048 * 4, 16 + 4096),
+                                (_lib.F64WIRE, 16 + 512 * 8, 16 + 4096)):
         o = [ctypes.c_int64() for _ in range(3)]
         _lib.check(lib.bfly_ring_fused_layout(148, 4, dtype, *[ctypes.byref(x) for x in o]))
         off_fin, off_flags, total = (x.value for x in o)
-        assert off_fin == 148 * 4 * acc_b
-        assert off_flags == off_fin + 148 * 4 * fin_b
-        assert total == (off_flags + 5 * 148 * 8 + 255) // 256 * 256
+        assert off_fin == align(148 * 4 * acc_b)
+        assert off_flags == align(off_fin + 148 * 4 * fin_b)
+        # flags, the persisted step counts of both lane sides, rank 0's tile counter
+        assert total == align(align(align(off_flags + 5 * 148 * 8) + 2 * 148 * 8) + 8)
     with pytest.raises(Exception):
         _lib.check(lib.bfly_ring_fused_layout(148, 1, _lib.F32, *[ctypes.byref(ctypes.c_int64()) for _ in range(3)]))
 
