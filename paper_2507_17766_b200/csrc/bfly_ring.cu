@@ -58,6 +58,8 @@ constexpr int kRB = 8;            // replica tiles per stage
 constexpr int kNR = 4;            // relay stages
 constexpr int kNO = 4;            // outgoing-tile stages
 constexpr int kNT = 8;            // chain steps the loader may lead the storer by (tile-id ring)
+constexpr int kSR = 512;          // tile schedule ring per lane (rank 0 -> every other rank)
+constexpr int kMaxG = 16;         // ranks the persistent ring supports
 constexpr int kMaxLag = 3;        // a step is published p.lag (1..3) steps later, when its bytes have landed
 constexpr int kTileBytes = 4096;  // one replica's share of a tile
 
@@ -71,6 +73,8 @@ struct RingParams {
   unsigned char* fpred;  // relay predecessor (last for rank 0, else g - 1)
   int64_t off_fin, off_flags, off_steps;
   unsigned long long* tile_ctr;  // rank 0: next tile of the round (zeroed before the launch)
+  int64_t off_sched;             // per lane kSR schedule words: (step + 1) << 32 | (tile + 1)
+  unsigned char* region[kMaxG];  // every rank's region (rank 0 writes the schedule into them)
   const void* const* src;
   int n_src;
   void* const* dst;
@@ -405,6 +409,22 @@ __device__ __forceinline__ int64_t slot_tile(const void* slot) {
   return v;
 }
 
+// The tile of chain step j of lane c, from the schedule rank 0 writes ahead of its data.
+__device__ __forceinline__ int64_t sched_read(const RingParams& p, int c, uint64_t j) {
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(p.my + p.off_sched) + (int64_t)c * kSR + j % kSR;
+  const uint32_t want = (uint32_t)(j + 1);
+  uint64_t v = ld_acquire_sys(w);
+  if ((uint32_t)(v >> 32) != want) {
+    const uint64_t t0 = global_ns();
+    const volatile uint64_t* abort_word = flag_at(p.my, p, kFAbort, 0);
+    while ((uint32_t)((v = ld_acquire_sys(w)) >> 32) != want) {
+      __nanosleep(20);
+      if (*abort_word || global_ns() - t0 > kRingTimeoutNs) ring_abort(p);
+    }
+  }
+  return (int64_t)(uint32_t)v - 1;
+}
+
 // LOADER (lane 0 of warp kWLoad).  Rank 0 deals the tiles: each step takes the next
 // tile of the round from a counter shared by its lanes (a lane on a slower SM simply
 // takes fewer), and the tile id travels in every slot header, so lane c of every later
@@ -426,14 +446,16 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
     if (i >= kNT) mbar_wait(p, B.tile_empty + k, (unsigned)((i / kNT - 1) & 1));
     int64_t tile;
     const unsigned char* in = reinterpret_cast<const unsigned char*>(acc_slot<D>(p.my, p, ln.c, (int)(j % (uint64_t)p.NB)));
-    if (has_in) {
+    if (has_in) {  // the tile rank 0 dealt for this step, known before its running sums arrive
       pf.start();
-      flag_wait(p, ready_in, j + 1, known);
+      tile = sched_read(p, ln.c, j);
       pf.stop(1);
-      tile = slot_tile(in);
     } else {
       tile = (int64_t)atomicAdd(p.tile_ctr, 1ull);
       if (tile >= p.T) tile = -1;
+      const uint64_t word = ((j + 1) << 32) | (uint64_t)(uint32_t)(tile + 1);
+      for (int r = 1; r < p.G; ++r)
+        st_relaxed_sys(reinterpret_cast<uint64_t*>(p.region[r] + p.off_sched) + (int64_t)ln.c * kSR + j % kSR, word);
     }
     B.tile_of[k] = tile;
     mbar_arrive(B.tile_full + k);
@@ -458,6 +480,7 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
       const int a = (int)(i & 1);
       const int64_t ua = i >> 1;
       pf.start();
+      flag_wait(p, ready_in, j + 1, known);
       if (ua >= 1) mbar_wait(p, B.acc_empty + a, (unsigned)((ua - 1) & 1));
       pf.stop(2);
       const unsigned bytes = round16(n * (int64_t)sizeof(typename G::Acc));
@@ -946,8 +969,9 @@ int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* of
   auto align = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
   *off_fin = align((int64_t)lanes * nb * acc_b);
   *off_flags = align(*off_fin + (int64_t)lanes * nb * fin_b);
-  // then the persisted step counts (2 x lanes) and rank 0's tile counter
-  *total = align(align(align(*off_flags + (int64_t)(kFAbort + 1) * lanes * 8) + 2 * (int64_t)lanes * 8) + 8);
+  // then the persisted step counts (2 x lanes), rank 0's tile counter and the schedule
+  *total = align(align(align(align(*off_flags + (int64_t)(kFAbort + 1) * lanes * 8) + 2 * (int64_t)lanes * 8) + 8) +
+                 (int64_t)kSR * lanes * 8);
   return BFLY_OK;
 }
 
@@ -985,6 +1009,11 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   auto align = [](int64_t x) { return (x + 255) & ~(int64_t)255; };
   p.off_steps = align(off_flags + (int64_t)(kFAbort + 1) * p.L * 8);
   p.tile_ctr = reinterpret_cast<unsigned long long*>(p.my + align(p.off_steps + 2 * (int64_t)p.L * 8));
+  p.off_sched = align(align(p.off_steps + 2 * (int64_t)p.L * 8) + 8);
+  if (G > kMaxG) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many ranks");
+  if ((int64_t)kSR < (int64_t)(G - 1) * (kNT + d->nb) + 1)
+    return fail(BFLY_E_UNSUPPORTED, "fused ring: schedule ring too short for this many ranks and slots");
+  for (int r = 0; r < G; ++r) p.region[r] = region(r);
   if (g == 0) {  // the tiles of this round are dealt from 0 again
     cudaError_t e = cudaMemsetAsync(p.tile_ctr, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_fail(e, "fused ring: tile counter");

@@ -95,8 +95,9 @@ def test_fused_ring_layout():
         off_fin, off_flags, total = (x.value for x in o)
         assert off_fin == align(148 * 4 * acc_b)
         assert off_flags == align(off_fin + 148 * 4 * fin_b)
-        # flags, the persisted step counts of both lane sides, rank 0's tile counter
-        assert total == align(align(align(off_flags + 5 * 148 * 8) + 2 * 148 * 8) + 8)
+        # flags, the persisted step counts of both lane sides, rank 0's tile counter, the
+        # tile schedule rank 0 writes ahead (512 words per lane)
+        assert total == align(align(align(align(off_flags + 5 * 148 * 8) + 2 * 148 * 8) + 8) + 512 * 148 * 8)
     with pytest.raises(Exception):
         _lib.check(lib.bfly_ring_fused_layout(148, 1, _lib.F32, *[ctypes.byref(ctypes.c_int64()) for _ in range(3)]))
 
