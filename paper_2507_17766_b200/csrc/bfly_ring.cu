@@ -57,6 +57,7 @@ constexpr int kNS = 4;            // replica stages
 constexpr int kRB = 8;            // replica tiles per stage
 constexpr int kNR = 4;            // relay stages
 constexpr int kNO = 4;            // outgoing-tile stages
+constexpr int kNA = 4;            // incoming running-sum stages
 constexpr int kNT = 8;            // chain steps the loader may lead the storer by (tile-id ring)
 constexpr int kSR = 512;          // tile schedule ring per lane (rank 0 -> every other rank)
 constexpr int kMaxG = 16;         // ranks the persistent ring supports
@@ -105,10 +106,10 @@ struct RingGeom {
   // tile rings, mailbox | pointers
   static constexpr int OFF_REP = 0;
   static constexpr int OFF_ACC = OFF_REP + kNS * kRB * kTileBytes;
-  static constexpr int OFF_OUT = OFF_ACC + 2 * ACC_BYTES;
+  static constexpr int OFF_OUT = OFF_ACC + kNA * ACC_BYTES;
   static constexpr int OFF_REL = OFF_OUT + kNO * OUT_SLOT;
   static constexpr int OFF_BAR = OFF_REL + kNR * FIN_SLOT;
-  static constexpr int N_BAR = 2 * kNS + 4 + 2 * kNO + 2 * kNR + 2 * kNT;
+  static constexpr int N_BAR = 2 * kNS + 2 * kNA + 2 * kNO + 2 * kNR + 2 * kNT;
   static constexpr int OFF_PTR = OFF_BAR + 8 * (N_BAR + kNT + kNR + 4);
 };
 
@@ -388,12 +389,12 @@ struct Bars {
     r.rep_full = b;
     r.rep_empty = b + kNS;
     r.acc_full = b + 2 * kNS;
-    r.acc_empty = b + 2 * kNS + 2;
-    r.out_full = b + 2 * kNS + 4;
-    r.out_empty = b + 2 * kNS + 4 + kNO;
-    r.rel_full = b + 2 * kNS + 4 + 2 * kNO;
-    r.rel_empty = b + 2 * kNS + 4 + 2 * kNO + kNR;
-    r.tile_full = b + 2 * kNS + 4 + 2 * kNO + 2 * kNR;
+    r.acc_empty = r.acc_full + kNA;
+    r.out_full = r.acc_empty + kNA;
+    r.out_empty = r.out_full + kNO;
+    r.rel_full = r.out_empty + kNO;
+    r.rel_empty = r.rel_full + kNR;
+    r.tile_full = r.rel_empty + kNR;
     r.tile_empty = r.tile_full + kNT;
     r.tile_of = reinterpret_cast<volatile int64_t*>(r.tile_empty + kNT);
     r.rtile_of = r.tile_of + kNT;
@@ -477,8 +478,8 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
     }
     // (the partial last tile: compute warps read its replicas directly)
     if (has_in) {
-      const int a = (int)(i & 1);
-      const int64_t ua = i >> 1;
+      const int a = (int)(i % kNA);
+      const int64_t ua = i / kNA;
       pf.start();
       flag_wait(p, ready_in, j + 1, known);
       if (ua >= 1) mbar_wait(p, B.acc_empty + a, (unsigned)((ua - 1) & 1));
@@ -511,8 +512,8 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
     if (tile < 0) break;
     const int64_t t0 = tile * G::TE;
     const int64_t n = min((int64_t)G::TE, p.P - t0);
-    const int a = (int)(i & 1);
-    const int64_t ua = i >> 1;
+    const int a = (int)(i % kNA);
+    const int64_t ua = i / kNA;
     const Acc* in = reinterpret_cast<const Acc*>(sm + G::OFF_ACC + a * G::ACC_BYTES);
     const int o = (int)(i % kNO);
     const int64_t uo = i / kNO;
@@ -829,7 +830,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
       mbar_init(B.rep_full + s, 1);       // the loader's expect_tx + the bytes
       mbar_init(B.rep_empty + s, warps);  // every compute warp
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kNA; ++a) {
       mbar_init(B.acc_full + a, 1);
       mbar_init(B.acc_empty + a, warps);
     }
