@@ -348,7 +348,40 @@ __device__ __forceinline__ bool tile_fast(const RingParams& p, int64_t t0, int64
 // fallback for shards predicted to fall back; a shard without a prediction carries the
 // mean until FINISH rewrites it.  Means of special shards go to the workspace.
 template <class D>
-__device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean) {
+__device__ __forceinline__ double fallback_one(const RingParams& p, int64_t e) {
+  return p.sp.fallback ? p.sp.fallback[e]
+                       : (p.sp.fb_src ? D::raw(p.sp.fb_src, e) : __longlong_as_double(0x7ff8000000000000LL));
+}
+
+// The fallback values of a thread's KE elements (from e0, 16-byte aligned in the replica),
+// loaded at once: usually from the lowest alive miner's replica on another GPU, so one
+// vector load over NVLink instead of KE dependent scalar ones.
+template <class D>
+__device__ __forceinline__ void fallback_vec16(const RingParams& p, int64_t e0, double* fb) {
+  constexpr int KE = RingGeom<D>::KE;
+  if (p.sp.fallback) {
+#pragma unroll
+    for (int k = 0; k < KE; ++k) fb[k] = p.sp.fallback[e0 + k];
+  } else if (p.sp.fb_src) {
+    uint32_t w[4];
+    asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"((const unsigned char*)p.sp.fb_src + e0 * RingGeom<D>::ESIZE));
+    V8 v;
+    v.w[0] = w[0], v.w[1] = w[1], v.w[2] = w[2], v.w[3] = w[3];
+    v.w[4] = v.w[5] = v.w[6] = v.w[7] = 0;
+    double t[8 * 4 / RingGeom<D>::ESIZE > 0 ? 8 * 4 / RingGeom<D>::ESIZE : 1];
+    D::unpack_raw(v, t);
+#pragma unroll
+    for (int k = 0; k < KE; ++k) fb[k] = t[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < KE; ++k) fb[k] = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+template <class D>
+__device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean, const double* fb_pre = nullptr) {
   const int64_t s = p.sp.bnd.shard_of(e);
   const uint8_t c = p.sp.cls[s];
   if (c == kFast) {
@@ -358,8 +391,7 @@ __device__ __forceinline__ double final_value(const RingParams& p, int64_t e, do
   if (c == kSpecial) p.sp.ws[e] = mean;
   const uint8_t pr = p.sp.pred[s] & kPredMask;
   if (pr == kPredFallback) {
-    const double v = p.sp.fallback ? p.sp.fallback[e]
-                                   : (p.sp.fb_src ? D::raw(p.sp.fb_src, e) : __longlong_as_double(0x7ff8000000000000LL));
+    const double v = fb_pre ? *fb_pre : fallback_one<D>(p, e);
     if (p.merged && (c == kLost || p.sp.merged_apart)) p.merged[e] = v;
     return v;
   }
@@ -548,9 +580,17 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
 #pragma unroll
         for (int k = 0; k < KE; ++k) acc[k] = D::mean(acc[k], p.n_div);
         if (p.special && !tile_fast(p, t0, G::TE)) {  // predicted outcomes (k_classify) of special / lost shards
-          double v[KE];
+          double v[KE], fb[KE];
+          const int64_t e0 = t0 + tid * KE;
+          bool need_fb = false;
 #pragma unroll
-          for (int k = 0; k < KE; ++k) v[k] = final_value<D>(p, t0 + tid * KE + k, D::widen(acc[k]));
+          for (int k = 0; k < KE; ++k) {
+            const int64_t sh = p.sp.bnd.shard_of(e0 + k);
+            need_fb |= p.sp.cls[sh] != kFast && (p.sp.pred[sh] & kPredMask) == kPredFallback;
+          }
+          if (need_fb) fallback_vec16<D>(p, e0, fb);
+#pragma unroll
+          for (int k = 0; k < KE; ++k) v[k] = final_value<D>(p, e0 + k, D::widen(acc[k]), need_fb ? fb + k : nullptr);
           *reinterpret_cast<uint4*>(out + tid * 16) = pack16d<D>(v);
         } else {
           if (p.merged) {
