@@ -84,7 +84,6 @@ struct RingParams {
   double* merged;
   unsigned long long* prof;  // diagnostics (BFLY_RING_PROFILE): wait cycles per CTA and counter
   int pub_every;             // publish every pub_every-th step (each publication covers the ones before)
-  int pub_relaxed;           // 1: after wait_group the flag is a relaxed store (no MEMBAR.SYS)
   int lag;                   // publication lag in steps (1..kMaxLag)
   int special;               // last rank: some shard is corrupted or lost (see RingSpecial)
   RingSpecial sp;
@@ -133,16 +132,12 @@ __device__ __forceinline__ void st_release_sys(uint64_t* a, uint64_t v) {
 __device__ __forceinline__ void st_relaxed_sys(uint64_t* a, uint64_t v) {
   asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
-// Publish `v` (steps landed) to the consumer.  The bulk group holding the data has
-// completed (cp.async.bulk.wait_group: its writes are performed at the destination),
-// so the flag may follow as a plain system-scope store; pub_relaxed == 0 keeps the
-// formal release (a MEMBAR.SYS per publication).
-__device__ __forceinline__ void publish(const RingParams& p, uint64_t* f, uint64_t v) {
-  if (p.pub_relaxed)
-    st_relaxed_sys(f, v);
-  else
-    st_release_sys(f, v);
-}
+// Publish `v` (steps landed) to the consumer: a system-scope release.  The storer saw
+// the bulk group complete (cp.async.bulk.wait_group + fence.proxy.async) and handed the
+// count over through shared memory (CTA-scope release / acquire), so the release is
+// cumulative over the data.  A relaxed store here was measured faster and is NOT safe:
+// stale tiles showed up in an 8-round stress test.
+__device__ __forceinline__ void publish(uint64_t* f, uint64_t v) { st_release_sys(f, v); }
 // storer -> publisher warp: `v` steps have landed (CTA-scope release through shared memory)
 __device__ __forceinline__ void mail_post(uint64_t* box, uint64_t v) {
   asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(box)), "l"(v)
@@ -828,14 +823,14 @@ __device__ void ring_publisher(const RingParams& p, const Lane& ln, unsigned cha
     bool moved = false;
     const uint64_t vc = mail_read(B.mail);
     if (vc > done_c) {
-      publish(p, out_c, vc);
+      publish(out_c, vc);
       done_c = vc;
       moved = true;
     }
     if (out_r) {
       const uint64_t vr = mail_read(B.mail + 1);
       if (vr > done_r) {
-        publish(p, out_r, vr);
+        publish(out_r, vr);
         done_r = vr;
         moved = true;
       }
@@ -1066,9 +1061,7 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.n_div = d->n_div;
   p.merged = g == Z ? d->d_merged : nullptr;
   p.pub_every = 1;
-  p.pub_relaxed = 0;
   if (const char* e = getenv("BFLY_RING_PUB_EVERY")) p.pub_every = atoi(e) > 0 ? atoi(e) : 1;
-  if (const char* e = getenv("BFLY_RING_PUB_RELAXED")) p.pub_relaxed = atoi(e) != 0;
   p.lag = 1;
   if (const char* e = getenv("BFLY_RING_LAG")) p.lag = atoi(e) < 1 ? 1 : (atoi(e) > kMaxLag ? kMaxLag : atoi(e));
   if (p.pub_every >= d->nb - p.lag) return fail(BFLY_E_INVALID_ARG, "fused ring: publication interval too long for nb");
