@@ -546,7 +546,12 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
     const int64_t uo = i / kNO;
     unsigned char* out = sm + G::OFF_OUT + o * G::OUT_SLOT + 16;  // after the header
     pf.start();
-    if (has_in) mbar_wait(p, B.acc_full + a, (unsigned)(ua & 1));
+    if (has_in) {
+      mbar_wait(p, B.acc_full + a, (unsigned)(ua & 1));
+      // the slot's sums are in shared memory: hand the slot back to the producer now,
+      // not after this step's compute and store (a shorter credit round trip)
+      if (tid == 0) st_relaxed_sys(flag_at(p.prv, p, kFAccFree, ln.c), ln.base_c + (uint64_t)i + 1);
+    }
     pf.stop(0);
     pf.start();
     if (uo >= 1) mbar_wait(p, B.out_empty + o, (unsigned)((uo - 1) & 1));
@@ -660,7 +665,7 @@ __device__ void ring_storer(const RingParams& p, const Lane& ln, unsigned char* 
     pf.start();
     if (tile >= 0) mbar_wait(p, B.out_full + o, (unsigned)((i / kNO) & 1));
     pf.stop(0);
-    if (credit) st_relaxed_sys(credit, j + 1);  // our inbox slot has been read
+    if (credit && tile < 0) st_relaxed_sys(credit, j + 1);  // the end marker's slot (data slots: compute)
     pf.start();
     if (j >= (uint64_t)p.NB) flag_wait(p, free_out, j + 1 - p.NB, known);
     pf.stop(1);

@@ -1,3 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_multigpu_gpu.py tests/test_multigpu_fuzz_gpu.py -x -q 2>&1 | tail -1
-BFLY_RING_TIMING=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29710 bench.py --gpus 4 --config c5 --no-e2e --steps 5 2>&1 | grep -o 'phases.*\|"ms_per_step": [0-9.]*'
+timeout 600 python -m pytest tests/test_multigpu_gpu.py -x -q -k "P3000017 or P4000037 or P1500007 or P777777 or P30007" 2>&1 | tail -1
+for G in 2 4; do for nb in 8 10; do
+echo "G=$G NB=$nb $(BFLY_FUSED_NB=$nb timeout 200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $G --master-addr 127.0.0.1 --master-port $((29000 + G * 100 + nb)) tools/ring_fused_probe.py 2>&1 | grep '^{"rank": 0' | cut -c1-40)"
+done; done
