@@ -90,6 +90,6 @@ def _free_port():
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_multigpu_host_collectives_gloo(world):
-    out = mp.Manager().dict()
+    out = mp.get_context("spawn").Manager().dict()  # no fork of a multi-threaded process
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert [out[r] for r in range(world)] == [1] * world
