@@ -8,37 +8,45 @@
 // replica (the scatter-back, orchestrator.py:581-590).
 //
 // k_ring runs that whole round in one launch, tile by tile:
-//   * the payload is cut into tiles of TE elements (4 KB of each replica), dealt
-//     round-robin to L lanes = one CTA per SM (tile t -> lane t % L, step t / L);
-//     lane c of rank g exchanges only with lane c of its neighbours;
+//   * the payload is cut into tiles of TE elements (4 KB of each replica); lane c
+//     (= CTA c, one per SM) of rank g exchanges only with lane c of its neighbours.
+//     Rank 0 deals the tiles dynamically — each step of a lane takes the next tile
+//     from a counter — and writes the tile id ahead into every other rank's schedule
+//     ring and into the header of every slot it sends, so lane c of every rank
+//     processes the same tiles in the same order; a lane on a slower SM simply takes
+//     fewer.  A tile id of -1 ends the lane's round;
 //   * per CTA, warp-specialised and asynchronous:
 //       LOADER warp   TMA bulk loads (cp.async.bulk ... mbarrier::complete_tx) of the
-//                     incoming running sums (inbox slot) and of the replica tiles into
-//                     a ring of shared-memory stages — up to NS x RB x 4 KB in flight;
+//                     replica tiles (as soon as the schedule names the tile) and of
+//                     the incoming running sums into rings of shared-memory stages;
 //       8 COMPUTE warps  read the stages, fp64 adds in ascending miner order (the
 //                     last rank also divides), write the outgoing tile to shared memory;
-//       STORER warp   TMA bulk stores of that tile into the next rank's inbox slot over
-//                     NVLink (and, on the last rank, into every local replica), then
-//                     publishes it;
+//       STORER warp   TMA bulk stores of that tile (with its header) into the next
+//                     rank's inbox slot over NVLink (and, on the last rank, into every
+//                     local replica);
 //       RELAY warps   (ranks < last) a bulk load of the final tile from the inbox and
 //                     bulk stores into every local replica and the successor's inbox:
 //                     the scatter-back without a single SM load or store;
+//       PUBLISHER     the system-scope releases of the `ready` flags;
 //   * each rank's inboxes are NB-slot rings per lane in its IPC region; producer and
 //     consumer order themselves with 64-bit monotonic counters (ready / free) in the
-//     waiter's region: the producer stores `ready` with st.release.sys after its bulk
-//     group has landed, the consumer polls with ld.acquire.sys and returns the slot
-//     (`free`) once it has been loaded.  No kernel launches, stream memory operations
-//     or host round trips per tile: NVLink transfers of tile i overlap the HBM stream
-//     of tile i+1 and the ring fills in G tile steps.  The inboxes (L x NB x 12 KB)
-//     stay small enough to live in L2.
+//     waiter's region: `ready` is released (st.release.sys) once the bulk group has
+//     landed, the consumer polls with ld.acquire.sys and returns the slot (`free`) as
+//     soon as its contents are in shared memory.  Step counts are persisted per lane,
+//     so the counters stay monotonic across rounds.  No kernel launches, stream memory
+//     operations or host round trips per tile: NVLink transfers of tile i overlap the
+//     HBM stream of tile i+1 and the ring fills in G tile steps.  The inboxes
+//     (L x NB x 12 KB) stay small enough to live in L2.
 // Deadlock freedom: every wait of step j points at step j of an earlier stage of the
 // path (chain 0..last, relay 0..last-1) or at step j - NB; the chain and the relay of a
-// lane run in different warps, and all CTAs are co-resident (cooperative launch).
-// Every wait traps after kRingTimeoutNs instead of hanging the GPU.
+// lane run in different warps, and all CTAs are co-resident (cooperative launch).  A
+// CPU model of the protocol runs under random interleavings for G = 2..8
+// (tests/test_ring_protocol.py).  Every wait traps after kRingTimeoutNs instead of
+// hanging the GPU.
 //
-// Only rounds whose shards are all fast use it (no corrupted survivor, fewer than r
-// failures): their final value is the mean, so no decision waits for the whole
-// vector.  Rounds with corrupted / lost shards run the chunked ring of bfly_peer.cu.
+// Corrupted / lost shards (p.special, last rank): their tiles leave with the outcome
+// k_classify predicts (the means go to the workspace); FINISH decides those shards after
+// the kernel and the host re-broadcasts the few decided otherwise (multigpu.py).
 #include <cuda_runtime.h>
 #include <stdlib.h>
 
