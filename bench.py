@@ -384,6 +384,10 @@ def run_multi(cfg, args, rank, world):
                                     "whole round per GPU (chain / reduce / fan-out kernels + NVLink ring)"),
                          "t_roof_ms": t_roof * 1e3, "hbm_bytes_per_gpu": per_gpu_hbm,
                          "nvlink_bytes_in_per_gpu": float(nvl.item()),
+                         # algorithmic NVLink bytes into the busiest rank / round time, against
+                         # the 900 GB/s per-direction spec (770 GB/s measured peer copy)
+                         "nvlink_achieved_GBps": float(nvl.item()) / t_step / 1e9,
+                         "nvlink_frac_of_spec": float(nvl.item()) / t_step / 900e9,
                          "peaks": {"hbm_GBps": hbm_peak, "nvlink_GBps_per_direction": nvl_peak,
                                    "source": "MEASURED_PEAKS.json hbm_gbs; NVLink 770 GB/s measured peer copy "
                                              "(B200_PROFILING.md)"}},
