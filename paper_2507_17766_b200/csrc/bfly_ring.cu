@@ -384,14 +384,15 @@ __device__ __forceinline__ void fallback_vec16(const RingParams& p, int64_t e0, 
 }
 
 template <class D>
-__device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean, const double* fb_pre = nullptr) {
-  const int64_t s = p.sp.bnd.shard_of(e);
+__device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean, const double* fb_pre = nullptr,
+                                              int64_t s = -1, bool ws_done = false) {
+  if (s < 0) s = p.sp.bnd.shard_of(e);
   const uint8_t c = p.sp.cls[s];
   if (c == kFast) {
     if (p.merged) p.merged[e] = mean;
     return mean;
   }
-  if (c == kSpecial) p.sp.ws[e] = mean;
+  if (c == kSpecial && !ws_done) p.sp.ws[e] = mean;
   const uint8_t pr = p.sp.pred[s] & kPredMask;
   if (pr == kPredFallback) {
     const double v = fb_pre ? *fb_pre : fallback_one<D>(p, e);
@@ -590,15 +591,30 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
         if (p.special && !tile_fast(p, t0, G::TE)) {  // predicted outcomes (k_classify) of special / lost shards
           double v[KE], fb[KE];
           const int64_t e0 = t0 + tid * KE;
+          // the shard of each element: one division, then boundary compares
+          int64_t sk[KE];
+          int64_t sh = p.sp.bnd.shard_of(e0), nxt = p.sp.bnd.start(sh + 1);
           bool need_fb = false;
 #pragma unroll
           for (int k = 0; k < KE; ++k) {
-            const int64_t sh = p.sp.bnd.shard_of(e0 + k);
+            while (e0 + k >= nxt) nxt = p.sp.bnd.start(++sh + 1);
+            sk[k] = sh;
             need_fb |= p.sp.cls[sh] != kFast && (p.sp.pred[sh] & kPredMask) == kPredFallback;
           }
           if (need_fb) fallback_vec16<D>(p, e0, fb);
+          // the means of a special shard to the workspace in one vector store
+          const bool ws_vec = sk[0] == sk[KE - 1] && p.sp.cls[sk[0]] == kSpecial && KE % 2 == 0;
+          if (ws_vec) {
+            double* w = p.sp.ws + e0;
 #pragma unroll
-          for (int k = 0; k < KE; ++k) v[k] = final_value<D>(p, e0 + k, D::widen(acc[k]), need_fb ? fb + k : nullptr);
+            for (int k = 0; k + 1 < KE; k += 2)
+              asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(w + k), "d"(D::widen(acc[k])),
+                           "d"(D::widen(acc[k + 1]))
+                           : "memory");
+          }
+#pragma unroll
+          for (int k = 0; k < KE; ++k)
+            v[k] = final_value<D>(p, e0 + k, D::widen(acc[k]), need_fb ? fb + k : nullptr, sk[k], ws_vec);
           *reinterpret_cast<uint4*>(out + tid * 16) = pack16d<D>(v);
         } else {
           if (p.merged) {
