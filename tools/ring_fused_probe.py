@@ -25,7 +25,7 @@ from paper_2507_17766_b200 import _lib as L  # noqa: E402
 from paper_2507_17766_b200.device import DevicePlan  # noqa: E402
 from paper_2507_17766_b200.multigpu import ShardedButterflyMerge  # noqa: E402
 
-NAMES = ["ld.rep_empty", "ld.ready_flag", "ld.acc_empty", "-", "cmp.acc_full", "cmp.out_empty", "cmp.rep_full",
+NAMES = ["ld.rep_empty", "ld.schedule", "ld.ready_flag+acc_empty", "-", "cmp.acc_full", "cmp.out_empty", "cmp.rep_full",
          "total_cycles", "st.out_full", "st.free_flag", "st.read", "st.landed", "rl.ready_flag", "rl.rel_empty", "-",
          "-", "rs.rel_full", "rs.free_flag", "rs.read", "rs.landed", "t_start", "t_end", "-", "-"]
 
