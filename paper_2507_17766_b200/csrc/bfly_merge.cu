@@ -754,56 +754,41 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
     alive[k] = !p.failed[mem[k]];
     c[k] = p.corr[mem[k]];
   }
-  // the CTA scans kThreads tiles at a time and works through the ones k_reduce left
-  __shared__ int64_t todo[kThreads];
-  __shared__ int n_todo;
+  // the CTAs of a shard take its tiles in turn (blockIdx.y, stride gridDim.y) and
+  // skip the ones k_reduce already covered (done[]); one slot per tile, so the order of
+  // the work does not matter
   const int64_t t_first = start / p.stile, t_last = (hi_s - 1) / p.stile;
-  for (int64_t batch = t_first + (int64_t)blockIdx.y * kThreads; batch <= t_last;
-       batch += (int64_t)gridDim.y * kThreads) {
-    if (threadIdx.x == 0) n_todo = 0;
-    __syncthreads();
-    const int64_t tc = batch + threadIdx.x;
-    const bool need = tc <= t_last && !p.done[tc];
-    const unsigned ballot = __ballot_sync(0xffffffffu, need);
-    int base = 0;
-    if ((threadIdx.x & 31) == 0 && ballot) base = atomicAdd(&n_todo, __popc(ballot));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (need) todo[base + __popc(ballot & ((1u << (threadIdx.x & 31)) - 1))] = tc;
-    __syncthreads();
-    const int nt = n_todo;
-    for (int it = 0; it < nt; ++it) {
-      const int64_t t = todo[it];  // order within the batch is irrelevant: one slot per tile
-      const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
-      const int64_t g_lo = lo & ~(int64_t)7;
-      for (int a = 0; a < p.r; ++a)
-        for (int b = a + 1; b < p.r; ++b) {
-          if (!alive[a] || !alive[b]) continue;
-          PairStat st{0.0, 0.0, 0.0, 0.0};
-          for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
-            double m[8], x[8], y[8];
-            const unsigned valid = load_group(p.ws, e0, lo, hi, m);
-            corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
-            corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
-  #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              if (!((valid >> i) & 1)) continue;
-              st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
-              st.ab = fma(x[i], y[i], st.ab);
-              st.aa = fma(x[i], x[i], st.aa);
-              st.bb = fma(y[i], y[i], st.bb);
-            }
-          }
-          st = block_combine(st);
-          if (threadIdx.x == 0) {
-            double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
-            o[0] = st.mx;
-            o[1] = st.ab;
-            o[2] = st.aa;
-            o[3] = st.bb;
+  for (int64_t t = t_first + (int64_t)blockIdx.y; t <= t_last; t += (int64_t)gridDim.y) {
+    if (p.done[t]) continue;  // uniform across the CTA
+    const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
+    const int64_t g_lo = lo & ~(int64_t)7;
+    for (int a = 0; a < p.r; ++a)
+      for (int b = a + 1; b < p.r; ++b) {
+        if (!alive[a] || !alive[b]) continue;
+        PairStat st{0.0, 0.0, 0.0, 0.0};
+        for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
+          double m[8], x[8], y[8];
+          const unsigned valid = load_group(p.ws, e0, lo, hi, m);
+          corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
+          corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (!((valid >> i) & 1)) continue;
+            st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
+            st.ab = fma(x[i], y[i], st.ab);
+            st.aa = fma(x[i], x[i], st.aa);
+            st.bb = fma(y[i], y[i], st.bb);
           }
         }
-    }
-    __syncthreads();  // todo / n_todo are rewritten by the next batch
+        st = block_combine(st);
+        if (threadIdx.x == 0) {
+          double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
+          o[0] = st.mx;
+          o[1] = st.ab;
+          o[2] = st.aa;
+          o[3] = st.bb;
+        }
+      }
   }
 }
 
@@ -1226,8 +1211,10 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   if (do_finish) {
     const unsigned ns = (unsigned)p.n_fin;
     const int64_t tps = (p.bnd.base + (p.bnd.rem ? 1 : 0) + p.stile - 1) / p.stile + 1;  // tiles per shard
-    const int64_t nb = (tps + kThreads - 1) / kThreads;  // tile batches per shard
-    k_stats<<<dim3(ns, (unsigned)(nb < 65535 ? nb : 65535)), kThreads, 0, st>>>(p);
+    // up to 64 CTAs per shard: a shard whose tiles were not covered by k_reduce (the
+    // multi-GPU persistent ring computes no statistics) spreads over the GPU
+    const int64_t ny = tps < 64 ? tps : 64;
+    k_stats<<<dim3(ns, (unsigned)ny), kThreads, 0, st>>>(p);
     k_decide<<<ns, 32, 0, st>>>(p);
     if (p.r > 2) {
       const int64_t nn = (int64_t)p.n * p.n;
