@@ -1050,14 +1050,26 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   int64_t off_fin = 0, off_flags = 0, total = 0;
   int rc = bfly_ring_fused_layout(d->lanes, d->nb, d->dtype, &off_fin, &off_flags, &total);
   if (rc) return rc;
+  // every check before the first CUDA call
+  if (g == Z && d->special && !d->merge_args) return fail(BFLY_E_INVALID_ARG, "fused ring: special shards need merge_args");
+  if (G > kMaxG) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many ranks");
+  if ((int64_t)kSR < (int64_t)(G - 1) * (kNT + d->nb) + 1)
+    return fail(BFLY_E_UNSUPPORTED, "fused ring: schedule ring too short for this many ranks and slots");
+  int pub_every = 1, lag = 1;
+  if (const char* e = getenv("BFLY_RING_PUB_EVERY")) pub_every = atoi(e) > 0 ? atoi(e) : 1;
+  if (const char* e = getenv("BFLY_RING_LAG")) lag = atoi(e) < 1 ? 1 : (atoi(e) > kMaxLag ? kMaxLag : atoi(e));
+  // a step is visible at most lag + pub_every - 1 steps after it is stored; its producer
+  // must not need the credit of that step before then
+  if (pub_every > d->nb - lag) return fail(BFLY_E_INVALID_ARG, "fused ring: nb too small for the publication lag");
   cudaStream_t st = (cudaStream_t)stream;
   RingParams p{};
+  p.pub_every = pub_every;
+  p.lag = lag;
   if (g == Z && d->merge_args) {
     rc = ring_round_setup(d->merge_args, stream, &p.sp);
     if (rc) return rc;
     p.special = d->special != 0;
   }
-  if (p.special && !d->merge_args) return fail(BFLY_E_INVALID_ARG, "fused ring: special shards need merge_args");
   p.g = g;
   p.G = G;
   p.L = d->lanes;
@@ -1075,9 +1087,6 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.off_steps = align(off_flags + (int64_t)(kFAbort + 1) * p.L * 8);
   p.tile_ctr = reinterpret_cast<unsigned long long*>(p.my + align(p.off_steps + 2 * (int64_t)p.L * 8));
   p.off_sched = align(align(p.off_steps + 2 * (int64_t)p.L * 8) + 8);
-  if (G > kMaxG) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many ranks");
-  if ((int64_t)kSR < (int64_t)(G - 1) * (kNT + d->nb) + 1)
-    return fail(BFLY_E_UNSUPPORTED, "fused ring: schedule ring too short for this many ranks and slots");
   for (int r = 0; r < G; ++r) p.region[r] = region(r);
   if (g == 0) {  // the tiles of this round are dealt from 0 again
     cudaError_t e = cudaMemsetAsync(p.tile_ctr, 0, sizeof(unsigned long long), st);
@@ -1089,11 +1098,6 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.n_dst = d->n_dst;
   p.n_div = d->n_div;
   p.merged = g == Z ? d->d_merged : nullptr;
-  p.pub_every = 1;
-  if (const char* e = getenv("BFLY_RING_PUB_EVERY")) p.pub_every = atoi(e) > 0 ? atoi(e) : 1;
-  p.lag = 1;
-  if (const char* e = getenv("BFLY_RING_LAG")) p.lag = atoi(e) < 1 ? 1 : (atoi(e) > kMaxLag ? kMaxLag : atoi(e));
-  if (p.pub_every >= d->nb - p.lag) return fail(BFLY_E_INVALID_ARG, "fused ring: publication interval too long for nb");
   if (getenv("BFLY_RING_PROFILE")) {
     if (!g_prof || g_prof_n < p.L * kProfSlots) {
       if (g_prof) cudaFree(g_prof);

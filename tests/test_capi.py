@@ -158,3 +158,37 @@ def test_plan_metadata_and_helpers():
     assert plan.byte_bounds(1) == (16, 28)
     assert plan.metadata() == b"[[0, 0, 16], [1, 16, 12], [2, 28, 12]]"
     assert sorted(s for m in range(3) for s in plan.shards_of(m)) == [0, 0, 1, 1, 2, 2]
+
+
+def test_fused_ring_rejects_bad_descriptors():
+    """bfly_ring_fused validates its descriptor before any CUDA call (so this runs
+    without a GPU): ring size, slots, ranks beyond the schedule ring, a last rank
+    without an alive miner, special shards without the merge arguments."""
+    from paper_2507_17766_b200 import _lib, errors
+
+    lib = _lib.lib()
+    peers = (ctypes.c_uint64 * 17)(*[0x10000 * (r + 1) for r in range(17)])
+
+    def call(**kw):
+        d = _lib.RingFusedDesc()
+        d.rank, d.world, d.lanes, d.nb, d.dtype = 0, 2, 148, 10, _lib.F32
+        d.n_src = d.n_dst = 0
+        d.n_div = 4
+        d.payload_len = 1 << 20
+        d.peer_base = ctypes.cast(peers, ctypes.c_void_p)
+        for k, v in kw.items():
+            setattr(d, k, v)
+        _lib.check(lib.bfly_ring_fused(ctypes.byref(d), None))
+
+    with pytest.raises(errors.InvalidArgumentError):
+        call(world=1)
+    with pytest.raises(errors.InvalidArgumentError):
+        call(nb=1)
+    with pytest.raises(errors.InvalidArgumentError):
+        call(rank=1, n_div=0)  # the last rank divides by the alive miners
+    with pytest.raises(errors.InvalidArgumentError):
+        call(rank=1, special=1)  # special shards need the merge arguments
+    with pytest.raises(NotImplementedError):
+        call(world=17)
+    with pytest.raises(NotImplementedError):
+        call(world=8, nb=70)  # 7 x (8 + 70) + 1 > 512 schedule words per lane
