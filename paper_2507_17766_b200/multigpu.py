@@ -94,6 +94,19 @@ def classify_host(assign: np.ndarray, failures: set, corrupted: set, n_alive: in
     return cls, pred
 
 
+def mispredicted_shards(special_ids: np.ndarray, pred: np.ndarray, source: np.ndarray,
+                        corr_kind: np.ndarray) -> np.ndarray:
+    """The special / lost shards whose decision differs from k_classify's prediction, as
+    k_apply judges it (csrc/bfly_merge.cu): a fallback outcome is as predicted when the
+    prediction was the fallback, an adopted copy when the prediction was the mean and the
+    adopted assignee is honest.  The persistent ring re-broadcasts exactly these."""
+    pr = pred[special_ids]
+    src = source[special_ids]
+    honest_src = corr_kind[np.maximum(src, 0)] == 0
+    as_pred = np.where(src < 0, pr == PRED_FALLBACK, (pr == PRED_MEAN) & honest_src)
+    return special_ids[~as_pred]
+
+
 def pack_results(entries, source, status, flagged, out):
     """entries | source | status | flagged into one byte buffer (8-byte aligned parts first)."""
     parts = [entries.reshape(-1).view(torch.uint8), source.view(torch.uint8), status.view(torch.uint8),
@@ -687,13 +700,7 @@ class ShardedButterflyMerge:
         """Persistent ring: the relayed tiles of special / lost shards carried the predicted
         outcome; the shards FINISH decided otherwise (k_apply rewrote them on the last rank)
         are sent to the other ranks and scattered into their replicas."""
-        src = self.source.cpu().numpy()
-        ids = self._special_ids
-        pred = self._pred[ids]
-        srcs = src[ids]
-        honest_src = self._corr_kind[np.maximum(srcs, 0)] == 0
-        as_pred = np.where(srcs < 0, pred == PRED_FALLBACK, (pred == PRED_MEAN) & honest_src)
-        mis = ids[~as_pred]
+        mis = mispredicted_shards(self._special_ids, self._pred, self.source.cpu().numpy(), self._corr_kind)
         self.mispredicted = len(mis)
         if not len(mis):
             return

@@ -52,3 +52,31 @@ def test_classify_host_matches_oracle_decisions(seed):
             else:  # a lone corrupted survivor: adopted, so no prediction of the fallback
                 assert pred[s] == PRED_NONE and surv == [s_ for s_ in surv if s_ in bad] and len(surv) == 1
                 assert want["status"][s] == STATUS_MERGED
+
+
+def test_mispredicted_shards_are_the_unpredictable_ones():
+    """Colluders sharing a noise key agree, so their shard adopts a corrupted copy
+    although no majority was predicted; a lone corrupted survivor is adopted without a
+    prediction.  Exactly those shards are re-broadcast after the persistent ring."""
+    from paper_2507_17766_b200.multigpu import mispredicted_shards
+
+    n, P, seed = 9, 9 * 8 * 40, 5
+    rng = np.random.default_rng(3)
+    reps = [rng.uniform(-1, 1, P).astype(np.float32) for _ in range(n)]
+    fails = {0}
+    bad = {3, 4, 1}  # 3 and 4 collude (one key); 0 failed, so shards (0, 1/3/4) keep a lone corrupted survivor
+    specs = {3: (orc.NOISE, 2.0, 11, 11), 4: (orc.NOISE, 2.0, 11, 11), 1: (orc.NOISE, 2.0, 99, 1)}
+    assign, bounds = orc.plan(n, P, seed)
+    want = orc.merge(reps, assign, bounds, failures=tuple(fails), corruptions=specs, fallback=np.zeros(P))
+    cls, pred = classify_host(assign, fails, bad, n - len(fails))
+    kind = np.zeros(n, dtype=np.int32)
+    for m in bad:
+        kind[m] = 3
+    special = np.flatnonzero(cls != CLS_FAST)
+    mis = set(mispredicted_shards(special, pred, want["source"].astype(np.int64), kind).tolist())
+    expect = set()
+    for s in range(assign.shape[0]):
+        pair = {int(x) for x in assign[s]}
+        if pair == {3, 4} or (0 in pair and len(pair & bad) == 1):
+            expect.add(s)
+    assert mis == expect
