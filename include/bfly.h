@@ -65,6 +65,10 @@ typedef struct bfly_corruption {
 #define BFLY_PHASE_ALL 0       /* reduce + compare + decide + adopt/scatter-back */
 #define BFLY_PHASE_REDUCE 1    /* reduce only: means of every element -> d_merged/d_ws */
 #define BFLY_PHASE_FINISH 2    /* compare + decide + adopt, after PHASE_REDUCE and host copies */
+#define BFLY_PHASE_CHECK 3     /* only decide fast shards whose mean came out non-finite (after a
+                                  reduction that did not itself end at payload_len, e.g. the
+                                  multi-GPU persistent ring); PHASE_ALL / FINISH and a REDUCE of
+                                  the range ending at payload_len include it */
 
 typedef struct bfly_merge_args {
   int32_t n_miners;      /* N = plan.pair_set.n_miners                    (butterfly.py:188) */
@@ -109,7 +113,10 @@ typedef struct bfly_merge_args {
   const int32_t* d_shard_list;    /* FINISH these [n_shard_list] shards instead of the range
                                      (device array; e.g. shards straddling chunk edges) */
   int32_t n_shard_list;
-  int32_t pad3;
+  int32_t fallback_gone;          /* 1 = the fallback replica has been overwritten in place before
+                                     the shards decided after the reduction read it (multi-GPU
+                                     rounds: the relay); fast shards with non-finite means then
+                                     take d_fallback or NaN */
 } bfly_merge_args_t;
 
 /* ---- validator replay checks ---------------------- */
@@ -141,6 +148,12 @@ int bfly_philox_key(const char* seed_decimal, const char* stream_id, uint64_t ou
  * plan_shards  butterfly.py:84-114 (permutation simkernel.py:237-238). */
 int bfly_plan_host(int32_t n_miners, int32_t redundancy, int64_t payload_len, uint64_t key0,
                    uint64_t key1, int32_t* h_assign, int64_t* h_bounds);
+
+/* RngStream(seed, stream_id).permutation(n) on the host (simkernel.py:237-238):
+ * h_out[n] = Fisher-Yates from i = n-1 down to 1 with numpy's random_interval.
+ * plan_shards uses it for a caller-built PairSet: assignment[s] = pairs[h_out[s]]
+ * (butterfly.py:98-100). */
+int bfly_permutation_host(int64_t n, uint64_t key0, uint64_t key1, int64_t* h_out);
 
 /* Same plan computed on the device (GPU index map).  d_perm[S] receives the
  * shard -> combination-rank permutation; d_assign[S*r] the members. */
@@ -282,7 +295,12 @@ typedef struct bfly_ring_fused_desc {
   int32_t special;               /* last rank: some shard may be corrupted or lost — its
                                     tiles get k_classify's predicted outcome (and the means
                                     go to the workspace); FINISH runs after the kernel  */
+  int32_t pub_every;             /* publish a lane's ready flag every pub_every-th step (0 = 1) */
+  int32_t lag;                   /* ... once the step is lag steps old (1..3; 0 = 1); needs
+                                    nb >= lag + pub_every                              */
   int32_t pad;
+  unsigned long long* d_profile; /* diagnostics, or NULL: [lanes * 24] per-CTA wait cycles
+                                    per role, CTA start / end times (globaltimer), SM id */
 } bfly_ring_fused_desc_t;
 /* Lanes this device runs (all CTAs co-resident: cooperative launch). */
 int32_t bfly_ring_fused_lanes(int32_t dtype);
@@ -291,9 +309,13 @@ int32_t bfly_ring_fused_lanes(int32_t dtype);
 int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* off_fin, int64_t* off_flags,
                            int64_t* total);
 int bfly_ring_fused(const bfly_ring_fused_desc_t* desc, void* stream);
-/* Diagnostics: with BFLY_RING_PROFILE set, per CTA 24 counters of the last k_ring
- * launch (cycles spent in each wait, per role); copies n of them, returns the count. */
-int bfly_ring_fused_profile(unsigned long long* host_out, int32_t n);
+/* Single-device loopback: `world` ranks of one ring on THIS device, in one cooperative
+ * launch of world x lanes CTAs (CTA c serves lane c % lanes of rank c / lanes).  descs[g]
+ * is rank g's descriptor exactly as bfly_ring_fused takes it, with the regions being
+ * plain allocations of this device (peer_base[r] = rank r's region).  The same kernel
+ * code, protocol and results as the multi-GPU ring — driver-testable and profileable
+ * (ncu) on one GPU.  world <= 8. */
+int bfly_ring_fused_loopback(const bfly_ring_fused_desc_t* descs, int32_t world, void* stream);
 
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);

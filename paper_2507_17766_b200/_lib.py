@@ -19,19 +19,20 @@ F32, BF16, F64WIRE = 0, 1, 2
 MERGED, LOST, DISAGREEMENT = 0, 1, 2
 STATUS_NAMES = ("merged", "lost", "disagreement")
 CORR_NONE, CORR_ADD, CORR_SCALE, CORR_NOISE, CORR_NOISE_ADD, CORR_HOST = 0, 1, 2, 3, 4, 5
-PHASE_ALL, PHASE_REDUCE, PHASE_FINISH = 0, 1, 2
+PHASE_ALL, PHASE_REDUCE, PHASE_FINISH, PHASE_CHECK = 0, 1, 2, 3
 
 # every symbol include/bfly.h declares (tests/test_capi.py checks the export table)
 EXPORTS = (
     "bfly_ring_fused",
     "bfly_ring_fused_lanes",
     "bfly_ring_fused_layout",
-    "bfly_ring_fused_profile",
+    "bfly_ring_fused_loopback",
     "bfly_version",
     "bfly_last_error",
     "bfly_n_shards",
     "bfly_philox_key",
     "bfly_plan_host",
+    "bfly_permutation_host",
     "bfly_plan_device",
     "bfly_merge_scratch_bytes",
     "bfly_merge",
@@ -107,7 +108,7 @@ class MergeArgs(ctypes.Structure):
         ("shard_end", ctypes.c_int64),
         ("d_shard_list", ctypes.c_void_p),
         ("n_shard_list", ctypes.c_int32),
-        ("pad3", ctypes.c_int32),
+        ("fallback_gone", ctypes.c_int32),
     ]
 
 
@@ -160,7 +161,10 @@ class RingFusedDesc(ctypes.Structure):
         ("d_merged", ctypes.c_void_p),
         ("merge_args", ctypes.POINTER(MergeArgs)),
         ("special", ctypes.c_int32),
+        ("pub_every", ctypes.c_int32),
+        ("lag", ctypes.c_int32),
         ("pad", ctypes.c_int32),
+        ("d_profile", ctypes.c_void_p),
     ]
 
 
@@ -183,6 +187,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_n_shards.restype = i64
     L.bfly_philox_key.argtypes = [ctypes.c_char_p, ctypes.c_char_p, vp]
     L.bfly_plan_host.argtypes = [i32, i32, i64, u64, u64, vp, vp]
+    L.bfly_permutation_host.argtypes = [i64, u64, u64, vp]
     L.bfly_plan_device.argtypes = [i32, i32, i64, u64, u64, vp, vp, vp]
     L.bfly_merge_scratch_bytes.argtypes = [i32, i32, i64]
     L.bfly_merge_scratch_bytes.restype = sz
@@ -213,7 +218,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_ring_fused_lanes.restype = i32
     L.bfly_ring_fused_layout.argtypes = [i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.bfly_ring_fused.argtypes = [ctypes.POINTER(RingFusedDesc), vp]
-    L.bfly_ring_fused_profile.argtypes = [vp, i32]
+    L.bfly_ring_fused_loopback.argtypes = [vp, i32, vp]
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)
     _lib = L

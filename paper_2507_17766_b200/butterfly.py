@@ -20,9 +20,9 @@ There is no CPU fallback: without a CUDA device these functions raise.
 from __future__ import annotations
 
 import ctypes
-import os
 import json
 import math
+import sys
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -52,52 +52,82 @@ __all__ = [
 BYTES_PER_WEIGHT = 4  # the wire format is "<f4" (butterfly.py:37)
 
 
-@dataclass(frozen=True)
-class PairSet:
-    n_miners: int
-    pairs: tuple  # (i, j), i < j, lexicographic
+def _reference_types():
+    """The caller's iota_sim.butterfly result types, when that package is importable:
+    the drop-in then returns the reference's own PairSet / ShardPlan / AgreementMatrix /
+    MergeResult (isinstance checks and equality in callers keep working)."""
+    mod = sys.modules.get("iota_sim.butterfly")
+    if mod is None or mod.__name__ == __name__:
+        try:
+            import iota_sim.butterfly as mod  # noqa: F811
+        except Exception:
+            return None
+    names = ("PairSet", "ShardPlan", "AgreementMatrix", "MergeResult")
+    if getattr(mod, "__name__", None) == __name__ or not all(hasattr(mod, n) for n in names):
+        return None
+    return mod
 
 
-@dataclass(frozen=True)
-class ShardPlan:
-    """Shard -> miner-pair bijection and element bounds (butterfly.py:46-73)."""
+_ref_types = _reference_types()
 
-    pair_set: PairSet
-    assignment: tuple
-    bounds: tuple
-    bytes_per_weight: int
-    seed: int
+if _ref_types is not None:
+    PairSet = _ref_types.PairSet
+    ShardPlan = _ref_types.ShardPlan
+    AgreementMatrix = _ref_types.AgreementMatrix
+    MergeResult = _ref_types.MergeResult
+else:
+    @dataclass(frozen=True)
+    class PairSet:
+        n_miners: int
+        pairs: tuple  # (i, j), i < j, lexicographic
 
-    @property
-    def n_shards(self) -> int:
-        return len(self.assignment)
+    @dataclass(frozen=True)
+    class ShardPlan:
+        """Shard -> miner-pair bijection and element bounds (butterfly.py:46-73)."""
 
-    def byte_bounds(self, shard_idx: int) -> tuple[int, int]:
-        lo, hi = self.bounds[shard_idx]
-        return lo * self.bytes_per_weight, hi * self.bytes_per_weight
+        pair_set: PairSet
+        assignment: tuple
+        bounds: tuple
+        bytes_per_weight: int
+        seed: int
 
-    def shards_of(self, miner: int) -> list[int]:
-        return [s for s, members in enumerate(self.assignment) if miner in members]
+        @property
+        def n_shards(self) -> int:
+            return len(self.assignment)
 
-    def metadata(self) -> bytes:
-        """JSON sidecar [[shard, start_byte, length_bytes], ...] (butterfly.py:67-73)."""
-        rows = [[s, lo * self.bytes_per_weight, (hi - lo) * self.bytes_per_weight]
-                for s, (lo, hi) in enumerate(self.bounds)]
-        return json.dumps(rows).encode()
+        def byte_bounds(self, shard_idx: int) -> tuple[int, int]:
+            lo, hi = self.bounds[shard_idx]
+            return lo * self.bytes_per_weight, hi * self.bytes_per_weight
+
+        def shards_of(self, miner: int) -> list[int]:
+            return [s for s, members in enumerate(self.assignment) if miner in members]
+
+        def metadata(self) -> bytes:
+            """JSON sidecar [[shard, start_byte, length_bytes], ...] (butterfly.py:67-73)."""
+            rows = [[s, lo * self.bytes_per_weight, (hi - lo) * self.bytes_per_weight]
+                    for s, (lo, hi) in enumerate(self.bounds)]
+            return json.dumps(rows).encode()
+
+    @dataclass(frozen=True)
+    class AgreementMatrix:
+        n_miners: int
+        entries: np.ndarray
+
+    @dataclass
+    class MergeResult:
+        merged: np.ndarray
+        shard_status: list
+        agreement_matrix: AgreementMatrix
+        flagged: set = field(default_factory=set)
 
 
-@dataclass(frozen=True)
-class AgreementMatrix:
-    n_miners: int
-    entries: np.ndarray
-
-
-@dataclass
-class MergeResult:
-    merged: np.ndarray
-    shard_status: list
-    agreement_matrix: AgreementMatrix
-    flagged: set = field(default_factory=set)
+def _types_of(obj):
+    """(ShardPlan, AgreementMatrix, MergeResult) of the module that defined ``obj``'s
+    type (the caller's plan or pair set), else this module's."""
+    mod = sys.modules.get(type(obj).__module__)
+    if mod is not None and all(hasattr(mod, n) for n in ("ShardPlan", "AgreementMatrix", "MergeResult")):
+        return mod.ShardPlan, mod.AgreementMatrix, mod.MergeResult
+    return ShardPlan, AgreementMatrix, MergeResult
 
 
 def enumerate_pairs(n: int) -> PairSet:
@@ -105,6 +135,13 @@ def enumerate_pairs(n: int) -> PairSet:
     if n < 2:
         raise TooFewMinersError(f"need at least 2 miners, got {n}")
     return PairSet(n_miners=n, pairs=tuple((i, j) for i in range(n) for j in range(i + 1, n)))
+
+
+def _is_mean_reducer(reducer) -> bool:
+    """This module's mean_reducer or the reference's (butterfly.py:156-158): the only
+    reducer the device merge implements."""
+    return reducer is mean_reducer or (getattr(reducer, "__name__", "") == "mean_reducer"
+                                       and getattr(reducer, "__module__", "") == "iota_sim.butterfly")
 
 
 def _host_plan(n: int, r: int, payload_len: int, seed: int):
@@ -116,15 +153,44 @@ def _host_plan(n: int, r: int, payload_len: int, seed: int):
     return assign[:S], bounds
 
 
+def _lexicographic_pairs(pairs, n: int) -> bool:
+    if len(pairs) != n * (n - 1) // 2:
+        return False
+    k = 0
+    for i in range(n):
+        for j in range(i + 1, n):
+            if tuple(pairs[k]) != (i, j):
+                return False
+            k += 1
+    return True
+
+
 def plan_shards(pair_set: PairSet, payload_len: int, bytes_per_weight: int, seed: int) -> ShardPlan:
-    """Seeded shard -> pair bijection with near-equal bounds (butterfly.py:84-114)."""
+    """Seeded shard -> pair bijection with near-equal bounds (butterfly.py:84-114).
+
+    The pairs of ``enumerate_pairs`` go through the native index map (bfly_plan_host,
+    the same code as the GPU's k_plan); any other PairSet is permuted as the reference
+    does, ``pairs[order[s]]`` with ``order = RngStream(seed, "shard-plan").permutation``
+    (bfly_permutation_host).  The plan is an instance of the pair set's module's
+    ShardPlan (the reference's when the caller passes its own PairSet)."""
     n_shards = len(pair_set.pairs)
     if payload_len < n_shards:
         raise DegenerateShardsError(f"payload of {payload_len} elements cannot fill {n_shards} shards")
-    assign, bounds = _host_plan(pair_set.n_miners, 2, payload_len, seed)
+    plan_type = _types_of(pair_set)[0]
+    if _lexicographic_pairs(pair_set.pairs, pair_set.n_miners):
+        assign, bounds = _host_plan(pair_set.n_miners, 2, payload_len, seed)
+        assignment = tuple(tuple(p) for p in assign.tolist())
+    else:
+        order = np.empty(max(n_shards, 1), dtype=np.int64)
+        k0, k1 = L.philox_key(seed, "shard-plan")
+        L.check(L.lib().bfly_permutation_host(n_shards, k0, k1, order.ctypes.data))
+        assignment = tuple(pair_set.pairs[k] for k in order[:n_shards].tolist())
+        base, rem = divmod(payload_len, n_shards)
+        idx = np.arange(n_shards + 1, dtype=np.int64)
+        bounds = idx * base + np.minimum(idx, rem)
     b = bounds.tolist()
-    return ShardPlan(pair_set=pair_set, assignment=tuple(tuple(p) for p in assign.tolist()),
-                     bounds=tuple(zip(b[:-1], b[1:])), bytes_per_weight=bytes_per_weight, seed=seed)
+    return plan_type(pair_set=pair_set, assignment=assignment, bounds=tuple(zip(b[:-1], b[1:])),
+                     bytes_per_weight=bytes_per_weight, seed=seed)
 
 
 def _to_device_f64(x, dev) -> torch.Tensor:
@@ -169,13 +235,28 @@ def mean_reducer(stack):
 # ---------------------------------------------------------------------------
 
 
+SNAPSHOT_STORE = False
+"""Ownership of the store objects a round writes.
+
+False (default): the weights objects are views of the caller's payload arrays and the
+re-uploaded reductions of merged shards are views of the returned ``merged`` vector,
+rendered as "<f4" bytes when first read (a ranged ``get`` converts only its range).
+Changing a payload in place after the call therefore changes what the store returns.
+Reductions that differ from ``merged`` (corrupted copies, shards whose mean is not
+finite) are rendered into host bytes before the call returns; no object keeps device
+memory of the round alive.
+
+True: every object is snapshotted into bytes before the call returns, as the
+reference's ``BlobStore.put`` copies them (simkernel.py:168) — at the reference's host
+cost (N x 4P bytes per round)."""
+
+
 class _LazyBlob:
     """Store object whose bytes are produced on first read (sizes are exact up front).
 
-    Objects of the merge are views of device-resident vectors in the "<f4" wire format:
-    a ranged read (``blob[a:b]``, what ``BlobStore.get(actor, key, start, length)``
-    does) copies only those elements back when a ``part`` reader is given; anything
-    else materialises the whole object once."""
+    A ranged read (``blob[a:b]``, what ``BlobStore.get(actor, key, start, length)``
+    does) renders only that range when a ``part`` reader is given; anything else
+    materialises the whole object once."""
 
     __slots__ = ("_n", "_make", "_data", "_part")
 
@@ -206,23 +287,31 @@ class _LazyBlob:
     __hash__ = None
 
 
-def _wire_part(values, header: bytes = b""):
-    """Ranged reader of ``header + values.astype("<f4")`` for a 1-D float vector
-    (device tensor or numpy): only the elements under [start, stop) are copied."""
-    h = len(header)
+def _wire_part(values):
+    """Ranged reader of ``values.astype("<f4")`` for a 1-D float vector (numpy or a
+    tensor): only the elements under [start, stop) are converted."""
 
     def part(start: int, stop: int) -> bytes:
-        out = header[start:stop] if start < h else b""
-        a, b = max(start, h) - h, stop - h
-        if b > a:
-            e0, e1 = a // 4, (b + 3) // 4
-            chunk = values[e0:e1]
-            if isinstance(chunk, torch.Tensor):
-                chunk = chunk.detach().to("cpu", torch.float64).numpy()
-            raw = np.asarray(chunk, dtype=np.float64).astype("<f4").tobytes()
-            out += raw[a - 4 * e0:b - 4 * e0]
-        return out
+        e0, e1 = start // 4, (stop + 3) // 4
+        chunk = values[e0:e1]
+        if isinstance(chunk, torch.Tensor):
+            chunk = chunk.detach().to("cpu", torch.float64).numpy()
+        raw = np.asarray(chunk, dtype=np.float64).astype("<f4").tobytes()
+        return raw[start - 4 * e0:stop - 4 * e0]
     return part
+
+
+def _wire_bytes(src) -> bytes:
+    if isinstance(src, torch.Tensor):
+        return src.detach().to("cpu", torch.float64).numpy().astype("<f4").tobytes()
+    return np.asarray(src, dtype=np.float64).astype("<f4").tobytes()
+
+
+def _wire_blob(values, nbytes: int):
+    """Store object holding ``values.astype("<f4")`` (a view unless SNAPSHOT_STORE)."""
+    if SNAPSHOT_STORE:
+        return _wire_bytes(values)
+    return _LazyBlob(nbytes, lambda: _wire_bytes(values), _wire_part(values))
 
 
 def _meter(store, actor: str) -> object:
@@ -250,6 +339,73 @@ def _payload_to_device(x, dev) -> tuple[torch.Tensor, int]:
     return torch.from_numpy(a).to(dev, non_blocking=True), len(a)
 
 
+def _runs(ranges):
+    """Merge sorted [lo, hi) element ranges into maximal runs."""
+    out = []
+    for lo, hi in ranges:
+        if out and out[-1][1] == lo:
+            out[-1][1] = hi
+        else:
+            out.append([lo, hi])
+    return out
+
+
+def _classes(plan, failed: set, corrupted: set):
+    """Per shard: "fast" (>= 1 survivor, none corrupted), "special" (a corrupted
+    survivor) or "lost" (no survivor) — k_classify's classes."""
+    out = []
+    for members in plan.assignment:
+        surv = [x for x in members if x not in failed]
+        out.append("lost" if not surv else "special" if any(x in corrupted for x in surv) else "fast")
+    return out
+
+
+def _host_copies(job, plan, failed, callables, dev):
+    """The reference's reduce-stage calls of the corruption callables (butterfly.py:219-233):
+    shard ascending, assignee i then j, each on a fresh copy of the shard's fp64 mean.
+    Only the special shards' means come back from the device and only their copies go
+    up (one D2H / H2D per run of adjacent shards).  Returns ({(shard, assignee): output},
+    device [2, P] copies)."""
+    P = job.P
+    host_reductions = {}
+    copies = torch.zeros((2, P), dtype=torch.float64, device=dev)
+    todo = [s for s, members in enumerate(plan.assignment)
+            if any(x not in failed and x in callables for x in members)]
+    runs = _runs([plan.bounds[s] for s in todo])
+    means = {}
+    for lo, hi in runs:  # one D2H per run of adjacent special shards
+        means[lo] = job.means[lo:hi].cpu().numpy()
+    run_of = {}
+    for lo, hi in runs:
+        for s in todo:
+            a, b = plan.bounds[s]
+            if lo <= a and b <= hi:
+                run_of[s] = lo
+    staged = {lo: np.zeros((2, hi - lo), dtype=np.float64) for lo, hi in runs}
+    for s in todo:
+        lo, hi = plan.bounds[s]
+        r0 = run_of[s]
+        mean = means[r0][lo - r0:hi - r0]
+        members = plan.assignment[s]
+        outs = {}
+        for slot, x in enumerate(members):
+            if x in failed or x not in callables:
+                continue
+            out = callables[x](mean.copy())
+            host_reductions[(s, x)] = out
+            outs[slot] = np.asarray(out, dtype=np.float64)
+        surv = [slot for slot, x in enumerate(members) if x not in failed]
+        shapes = {slot: (outs[slot].shape if slot in outs else (hi - lo,)) for slot in surv}
+        if len(surv) == 2 and shapes[surv[0]] != shapes[surv[1]]:  # agreement(), butterfly.py:125-126
+            raise ShapeError(f"reduction shapes differ: {shapes[surv[0]]} vs {shapes[surv[1]]}")
+        for slot, arr in outs.items():
+            # a broadcastable copy (a scalar, shape (1,)) merges as numpy assigns it (:263)
+            staged[r0][slot, lo - r0:hi - r0] = np.broadcast_to(arr, (hi - lo,))
+    for lo, hi in runs:  # one H2D per run
+        copies[:, lo:hi].copy_(torch.from_numpy(staged[lo]))
+    return host_reductions, copies
+
+
 def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reducer,
                    failures: frozenset | set = frozenset(), corruptions: dict | None = None,
                    fallback: np.ndarray | None = None, key_prefix: str = "merge",
@@ -260,9 +416,10 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     the device are accepted too).  ``failures`` / ``corruptions`` are keyed by
     index into sorted(payloads).  A corruption may be a reference-style callable
     fn(reduction) -> reduction (run on the host, in the reference's call order)
-    or a ``Corruption`` descriptor (applied inside the kernels).
+    or a ``Corruption`` descriptor (applied inside the kernels).  Returns the
+    MergeResult type of the plan's module (the reference's for its own plans).
     """
-    if reducer is not mean_reducer:
+    if not _is_mean_reducer(reducer):
         raise NotImplementedError("custom reducers cannot cross the C ABI; only mean_reducer is supported")
     corruptions = corruptions or {}
     n = plan.pair_set.n_miners
@@ -278,6 +435,7 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     if fallback is not None and len(fallback) != P:
         raise ShapeError("fallback length does not match payloads")
     dev = _require_cuda()
+    _, agreement_type, result_type = _types_of(plan)
     failed = set(int(m) for m in failures if 0 <= int(m) < n)
     alive = [m for m in range(n) if m not in failed]
     bpw = plan.bytes_per_weight
@@ -288,6 +446,7 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     # -- device merge ------------------------------------------------------
     reps = [None] * n
     pipelined = False
+    hosts = None
     host_f64 = [m for m in alive if not isinstance(payloads[miners[m]], torch.Tensor)]
     if host_f64 and len(host_f64) == len(alive):
         # host payloads: the upload stage's "<f4" serialisation (butterfly.py:213) runs on
@@ -322,27 +481,12 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
                          fallback=fb, scatter_back=False, want_merged=True, keep_means=True,
                          tolerance=agreement_tolerance)
 
-    host_reductions = {}  # (shard, assignee) -> callable output (fp64 host)
+    host_reductions = {}  # (shard, assignee) -> callable output
+    early = False
     if callables:
         job.run(L.PHASE_REDUCE)
-        means = job.means.cpu().numpy()
-        host_copies = np.zeros((2, P), dtype=np.float64)
-        for s, (i, j) in enumerate(plan.assignment):  # reference order: butterfly.py:219-233
-            lo, hi = plan.bounds[s]
-            for slot, x in enumerate((i, j)):
-                if x in failed or x not in callables:
-                    continue
-                out = callables[x](means[lo:hi].copy())
-                host_reductions[(s, x)] = out
-                arr = np.asarray(out, dtype=np.float64)
-                if arr.shape == (hi - lo,):
-                    host_copies[slot, lo:hi] = arr
-                else:
-                    other = j if x == i else i
-                    if other not in failed:
-                        raise ShapeError(f"reduction shapes differ: {arr.shape} vs {(hi - lo,)}")
-                    raise ValueError(f"could not broadcast reduction of shape {arr.shape} into ({hi - lo},)")
-        job.run(L.PHASE_FINISH, host_copies=torch.from_numpy(host_copies).to(dev))
+        host_reductions, copies = _host_copies(job, plan, failed, callables, dev)
+        job.run(L.PHASE_FINISH, host_copies=copies)
     elif pipelined:
         # merged values stream back chunk by chunk unless FINISH may still change them
         early = not _device_merged and not job.needs_finish()
@@ -355,37 +499,103 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     else:
         job.run(L.PHASE_ALL)
 
+    status_codes = job.status.cpu().numpy()
+    corrupted = set(descriptors) | set(callables)
+    classes = _classes(plan, failed, corrupted)
+    # fast shards whose mean is NaN / Inf somewhere: both (identical) copies score NaN
+    # (butterfly.py:127-133), so the shard falls back (:264-273) — from the fp64 payload
+    # of the lowest alive miner when no fallback was given
+    nonfinite = [s for s, c in enumerate(classes) if c == "fast" and status_codes[s] != L.MERGED]
+    nonfinite_means = {}
+    if nonfinite:
+        nonfinite_means = _nonfinite_means(plan, reps, alive, nonfinite)
+        if fb is None and alive:
+            src = payloads[miners[alive[0]]]
+            job.set_fallback(_to_device_f64(src if hosts is None else hosts[0], dev))
+            job.run(L.PHASE_CHECK)
+            early = False  # merged changed after the streamed copy: copy it again
+
     if _device_merged:  # stage glue (stage.py): the merged weights stay in HBM
         merged = job.merged
     else:
-        if not (pipelined and early):
+        if not early:
             merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True)  # cached pinned block
             merged_host.copy_(job.merged, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
         merged = merged_host.numpy()  # the array keeps the pinned tensor alive
-    status_codes = job.status.cpu().numpy()
     entries = job.entries.cpu().numpy()
     flagged_idx = np.flatnonzero(job.flagged.cpu().numpy())
     sources = job.source.cpu().numpy()
 
+    # reductions that differ from merged: corrupted copies (device descriptors) and the
+    # means of non-finite shards, rendered to host "<f4" bytes now (no device memory of
+    # this round stays referenced once the call returns)
+    rendered = _render_special(job, plan, failed, descriptors, classes, host_reductions, nonfinite_means)
+    del job, reps
     # -- blob store: objects + closed-form meter (butterfly.py:205-288) -----
-    special = [any(x not in failed and (x in descriptors or x in callables) for x in members)
-               for members in plan.assignment]
     _account_store(store, plan, miners, payloads, alive, failed, key_prefix, bpw, merged, status_codes, sources,
-                   job, descriptors, host_reductions, special)
+                   host_reductions, rendered)
 
-    return MergeResult(
+    return result_type(
         merged=merged,
         shard_status=[L.STATUS_NAMES[c] for c in status_codes],
-        agreement_matrix=AgreementMatrix(n_miners=n, entries=entries),
+        agreement_matrix=agreement_type(n_miners=n, entries=entries),
         flagged={miners[i] for i in flagged_idx},
     )
 
 
+def _nonfinite_means(plan, reps, alive, shards) -> dict:
+    """fp64 means of the given shards (mean_reducer's order, butterfly.py:156-158) from
+    the device replicas, which the drop-in never overwrites: shard -> host array."""
+    out = {}
+    for s in shards:
+        lo, hi = plan.bounds[s]
+        stack = torch.stack([reps[m][lo:hi].to(torch.float64) for m in alive])
+        out[s] = mean_reducer(stack).cpu().numpy()
+    return out
+
+
+def _render_special(job, plan, failed, descriptors, classes, host_reductions, nonfinite_means) -> dict:
+    """(shard, assignee) -> "<f4" bytes of the re-uploaded reductions that are not the
+    merged values (butterfly.py:235-240): every survivor of a special shard (honest ones
+    carry the mean, descriptor-corrupted ones their copy), and both survivors of a
+    non-finite shard.  Callable outputs are kept as returned."""
+    items = []
+    for s, members in enumerate(plan.assignment):
+        if classes[s] == "fast" and s not in nonfinite_means:
+            continue
+        if classes[s] == "lost":
+            continue
+        lo, hi = plan.bounds[s]
+        for x in members:
+            if x in failed or (s, x) in host_reductions:
+                continue
+            items.append((s, x, lo, hi))
+    if not items:
+        return {}
+    parts = []
+    for s, x, lo, hi in items:
+        if s in nonfinite_means:
+            parts.append(torch.from_numpy(nonfinite_means[s]).to(torch.float32))
+            continue
+        mean = job.means[lo:hi]
+        if x in descriptors:
+            out = torch.empty_like(mean)
+            L.check(L.lib().bfly_apply_corruption(descriptors[x].struct(), mean.data_ptr(), lo, hi - lo,
+                                                  out.data_ptr(), _stream_handle()))
+            mean = out
+        parts.append(mean.to(torch.float32))
+    flat = torch.cat([p.to(parts[0].device) if p.device != parts[0].device else p for p in parts]).cpu().numpy()
+    out, o = {}, 0
+    for s, x, lo, hi in items:
+        out[(s, x)] = flat[o:o + hi - lo].astype("<f4").tobytes()
+        o += hi - lo
+    return out
+
+
 def _merge_chunks(P: int) -> int:
-    """Pipeline depth of bfly_merge_host: chunks of >= 4M elements, at most 32
-    (BFLY_MERGE_CHUNKS overrides)."""
-    forced = os.environ.get("BFLY_MERGE_CHUNKS")
-    return int(forced) if forced else max(1, min(32, P >> 22))
+    """Pipeline depth of bfly_merge_host: chunks of >= 4M elements, at most 32."""
+    return max(1, min(32, P >> 22))
 
 
 def _chunk(size: int, start: int, length: int | None) -> int:
@@ -395,21 +605,18 @@ def _chunk(size: int, start: int, length: int | None) -> int:
 
 
 def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, merged, status_codes, sources,
-                   job, descriptors, host_reductions, special):
+                   host_reductions, rendered):
     objects = store.objects
     meta = plan.metadata()
     objects[f"{prefix}/shard-metadata"] = meta
     _meter(store, "orchestrator").bytes_uploaded += _wire(store, len(meta))
     P = len(merged)
     n_alive = len(alive)
-    weight_keys = {}
     wsize = 4 * P  # weights always travel as "<f4" (butterfly.py:213)
     for m in alive:  # upload stage
         key = f"{prefix}/miner/{miners[m]}/weights"
-        src = payloads[miners[m]]
-        objects[key] = _LazyBlob(wsize, lambda src=src: _wire_bytes(src), _wire_part(src))
+        objects[key] = _wire_blob(payloads[miners[m]], wsize)
         _meter(store, str(miners[m])).bytes_uploaded += _wire(store, wsize)
-        weight_keys[m] = key
     for s, (i, j) in enumerate(plan.assignment):  # reduce stage
         lo, hi = plan.bounds[s]
         for x in (i, j):
@@ -419,13 +626,13 @@ def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, me
             mt.bytes_downloaded += n_alive * _wire(store, _chunk(wsize, lo * bpw, (hi - lo) * bpw))
             if (s, x) in host_reductions:
                 red = np.asarray(host_reductions[(s, x)])
-                nbytes = 4 * red.size
-                make, part = (lambda red=red: red.astype("<f4").tobytes()), None
-            else:
-                nbytes = 4 * (hi - lo)
-                make, part = _reduction_maker(job, x, lo, hi, merged, special[s], descriptors)
-            objects[f"{prefix}/miner/{miners[x]}/merged/{s}"] = _LazyBlob(nbytes, make, part)
-            mt.bytes_uploaded += _wire(store, nbytes)
+                blob = red.astype("<f4").tobytes()
+            elif (s, x) in rendered:
+                blob = rendered[(s, x)]
+            else:  # every survivor of a merged fast shard re-uploaded the merged mean
+                blob = _wire_blob(merged[lo:hi], 4 * (hi - lo))
+            objects[f"{prefix}/miner/{miners[x]}/merged/{s}"] = blob
+            mt.bytes_uploaded += _wire(store, len(blob))
     for m in alive:  # redistribution stage (metering only)
         mt = _meter(store, str(miners[m]))
         down = 0
@@ -437,37 +644,6 @@ def _account_store(store, plan, miners, payloads, alive, failed, prefix, bpw, me
             else:
                 down += _wire(store, _chunk(wsize, lo * bpw, (hi - lo) * bpw))
         mt.bytes_downloaded += down
-
-
-def _host(x) -> np.ndarray:
-    return x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
-
-
-def _wire_bytes(src) -> bytes:
-    if isinstance(src, torch.Tensor):
-        return src.detach().to("cpu", torch.float64).numpy().astype("<f4").tobytes()
-    return np.asarray(src, dtype=np.float64).astype("<f4").tobytes()
-
-
-def _reduction_maker(job, x, lo, hi, merged, special, descriptors):
-    """(whole, ranged) readers of assignee x's re-uploaded reduction ("<f4",
-    butterfly.py:235-240)."""
-    if not special:  # all survivors honest: every reduction equals the merged mean
-        return (lambda: _host(merged[lo:hi]).astype("<f4").tobytes()), _wire_part(merged[lo:hi])
-
-    class _Copy:  # element range of the assignee's copy, computed on the device on demand
-        def __getitem__(self, sl):
-            a, b = lo + sl.start, lo + min(sl.stop, hi - lo)
-            mean = job.means[a:b]
-            if x in descriptors:
-                out = torch.empty_like(mean)
-                L.check(L.lib().bfly_apply_corruption(descriptors[x].struct(), mean.data_ptr(), a, b - a,
-                                                      out.data_ptr(), _stream_handle()))
-                mean = out
-            return mean
-
-    copy = _Copy()
-    return (lambda: _host(copy[0:hi - lo]).astype("<f4").tobytes()), _wire_part(copy)
 
 
 # ---------------------------------------------------------------------------

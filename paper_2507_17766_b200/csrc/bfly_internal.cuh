@@ -43,7 +43,8 @@ struct ScratchLayout {
   int64_t S = 0, cps = 0;
   int npairs = 0;
   int64_t ntiles = 0;  // statistics tiles of the smallest size
-  size_t off_cls = 0, off_pred = 0, off_done = 0, off_source = 0, off_stats = 0, off_scores = 0, off_has = 0, off_inv = 0;
+  size_t off_cls = 0, off_pred = 0, off_done = 0, off_source = 0, off_stats = 0, off_scores = 0, off_has = 0, off_inv = 0,
+         off_nonfin = 0;
   size_t total = 0;
   void init(int32_t n, int32_t r, int64_t P) {
     S = binom(n, r);
@@ -73,6 +74,9 @@ struct ScratchLayout {
     o = align(o + (size_t)S * (size_t)npairs);
     off_inv = o;
     o = align(o + sizeof(int32_t) * (size_t)S);
+    // non-finite means of fast shards: a u32 "any" word, then one byte per shard
+    off_nonfin = o;
+    o = align(o + 4 + (size_t)S);
     total = o;
   }
 };
@@ -87,7 +91,14 @@ struct RingSpecial {
   const double* fallback = nullptr;
   const void* fb_src = nullptr;   // replica supplying fallback values
   bool merged_apart = false;      // merged is not the workspace
+  uint32_t* nonfin_any = nullptr; // some fast shard's mean is not finite (then nonfin[s] = 1)
+  uint8_t* nonfin = nullptr;
 };
+
+// An IEEE double that is neither NaN nor +-Inf (exponent field not all ones).
+__device__ __forceinline__ bool finite64(double x) {
+  return (__double_as_longlong(x) & 0x7ff0000000000000LL) != 0x7ff0000000000000LL;
+}
 int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out);
 
 }  // namespace bfly

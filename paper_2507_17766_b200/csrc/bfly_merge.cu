@@ -65,7 +65,19 @@ struct Params {
   int64_t sbeg, send;    // shard range of this FINISH call
   const int32_t* slist;  // or this shard list
   int32_t n_fin;         // shards of this FINISH call
+  bool fb_gone;          // the fallback replica was overwritten before FINISH (multi-GPU)
+  uint8_t* nonfin;       // [S] fast shard whose mean is not finite somewhere (k_reduce)
+  uint32_t* nonfin_any;  // any of them
 };
+
+// A fast shard whose mean is NaN or +-Inf somewhere: its (identical) copies score NaN
+// in the reference's agreement (max|a-b| = NaN, butterfly.py:127-133), so with two or
+// more survivors the shard is a disagreement (:255,264-267).  k_reduce only marks it;
+// k_nonfinite decides it.
+__device__ __forceinline__ void mark_nonfinite(const Params& p, int64_t s) {
+  p.nonfin[s] = 1;
+  *p.nonfin_any = 1u;
+}
 
 __device__ __forceinline__ int64_t fin_shard(const Params& p, unsigned i) {
   return p.slist ? (int64_t)p.slist[i] : p.sbeg + i;
@@ -482,6 +494,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
         }
         const V8 out = D::pack(acc);
         for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
+        bool fin = true;
+#pragma unroll
+        for (int k = 0; k < K; ++k) fin = fin && finite64(D::widen(acc[k]));
+        if (!fin) {  // rare: a replica holds NaN / Inf here
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (!finite64(D::widen(acc[k]))) mark_nonfinite(p, p.bnd.shard_of(e0 + k));
+        }
       } else if (c != 0xff) {  // one special or lost shard
         if (c == kSpecial) {  // the mean waits in the workspace for k_stats / k_apply
 #pragma unroll
@@ -518,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
           if (ce == kFast) {
             if (p.merged) p.merged[e] = D::widen(acc[k]);
             for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(acc[k]));
+            if (!finite64(D::widen(acc[k]))) mark_nonfinite(p, se);
           } else {
             emit_predicted<D>(p, s_dst, fb_raw, merged_apart, e, ce, p.pred[se] & kPredMask, D::widen(acc[k]));
           }
@@ -556,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
         if (c == kFast) {
           if (p.merged) p.merged[e] = D::widen(m);
           for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, D::widen(m));
+          if (!finite64(D::widen(m))) mark_nonfinite(p, s);
         } else {
           emit_predicted<D>(p, s_dst, fb_raw, merged_apart, e, c, p.pred[s] & kPredMask, D::widen(m));
         }
@@ -947,6 +969,58 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
   }
 }
 
+// Fast shards marked by k_reduce (non-finite mean somewhere) with >= 2 survivors:
+// status disagreement, every survivor flagged, entries NaN (r = 3: scores NaN), and
+// the fallback values into merged and the replicas (butterfly.py:255,264-273).  The
+// fallback is the caller's, else the lowest alive replica unless the scatter-back has
+// overwritten it in place (then NaN: its values are gone).  A persistent grid walks
+// (shard, chunk) items; without a marked shard every CTA returns at once.
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_nonfinite(Params p) {
+  extern __shared__ __align__(16) const void* s_ptr[];
+  if (*(volatile uint32_t*)p.nonfin_any == 0u) return;
+  void** s_dst = const_cast<void**>(s_ptr);
+  stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, 0);
+  const void* fb_raw = p.fb_src ? p.fb_src : (p.n_alive > 0 ? p.src[0] : nullptr);
+  bool fb_ok = fb_raw != nullptr && !p.fb_gone;
+  for (int d = 0; d < p.n_dst && fb_ok; ++d) fb_ok = s_dst[d] != fb_raw;
+  const int64_t items = (int64_t)p.n_fin * p.cps;  // this call's shards (all, a range or a list)
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t s = fin_shard(p, (unsigned)(it / p.cps)), ch = it % p.cps;
+    if (!p.nonfin[s] || p.cls[s] != kFast) continue;
+    const int32_t* mem = p.assign + s * p.r;
+    int surv[kMaxR], ns = 0;
+    for (int k = 0; k < p.r; ++k)
+      if (!p.failed[mem[k]]) surv[ns++] = k;
+    if (ns < 2) continue;  // a lone survivor agrees trivially: its mean stands
+    if (ch == 0 && threadIdx.x == 0) {
+      p.status[s] = BFLY_DISAGREEMENT;
+      p.source[s] = -1;
+      for (int x = 0; x < ns; ++x) {
+        p.flagged[mem[surv[x]]] = 1;
+        for (int y = x + 1; y < ns; ++y) {
+          const int i = mem[surv[x]], j = mem[surv[y]];
+          if (p.r == 2) {
+            p.entries[(int64_t)i * p.n + j] = nan64();
+            p.entries[(int64_t)j * p.n + i] = nan64();
+          } else {
+            const int pi = pair_index(p.r, surv[x], surv[y]);
+            p.scores[s * p.npairs + pi] = nan64();
+            p.has_score[s * p.npairs + pi] = 1;
+          }
+        }
+      }
+    }
+    const int64_t lo = p.bnd.start(s) + ch * kChunk, hi_s = p.bnd.start(s) + p.bnd.len(s);
+    const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+      const double v = p.fallback ? p.fallback[e] : (fb_ok ? D::raw(fb_raw, e) : nan64());
+      if (p.merged) p.merged[e] = v;
+      for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], e, v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // standalone agreement and mean_reducer
 // ---------------------------------------------------------------------------
@@ -1053,6 +1127,23 @@ static void launch_reduce(const Params& p, cudaStream_t st, int grid_per_sm = 8)
 }
 
 template <class D>
+static void launch_nonfinite(const Params& p, cudaStream_t st) {
+  const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_nonfinite<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int64_t grid = (int64_t)p.n_fin * p.cps;
+  if (grid > (int64_t)sm_count() * 2) grid = (int64_t)sm_count() * 2;
+  k_nonfinite<D><<<(unsigned)(grid < 1 ? 1 : grid), kThreads, smem, st>>>(p);
+}
+
+static void launch_nonfinite_dt(int32_t dtype, const Params& p, cudaStream_t st) {
+  switch (dtype) {
+    case BFLY_F32: launch_nonfinite<DF32>(p, st); break;
+    case BFLY_BF16: launch_nonfinite<DBF16>(p, st); break;
+    default: launch_nonfinite<DF64W>(p, st); break;
+  }
+}
+
+template <class D>
 static void launch_apply(const Params& p, cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1138,6 +1229,9 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.slist = a->d_shard_list;
   if (p.slist && a->n_shard_list < 0) return fail(BFLY_E_INVALID_ARG, "bad shard list");
   p.n_fin = p.slist ? a->n_shard_list : (int32_t)(p.send - p.sbeg);
+  p.fb_gone = a->fallback_gone != 0;
+  p.nonfin_any = (uint32_t*)(sc + L.off_nonfin);
+  p.nonfin = sc + L.off_nonfin + 4;
   return BFLY_OK;
 }
 
@@ -1164,12 +1258,15 @@ int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out)
     out->fallback = p.fallback;
     out->fb_src = p.fb_src;  // the multi-GPU last rank always names it (the lowest alive miner's replica)
     out->merged_apart = p.merged && p.merged != p.ws;
+    out->nonfin_any = p.nonfin_any;
+    out->nonfin = p.nonfin;
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nn = (int64_t)p.n * p.n;
   k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
   cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
   cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
+  cudaMemsetAsync(p.nonfin_any, 0, 4 + (size_t)p.S, st);
   k_classify<<<(unsigned)((p.S + 255) / 256), 256, 0, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ring round setup");
@@ -1186,14 +1283,20 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
   const int64_t S = p.S;
   cudaStream_t st = (cudaStream_t)stream;
 
+  if (a->phase < BFLY_PHASE_ALL || a->phase > BFLY_PHASE_CHECK) return fail(BFLY_E_INVALID_ARG, "bad phase");
   const bool do_reduce = a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_REDUCE;
   const bool do_finish = (a->phase == BFLY_PHASE_ALL || a->phase == BFLY_PHASE_FINISH) && p.n_fin > 0;
+  // non-finite fast shards are decided once the whole payload is reduced (the range
+  // ending at P), and again by every FINISH / CHECK call (idempotent)
+  const bool do_check = ((do_reduce && p.eend == p.P) || a->phase == BFLY_PHASE_FINISH ||
+                         a->phase == BFLY_PHASE_CHECK) && p.n_fin > 0;
   if (do_reduce) {
     if (p.ebeg == 0) {  // per-round setup runs with the first (or only) element range
       const int64_t nn = (int64_t)p.n * p.n;
       k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
       cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
       cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
+      cudaMemsetAsync(p.nonfin_any, 0, 4 + (size_t)p.S, st);
       k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
     }
     if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
@@ -1208,6 +1311,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
       }
     }
   }
+  if (do_check) launch_nonfinite_dt(a->dtype, p, st);
   if (do_finish) {
     const unsigned ns = (unsigned)p.n_fin;
     const int64_t tps = (p.bnd.base + (p.bnd.rem ? 1 : 0) + p.stile - 1) / p.stile + 1;  // tiles per shard

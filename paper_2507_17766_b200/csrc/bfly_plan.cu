@@ -130,6 +130,20 @@ __global__ void __launch_bounds__(kPlanThreads)
 
 using namespace bfly;
 
+// Generator.permutation(n) of RngStream(seed, ...) keyed (k0, k1): Fisher-Yates from
+// i = n-1 down to 1 with numpy's random_interval draws (simkernel.py:237-238).
+static void fisher_yates_host(int64_t n, uint64_t k0, uint64_t k1, int32_t* perm) {
+  for (int64_t i = 0; i < n; ++i) perm[i] = (int32_t)i;
+  PhiloxStream st;
+  st.init(k0, k1);
+  for (int64_t i = n - 1; i >= 1; --i) {
+    const int64_t j = (int64_t)random_interval(st, (uint64_t)i);
+    const int32_t t = perm[i];
+    perm[i] = perm[j];
+    perm[j] = t;
+  }
+}
+
 extern "C" {
 
 const char* bfly_version(void) { return "bfly 0.1.0 (sm_100a)"; }
@@ -157,6 +171,16 @@ int bfly_philox_key(const char* seed_decimal, const char* stream_id, uint64_t ou
   return BFLY_OK;
 }
 
+int bfly_permutation_host(int64_t n, uint64_t k0, uint64_t k1, int64_t* h_out) {
+  if (n < 0 || (n > 0 && !h_out)) return fail(BFLY_E_INVALID_ARG, "bad permutation arguments");
+  if (n > INT32_MAX) return fail(BFLY_E_UNSUPPORTED, "permutation too long");
+  int32_t* perm = new int32_t[n > 0 ? n : 1];
+  fisher_yates_host(n, k0, k1, perm);
+  for (int64_t i = 0; i < n; ++i) h_out[i] = perm[i];
+  delete[] perm;
+  return BFLY_OK;
+}
+
 int bfly_plan_host(int32_t n, int32_t r, int64_t P, uint64_t k0, uint64_t k1, int32_t* h_assign,
                    int64_t* h_bounds) {
   int64_t S;
@@ -164,15 +188,7 @@ int bfly_plan_host(int32_t n, int32_t r, int64_t P, uint64_t k0, uint64_t k1, in
   if (rc) return rc;
   if (r > 16) return fail(BFLY_E_INVALID_ARG, "redundancy too large");
   int32_t* perm = new int32_t[S];
-  for (int64_t i = 0; i < S; ++i) perm[i] = (int32_t)i;
-  PhiloxStream st;
-  st.init(k0, k1);
-  for (int64_t i = S - 1; i >= 1; --i) {
-    const int64_t j = (int64_t)random_interval(st, (uint64_t)i);
-    const int32_t t = perm[i];
-    perm[i] = perm[j];
-    perm[j] = t;
-  }
+  fisher_yates_host(S, k0, k1, perm);
   int32_t members[16];
   for (int64_t s = 0; s < S; ++s) {
     unrank_combination(n, r, perm[s], members);

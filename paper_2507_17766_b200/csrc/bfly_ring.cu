@@ -48,7 +48,6 @@
 // k_classify predicts (the means go to the workspace); FINISH decides those shards after
 // the kernel and the host re-broadcasts the few decided otherwise (multigpu.py).
 #include <cuda_runtime.h>
-#include <stdlib.h>
 
 #include "bfly_elem.cuh"
 #include "bfly_internal.cuh"
@@ -383,6 +382,14 @@ __device__ __forceinline__ void fallback_vec16(const RingParams& p, int64_t e0, 
   }
 }
 
+// A fast shard's mean came out NaN / Inf at e (a replica holds one): FINISH decides the
+// shard (k_nonfinite, bfly_merge.cu) after the kernel.  Rare, so one check per thread.
+__device__ __forceinline__ void ring_mark_nonfinite(const RingParams& p, int64_t e) {
+  if (!p.sp.nonfin) return;
+  p.sp.nonfin[p.sp.bnd.shard_of(e)] = 1;
+  *p.sp.nonfin_any = 1u;
+}
+
 template <class D>
 __device__ __forceinline__ double final_value(const RingParams& p, int64_t e, double mean, const double* fb_pre = nullptr,
                                               int64_t s = -1, bool ws_done = false) {
@@ -390,6 +397,7 @@ __device__ __forceinline__ double final_value(const RingParams& p, int64_t e, do
   const uint8_t c = p.sp.cls[s];
   if (c == kFast) {
     if (p.merged) p.merged[e] = mean;
+    if (!finite64(mean)) ring_mark_nonfinite(p, e);
     return mean;
   }
   if (c == kSpecial && !ws_done) p.sp.ws[e] = mean;
@@ -623,6 +631,14 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
             for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
           }
           *reinterpret_cast<uint4*>(out + tid * 16) = pack16<D>(acc);
+          bool fin = true;
+#pragma unroll
+          for (int k = 0; k < KE; ++k) fin = fin && finite64(D::widen(acc[k]));
+          if (!fin) {
+#pragma unroll
+            for (int k = 0; k < KE; ++k)
+              if (!finite64(D::widen(acc[k]))) ring_mark_nonfinite(p, t0 + tid * KE + k);
+          }
         }
       } else {
 #pragma unroll
@@ -640,6 +656,7 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
           } else {
             f = D::widen(v);
             if (p.merged) p.merged[t0 + e] = f;
+            if (!finite64(f)) ring_mark_nonfinite(p, t0 + e);
           }
           for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], t0 + e, f);
           D::store(out, e, f);
@@ -875,8 +892,9 @@ __device__ void ring_publisher(const RingParams& p, const Lane& ln, unsigned cha
   }
 }
 
+// One CTA = one lane of one rank: the roles above, dispatched by warp.
 template <class D>
-__global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
+__device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
   extern __shared__ __align__(1024) unsigned char sm[];
   using G = RingGeom<D>;
   const void** s_src = reinterpret_cast<const void**>(sm + G::OFF_PTR);
@@ -884,7 +902,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
   for (int q = threadIdx.x; q < p.n_src; q += blockDim.x) s_src[q] = p.src[q];
   for (int q = threadIdx.x; q < p.n_dst; q += blockDim.x) s_dst[q] = p.dst[q];
   Lane ln;
-  ln.c = (int)blockIdx.x;
+  ln.c = lane;
   ln.base_c = *steps_at(p, 0, ln.c);
   ln.base_r = *steps_at(p, 1, ln.c);
   const Bars B = Bars::at<D>(sm);
@@ -955,6 +973,24 @@ __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
   }
 }
 
+// One rank per GPU: CTA c is lane c.
+template <class D>
+__global__ void __launch_bounds__(kRingThreads, 1) k_ring(const __grid_constant__ RingParams p) {
+  ring_body<D>(p, (int)blockIdx.x);
+}
+
+// Single-device loopback: every rank of the ring on this GPU, CTA c is lane c % L of
+// rank c / L (all co-resident: one cooperative launch).
+constexpr int kMaxLoop = 8;
+struct RingLoopParams {
+  RingParams r[kMaxLoop];
+};
+template <class D>
+__global__ void __launch_bounds__(kRingThreads, 1) k_ring_loop(const __grid_constant__ RingLoopParams lp) {
+  const int L = lp.r[0].L;
+  ring_body<D>(lp.r[blockIdx.x / L], (int)(blockIdx.x % L));
+}
+
 template <class D>
 static size_t ring_smem_bytes(int n_src, int n_dst) {
   return (size_t)RingGeom<D>::OFF_PTR + sizeof(void*) * (size_t)(n_src + n_dst);
@@ -995,22 +1031,34 @@ static int ring_launch(RingParams p, cudaStream_t st) {
   return BFLY_OK;
 }
 
-
-static unsigned long long* g_prof = nullptr;  // diagnostics buffer (BFLY_RING_PROFILE)
-static int g_prof_n = 0;
+template <class D>
+static int ring_launch_loop(RingLoopParams& lp, int G, cudaStream_t st) {
+  int max_ptrs = 0;
+  for (int g = 0; g < G; ++g) {
+    RingParams& p = lp.r[g];
+    if (p.n_src + p.n_dst > kRingMaxPtrs) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many local replicas");
+    p.T = (p.P + RingGeom<D>::TE - 1) / RingGeom<D>::TE;
+    max_ptrs = max_ptrs > p.n_src + p.n_dst ? max_ptrs : p.n_src + p.n_dst;
+  }
+  const size_t smem = ring_smem_bytes<D>(max_ptrs, 0);
+  cudaFuncSetAttribute(k_ring_loop<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_loop<D>, kRingThreads, smem);
+  const int64_t ctas = (int64_t)G * lp.r[0].L;
+  if ((int64_t)per_sm * sm_count() < ctas)
+    return fail(BFLY_E_UNSUPPORTED, "fused ring loopback: " + std::to_string(ctas) + " CTAs cannot be co-resident");
+  void* args[] = {&lp};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_ring_loop<D>, dim3((unsigned)ctas), dim3(kRingThreads),
+                                              args, smem, st);
+  if (e != cudaSuccess) return cuda_fail(e, "k_ring_loop cooperative launch");
+  return BFLY_OK;
+}
 
 }  // namespace bfly
 
 using namespace bfly;
 
 extern "C" {
-
-int bfly_ring_fused_profile(unsigned long long* host_out, int32_t n) {
-  if (!g_prof) return fail(BFLY_E_INVALID_ARG, "no profile (set BFLY_RING_PROFILE)");
-  const int m = n < g_prof_n ? n : g_prof_n;
-  cudaError_t e = cudaMemcpy(host_out, g_prof, sizeof(unsigned long long) * (size_t)m, cudaMemcpyDeviceToHost);
-  return e == cudaSuccess ? m : cuda_fail(e, "profile copy");
-}
 
 int32_t bfly_ring_fused_lanes(int32_t dtype) {
   switch (dtype) {
@@ -1040,7 +1088,13 @@ int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* of
   return BFLY_OK;
 }
 
-int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
+}  // extern "C"
+
+namespace bfly {
+// Descriptor -> kernel parameters of one rank (every check before the first CUDA
+// call); the last rank's per-round setup (NaN entries, flags, classify) is issued on
+// `stream` here.
+static int ring_params(const bfly_ring_fused_desc_t* d, void* stream, RingParams* out) {
   if (!d || d->world < 2 || d->rank < 0 || d->rank >= d->world || d->lanes < 1 || d->nb < 2 || !d->peer_base ||
       d->payload_len < 1 || d->n_src < 0 || d->n_dst < 0 || (d->n_src > 0 && !d->d_src) ||
       (d->n_dst > 0 && !d->d_dst))
@@ -1050,14 +1104,12 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   int64_t off_fin = 0, off_flags = 0, total = 0;
   int rc = bfly_ring_fused_layout(d->lanes, d->nb, d->dtype, &off_fin, &off_flags, &total);
   if (rc) return rc;
-  // every check before the first CUDA call
   if (g == Z && d->special && !d->merge_args) return fail(BFLY_E_INVALID_ARG, "fused ring: special shards need merge_args");
   if (G > kMaxG) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many ranks");
   if ((int64_t)kSR < (int64_t)(G - 1) * (kNT + d->nb) + 1)
     return fail(BFLY_E_UNSUPPORTED, "fused ring: schedule ring too short for this many ranks and slots");
-  int pub_every = 1, lag = 1;
-  if (const char* e = getenv("BFLY_RING_PUB_EVERY")) pub_every = atoi(e) > 0 ? atoi(e) : 1;
-  if (const char* e = getenv("BFLY_RING_LAG")) lag = atoi(e) < 1 ? 1 : (atoi(e) > kMaxLag ? kMaxLag : atoi(e));
+  const int pub_every = d->pub_every > 0 ? d->pub_every : 1;
+  const int lag = d->lag < 1 ? 1 : (d->lag > kMaxLag ? kMaxLag : d->lag);
   // a step is visible at most lag + pub_every - 1 steps after it is stored; its producer
   // must not need the credit of that step before then
   if (pub_every > d->nb - lag) return fail(BFLY_E_INVALID_ARG, "fused ring: nb too small for the publication lag");
@@ -1098,19 +1150,50 @@ int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
   p.n_dst = d->n_dst;
   p.n_div = d->n_div;
   p.merged = g == Z ? d->d_merged : nullptr;
-  if (getenv("BFLY_RING_PROFILE")) {
-    if (!g_prof || g_prof_n < p.L * kProfSlots) {
-      if (g_prof) cudaFree(g_prof);
-      g_prof_n = p.L * kProfSlots;
-      if (cudaMalloc(&g_prof, sizeof(unsigned long long) * g_prof_n) != cudaSuccess) return fail(BFLY_E_CUDA, "prof");
-    }
-    cudaMemsetAsync(g_prof, 0, sizeof(unsigned long long) * g_prof_n, st);
-    p.prof = g_prof;
+  p.prof = d->d_profile;
+  if (p.prof) {
+    cudaError_t e = cudaMemsetAsync(p.prof, 0, sizeof(unsigned long long) * (size_t)p.L * kProfSlots, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused ring: profile buffer");
   }
+  *out = p;
+  return BFLY_OK;
+}
+}  // namespace bfly
+
+extern "C" {
+
+int bfly_ring_fused(const bfly_ring_fused_desc_t* d, void* stream) {
+  RingParams p;
+  int rc = ring_params(d, stream, &p);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
   switch (d->dtype) {
     case BFLY_F32: return ring_launch<DF32>(p, st);
     case BFLY_BF16: return ring_launch<DBF16>(p, st);
     case BFLY_F64WIRE: return ring_launch<DF64W>(p, st);
+    default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  }
+}
+
+int bfly_ring_fused_loopback(const bfly_ring_fused_desc_t* descs, int32_t world, void* stream) {
+  if (!descs || world < 2 || world > kMaxLoop) return fail(BFLY_E_INVALID_ARG, "fused ring loopback: bad world");
+  for (int g = 0; g < world; ++g) {
+    const bfly_ring_fused_desc_t& d = descs[g];
+    if (d.rank != g || d.world != world || d.lanes != descs[0].lanes || d.nb != descs[0].nb ||
+        d.dtype != descs[0].dtype || d.payload_len != descs[0].payload_len)
+      return fail(BFLY_E_INVALID_ARG, "fused ring loopback: descriptors disagree");
+    if (d.d_profile) return fail(BFLY_E_UNSUPPORTED, "fused ring loopback: no profile buffer");
+  }
+  RingLoopParams local{};
+  for (int g = 0; g < world; ++g) {
+    int rc = ring_params(&descs[g], stream, &local.r[g]);
+    if (rc) return rc;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (descs[0].dtype) {
+    case BFLY_F32: return ring_launch_loop<DF32>(local, world, st);
+    case BFLY_BF16: return ring_launch_loop<DBF16>(local, world, st);
+    case BFLY_F64WIRE: return ring_launch_loop<DF64W>(local, world, st);
     default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
   }
 }

@@ -258,25 +258,34 @@ class ButterflyMerge:
         self._acc_in = None
         self._graph = None  # CUDA graph of one round (capture())
 
+    def set_fallback(self, fallback: torch.Tensor | None) -> "ButterflyMerge":
+        """Replace the fp64 fallback vector (butterfly.py:169,268-273) for later phases."""
+        if fallback is not None and int(fallback.numel()) != self.P:
+            raise errors.ShapeError("fallback length does not match payloads")
+        self.fallback = None if fallback is None else fallback.to(self.dev, torch.float64).contiguous()
+        self._args.d_fallback = self.fallback.data_ptr() if self.fallback is not None else None
+        return self
+
     def _call(self, stream):
         with torch.cuda.device(self.dev):
             L.check(L.lib().bfly_merge(ctypes.byref(self._args), _stream_handle(stream)))
 
     def run(self, phase: int = L.PHASE_ALL, host_copies: torch.Tensor | None = None, stream=None) -> "ButterflyMerge":
         """Issue the merge kernels on ``stream`` (default: current stream). Asynchronous."""
-        if self.remote_sum and phase != L.PHASE_FINISH:
+        if self.remote_sum and phase not in (L.PHASE_FINISH, L.PHASE_CHECK):
             raise errors.InvalidArgumentError("a chained merge reduces through reduce_range(acc_in=...)")
         if host_copies is not None:
             self._host_copies = host_copies
             self._args.d_host_copies = host_copies.data_ptr()
+        requested = phase
         if phase == L.PHASE_FINISH and not self.needs_finish():
-            return self  # every shard is fast: nothing to compare, adopt or fall back
+            phase = L.PHASE_CHECK  # every shard is fast: only non-finite means can fall back
         if phase == L.PHASE_ALL and not self.needs_finish():
-            phase = L.PHASE_REDUCE  # every shard fast: k_classify already wrote its results
+            phase = L.PHASE_REDUCE  # every shard fast: k_classify wrote their results (REDUCE checks means)
         self._args.phase = phase
         self._args.d_acc_in = None
         self._args.elem_begin = self._args.elem_end = 0
-        if self._graph is not None and phase == L.PHASE_ALL and host_copies is None:
+        if self._graph is not None and requested == L.PHASE_ALL and host_copies is None:
             self._replay(stream)
         else:
             self._call(stream)
@@ -369,8 +378,31 @@ class ButterflyMerge:
         # r = 3: a pair's entry is the minimum over the shards it shares (k_entries3)
         return self.special or self.maybe_lost or self.r > 2
 
+    def fast_shards(self) -> np.ndarray:
+        """Shards with >= 1 surviving assignee, none of them corrupted (k_classify's kFast)."""
+        assign = self.plan.assign.cpu().numpy()
+        failed = self._failed.cpu().numpy().astype(bool)
+        kinds = self._corr_kinds()
+        alive = ~failed[assign]
+        corrupt = (kinds[assign] != L.CORR_NONE) & alive
+        return np.flatnonzero(alive.any(axis=1) & ~corrupt.any(axis=1))
+
+    def _corr_kinds(self) -> np.ndarray:
+        raw = self._corr.cpu().numpy().tobytes()
+        size = ctypes.sizeof(L.Corruption)
+        return np.array([int.from_bytes(raw[m * size:m * size + 4], "little", signed=True) for m in range(self.n)],
+                        dtype=np.int32)
+
+    def nonfinite_shards(self) -> np.ndarray:
+        """Fast shards decided a disagreement because their mean is NaN / Inf somewhere
+        (k_nonfinite; the reference's agreement of two NaN copies is NaN,
+        butterfly.py:127-133,255).  Reads the status back (synchronises)."""
+        fast = self.fast_shards()
+        status = self.status.cpu().numpy()
+        return fast[status[fast] != L.MERGED]
+
     # number of our kernels one run() launches (reported by bench.py as gpu_launches)
     def launches_per_run(self) -> int:
-        # k_fill_nan, k_classify, [k_reduce] + [k_stats, k_decide, [k_entries3], k_apply]
+        # k_fill_nan, k_classify, [k_reduce], k_nonfinite + [k_stats, k_decide, [k_entries3], k_apply]
         fin = (3 + (1 if self.r > 2 else 0)) if self.needs_finish() else 0
-        return 2 + (1 if self.local_alive or self.remote_sum else 0) + fin
+        return 3 + (1 if self.local_alive or self.remote_sum else 0) + fin

@@ -36,7 +36,7 @@ bit-identical to the single-GPU (and reference) result.
 from __future__ import annotations
 
 import ctypes
-import os
+import threading
 
 import numpy as np
 import torch
@@ -47,9 +47,215 @@ from . import errors
 from . import ringsched as rs
 from .device import ButterflyMerge, _DTYPES, _stream_handle
 
-NB = int(os.environ.get("BFLY_RING_NB", "3"))  # inbox slots per ring
+NB = 3  # inbox slots per ring of the chunked executor
 WINDOW = 4  # chunks the host may run ahead of the GPUs per stream
-FUSED_NB = int(os.environ.get("BFLY_FUSED_NB", "10"))  # slots per lane of the persistent ring
+FUSED_NB = 10  # slots per lane of the persistent ring (more spill the inboxes out of L2)
+
+
+# ---------------------------------------------------------------------------
+# communication: torch.distributed across processes, or threads on one device
+# ---------------------------------------------------------------------------
+
+
+class DistComm:
+    """One process per GPU (torch.distributed, NCCL): the production transport.  Peer
+    memory is shared through CUDA IPC handles; the persistent ring is one cooperative
+    launch per GPU."""
+
+    loopback = False
+
+    def __init__(self):
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+
+    def all_gather_object(self, obj) -> list:
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def all_reduce_min(self, x: int, dev) -> int:
+        t = torch.tensor([int(x)], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return int(t.item())
+
+    def barrier(self):
+        dist.barrier()
+
+    def broadcast(self, t: torch.Tensor, src: int):
+        dist.broadcast(t, src=src)
+
+    def share_region(self, base: int, handle: bytes, dev) -> dict:
+        """rank -> this process's mapping of every rank's region."""
+        handles = self.all_gather_object(bytes(handle))
+        peer = {}
+        with torch.cuda.device(dev):
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    peer[r] = base
+                    continue
+                p = ctypes.c_void_p()
+                L.check(L.lib().bfly_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p)))
+                peer[r] = p.value
+        dist.barrier()
+        return peer
+
+    def close_region(self, peer: dict, base: int, dev):
+        lib = L.lib()
+        with torch.cuda.device(dev):
+            for r, p in peer.items():
+                if r != self.rank:
+                    lib.bfly_ipc_close(ctypes.c_void_p(p))
+            lib.bfly_ipc_free(ctypes.c_void_p(base))
+
+    def export_tensor(self, t: torch.Tensor):
+        return _ipc_export(t)
+
+    def map_tensor(self, token, dev) -> int:
+        handle, off = token
+        return _ipc_map(handle, dev) + off
+
+    def unmap_tensor(self, token):
+        _ipc_unmap(token[0])
+
+    def launch_fused(self, desc, dev):
+        with torch.cuda.device(dev):
+            L.check(L.lib().bfly_ring_fused(ctypes.byref(desc), _stream_handle()))
+
+
+class LoopbackGroup:
+    """State shared by the ranks of a single-device loopback ring (one thread each)."""
+
+    def __init__(self, world: int, timeout: float = 300.0):
+        if not 2 <= world <= 8:
+            raise errors.InvalidArgumentError("loopback rings have 2..8 ranks")
+        self.world = world
+        self.barrier = threading.Barrier(world, timeout=timeout)
+        self.slots = [None] * world
+
+
+class LoopbackComm:
+    """G ranks of the ring as G threads of ONE process on ONE device (each with its own
+    CUDA stream): collectives are exchanges between the threads, peer memory is plain
+    device memory, and the persistent ring's G kernels become ONE cooperative launch of
+    G x L CTAs (bfly_ring_fused_loopback).  The kernels, the protocol and every line of
+    ShardedButterflyMerge above the transport are the multi-GPU ones — so the ring is
+    parity-tested and profiled on a single GPU."""
+
+    loopback = True
+
+    def __init__(self, group: LoopbackGroup, rank: int):
+        self.group, self.rank, self.world = group, rank, group.world
+
+    def _exchange(self, obj) -> list:
+        g = self.group
+        g.barrier.wait()
+        g.slots[self.rank] = obj
+        g.barrier.wait()
+        out = list(g.slots)
+        g.barrier.wait()
+        return out
+
+    def all_gather_object(self, obj) -> list:
+        return self._exchange(obj)
+
+    def all_reduce_min(self, x: int, dev) -> int:
+        return min(self._exchange(int(x)))
+
+    def barrier(self):
+        self.group.barrier.wait()
+
+    def broadcast(self, t: torch.Tensor, src: int):
+        cur = torch.cuda.current_stream(t.device)
+        if self.rank == src:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            slots = self._exchange((t, ev))
+            done = self._exchange(None)
+            for d in done:
+                if d is not None:
+                    cur.wait_event(d)  # the readers' copies finish before src writes t again
+            return
+        slots = self._exchange(None)
+        src_t, ev = slots[src]
+        cur.wait_event(ev)
+        t.copy_(src_t)
+        mine = torch.cuda.Event()
+        mine.record(cur)
+        self._exchange(mine)
+
+    def share_region(self, base: int, handle: bytes, dev) -> dict:
+        return dict(enumerate(self._exchange(base)))
+
+    def close_region(self, peer: dict, base: int, dev):
+        self.barrier()  # no rank frees its region while another's kernel may still use it
+        torch.cuda.synchronize(dev)
+        self.barrier()
+        with torch.cuda.device(dev):
+            L.lib().bfly_ipc_free(ctypes.c_void_p(base))
+
+    def export_tensor(self, t: torch.Tensor):
+        return t.data_ptr()
+
+    def map_tensor(self, token, dev) -> int:
+        return int(token)
+
+    def unmap_tensor(self, token):
+        pass
+
+    def launch_fused(self, desc, dev):
+        """Rank 0 launches every rank's lanes once all ranks' preceding work is queued."""
+        cur = torch.cuda.current_stream(dev)
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        got = self._exchange((desc, ready))
+        err, done = None, None
+        if self.rank == 0:
+            for _, ev in got:
+                cur.wait_event(ev)
+            arr = (L.RingFusedDesc * self.world)()
+            for g, (d, _) in enumerate(got):
+                arr[g] = d
+            with torch.cuda.device(dev):
+                rc = L.lib().bfly_ring_fused_loopback(arr, self.world, _stream_handle())
+            if rc != L.OK:
+                err = (rc, L.lib().bfly_last_error().decode(errors="replace"))
+            done = torch.cuda.Event()
+            done.record(cur)
+        res = self._exchange((err, done))
+        err, done = res[0]
+        if err is not None:
+            raise RuntimeError(f"loopback ring launch failed ({err[0]}): {err[1]}")
+        cur.wait_event(done)
+
+
+def run_loopback(world: int, fn, device=None, timeout: float = 300.0) -> list:
+    """Run ``fn(rank, comm)`` for every rank of a ``world``-rank ring on ``world`` threads
+    of this process, all on one CUDA device (each thread on its own stream), and return
+    the per-rank results.  The first exception of any rank is re-raised (the others'
+    collectives are aborted)."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    group = LoopbackGroup(world, timeout)
+    results, failures = [None] * world, [None] * world
+
+    def body(rank):
+        try:
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(torch.cuda.Stream(device=dev)):
+                results[rank] = fn(rank, LoopbackComm(group, rank))
+                torch.cuda.current_stream(dev).synchronize()
+        except BaseException as e:  # noqa: BLE001 - re-raised in the caller
+            failures[rank] = e
+            group.barrier.abort()
+
+    threads = [threading.Thread(target=body, args=(r,), name=f"bfly-loopback-{r}") for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    first = [e for e in failures if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if first or any(failures):
+        raise first[0] if first else next(e for e in failures if e is not None)
+    return results
 
 
 def special_ranges(assign: np.ndarray, P: int, failures: set, corrupted: set) -> list:
@@ -211,12 +417,23 @@ class ShardedButterflyMerge:
                  .n_shards/.redundancy/.payload_len), identical on every rank.
     failures / corruptions / fallback / tolerance: as ButterflyMerge, global indices.
     chunk        elements per pipelined chunk (multiple of 4096).
+    comm         the transport: DistComm() (default, one process per GPU) or a
+                 LoopbackComm (ranks as threads on one device, see run_loopback).
+    executor     "auto" (the persistent ring whenever it applies) or "chunked".
+    per_chunk_finish  chunked ring: the last rank decides each chunk's special shards
+                 before relaying it (False: all after the ring; diagnostics).
+    debug / timing    diagnostics of the chunked ring (per-op watchdog, timeline) and
+                 per-phase CUDA-event times of a round (``.timings``).
     """
 
     def __init__(self, local: list, plan, *, failures=(), corruptions=None, fallback=None,
-                 want_merged: bool = False, tolerance: float = 1e-6, chunk: int = 1 << 24):
-        self.rank = dist.get_rank()
-        self.world = G = dist.get_world_size()
+                 want_merged: bool = False, tolerance: float = 1e-6, chunk: int = 1 << 24, comm=None,
+                 executor: str = "auto", per_chunk_finish: bool = True, debug: int = 0, timing: bool = False):
+        self.comm = comm if comm is not None else DistComm()
+        self.rank = self.comm.rank
+        self.world = G = self.comm.world
+        if executor not in ("auto", "chunked"):
+            raise errors.InvalidArgumentError(f"unknown executor {executor!r}")
         if not local:
             raise errors.InvalidArgumentError("every rank must hold at least one miner")
         self.local = list(local)
@@ -231,9 +448,7 @@ class ShardedButterflyMerge:
         self.chunk = int(min(chunk, ((self.P + 4095) // 4096) * 4096))  # inbox slot size
         self.edges = chunk_edges(self.P, self.chunk, ramp=G > 1)
         self.K = len(self.edges) - 1
-        counts = [torch.zeros(1, dtype=torch.int64, device=self.dev) for _ in range(G)]
-        dist.all_gather(counts, torch.tensor([len(local)], dtype=torch.int64, device=self.dev))
-        self.counts = [int(c.item()) for c in counts]
+        self.counts = [int(c) for c in self.comm.all_gather_object(len(local))]
         self.offset = sum(self.counts[: self.rank])
         self.n = sum(self.counts)
         if self.n != plan.n_miners:
@@ -248,8 +463,8 @@ class ShardedButterflyMerge:
         self.is_last = self.rank == G - 1
         self.plan_r = int(getattr(plan, "redundancy", 2))
         self._round = 0
-        self.debug = int(__import__("os").environ.get("BFLY_DEBUG_RING", "0"))
-        self.timing = bool(int(__import__("os").environ.get("BFLY_RING_TIMING", "0")))  # per-phase ms in .timings
+        self.debug = int(debug)
+        self.timing = bool(timing)  # per-phase ms in .timings
         self.timings = {}
         self._tables = []  # keeps the device pointer tables alive
         self._peer = None
@@ -263,8 +478,7 @@ class ShardedButterflyMerge:
         self._finish_ranges, straddlers = self._chunk_shard_ranges(plan.n_shards)
         self.straddlers = straddlers
         self._straddle_dev = torch.tensor(straddlers, dtype=torch.int32, device=self.dev)
-        # BFLY_RING_LATE=0 (diagnostics): no per-chunk finishing, every special shard after the ring
-        self._per_chunk_finish = os.environ.get("BFLY_RING_LATE", "1") != "0"
+        self._per_chunk_finish = bool(per_chunk_finish)
         # fallback values come from the lowest alive miner when no fallback is given; when
         # that replica lives on another rank the last rank reads it in place over NVLink
         # (IPC-mapped): chunk k of it is only overwritten by the relay, which starts after
@@ -284,12 +498,11 @@ class ShardedButterflyMerge:
         self._cls, self._pred = classify_host(assign, failures, corrupted, len(self.alive))
         self._special_ids = np.flatnonzero(self._cls != CLS_FAST)
         honest_major = bool(np.any((self._cls == CLS_SPECIAL) & (self._pred == PRED_MEAN)))
-        self.fused = bool(G > 1 and self.P // plan.n_shards >= 2 and os.environ.get("BFLY_RING_FUSED", "1") != "0"
+        self.fused = bool(G > 1 and self.P // plan.n_shards >= 2 and executor == "auto"
                           and not (self._needs_fb and (self.fb_owner == G - 1 or honest_major)))
         if self.fused:
-            ok = torch.tensor([int(all(t.data_ptr() % 16 == 0 for t in self.local))], device=self.dev)
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-            self.fused = bool(ok.item())
+            self.fused = bool(self.comm.all_reduce_min(int(all(t.data_ptr() % 16 == 0 for t in self.local)),
+                                                       self.dev))
         self._corr_kind = np.zeros(self.n, dtype=np.int32)
         for m, c in (corruptions or {}).items():
             self._corr_kind[int(m)] = int(c.code()) if hasattr(c, "code") else 1
@@ -300,12 +513,11 @@ class ShardedButterflyMerge:
         self.special_runs = late  # kept name: ranges broadcast after the ring
         self._late_set = self._range_set(late) if late else None
         if G > 1 and self._needs_fb and self.fb_owner != G - 1:
-            info = _ipc_export(local[m0 - self.offset]) if self.rank == self.fb_owner else None
-            infos = [None] * G
-            dist.all_gather_object(infos, info)
+            info = self.comm.export_tensor(local[m0 - self.offset]) if self.rank == self.fb_owner else None
+            infos = self.comm.all_gather_object(info)
             if self.is_last:
-                self._fb_handle, off = infos[self.fb_owner]
-                self._fb_ptr = _ipc_map(self._fb_handle, self.dev) + off
+                self._fb_handle = infos[self.fb_owner]
+                self._fb_ptr = self.comm.map_tensor(self._fb_handle, self.dev)
                 if late:  # shards straddling chunk edges finish after the relay: copy theirs first
                     self._fb_buf = torch.empty_like(local[0])
 
@@ -320,6 +532,9 @@ class ShardedButterflyMerge:
             self.job = ButterflyMerge(reps, plan, remote_sum=G > 1, n_div=len(self.alive), failures=failures,
                                       corruptions=corruptions, fallback=fallback, fallback_src=fb_src,
                                       scatter_back=True, want_merged=want_merged, tolerance=tolerance)
+            # shards decided after the exchange (non-finite means) cannot read the lowest
+            # alive replica any more: the relay has overwritten it (bfly.h fallback_gone)
+            self.job._args.fallback_gone = int(G > 1)
         # last rank: late shards possible (corrupted survivors, or shards whose assignees
         # all failed) -> each chunk's are finished on the late-shard stream
         self._late_mode = bool(self.is_last and self.job.needs_finish() and self._per_chunk_finish)
@@ -392,33 +607,23 @@ class ShardedButterflyMerge:
         return t
 
     def _open_region(self, total: int):
-        """Allocate this rank's IPC region (zeroed) and map every other rank's."""
+        """Allocate this rank's region (zeroed, IPC-exportable) and map every other rank's."""
         lib = L.lib()
         base = ctypes.c_void_p()
         handle = (ctypes.c_uint8 * 64)()
         with torch.cuda.device(self.dev):
             L.check(lib.bfly_ipc_alloc(total, ctypes.byref(base), handle))
         self._base = base.value
-        handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(handle))
-        self._peer = {}
-        with torch.cuda.device(self.dev):
-            for r, h in enumerate(handles):
-                if r == self.rank:
-                    self._peer[r] = self._base
-                    continue
-                p = ctypes.c_void_p()
-                L.check(lib.bfly_ipc_open((ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p)))
-                self._peer[r] = p.value
-        dist.barrier()
+        self._peer = self.comm.share_region(self._base, bytes(handle), self.dev)
         self._peer_arr = (ctypes.c_uint64 * self.world)(*[self._peer[r] for r in range(self.world)])
 
     def _setup_fused(self):
         """The persistent single-kernel ring (bfly_ring_fused, csrc/bfly_ring.cu)."""
         lib = L.lib()
-        lanes = torch.tensor([int(lib.bfly_ring_fused_lanes(self.dtype))], dtype=torch.int64, device=self.dev)
-        dist.all_reduce(lanes, op=dist.ReduceOp.MIN)  # every rank must deal tiles to the same lanes
-        self.lanes = int(lanes.item())
+        lanes = int(lib.bfly_ring_fused_lanes(self.dtype))
+        if self.comm.loopback:  # every rank's lanes share this one device
+            lanes //= self.world
+        self.lanes = self.comm.all_reduce_min(lanes, self.dev)  # every rank deals tiles to the same lanes
         if self.lanes < 1:
             raise RuntimeError("fused ring: no co-resident lanes on this device")
         o = [ctypes.c_int64() for _ in range(3)]
@@ -440,10 +645,10 @@ class ShardedButterflyMerge:
     def _setup_ring(self):
         self.layout = lay = _Region(self.chunk, self.esize)
         self._open_region(lay.total)
-        self._relay = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("BFLY_RELAY_PRIORITY", "0")))
+        self._relay = torch.cuda.Stream(device=self.dev)
         # last rank: per-chunk late shards, high priority so a chunk's decision does not queue
         # behind the next chunk's reduce CTAs (the relay waits for it)
-        self._late = torch.cuda.Stream(device=self.dev, priority=int(os.environ.get("BFLY_LATE_PRIORITY", "-1")))
+        self._late = torch.cuda.Stream(device=self.dev, priority=-1)
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -490,22 +695,19 @@ class ShardedButterflyMerge:
         self._desc = d
 
     def close(self):
+        """Release the peer regions (a collective: every rank calls it)."""
         if self._peer:
-            lib = L.lib()
             torch.cuda.synchronize(self.dev)
-            with torch.cuda.device(self.dev):
-                for r, p in self._peer.items():
-                    if r != self.rank:
-                        lib.bfly_ipc_close(ctypes.c_void_p(p))
-                lib.bfly_ipc_free(ctypes.c_void_p(self._base))
-                if self._fb_handle is not None:
-                    _ipc_unmap(self._fb_handle)
-                    self._fb_handle = None
+            self.comm.close_region(self._peer, self._base, self.dev)
+            if self._fb_handle is not None:
+                self.comm.unmap_tensor(self._fb_handle)
+                self._fb_handle = None
             self._peer = None
 
     def __del__(self):
         try:
-            self.close()
+            if not self.comm.loopback:  # (a loopback close is a collective of the threads)
+                self.close()
         except Exception:
             pass
 
@@ -608,8 +810,7 @@ class ShardedButterflyMerge:
                 self.job.reduce_range(b, e)
         elif self.fused:
             self._fdesc.round_index = self._round
-            with torch.cuda.device(self.dev):
-                L.check(L.lib().bfly_ring_fused(ctypes.byref(self._fdesc), _stream_handle()))
+            self.comm.launch_fused(self._fdesc, self.dev)
         else:
             # fallback values (the lowest alive miner's replica) for the late shards: packed
             # before the relay overwrites that replica, sent while the ring runs
@@ -658,6 +859,8 @@ class ShardedButterflyMerge:
                     self.job._args.d_fallback_src = self._fb_buf.data_ptr()
                 self.job.run(L.PHASE_FINISH)
                 self.job._args.d_fallback_src = self._fb_ptr if self._fb_ptr is not None else self.job._args.d_fallback_src
+            elif self.fused:  # every shard fast: only a non-finite mean can still fall back
+                self.job.run(L.PHASE_CHECK)
             elif self.job.needs_finish() and self.straddlers:
                 a = self.job._args
                 if self._fb_buf is not None:  # the owner's replica may hold relayed values by now
@@ -671,10 +874,10 @@ class ShardedButterflyMerge:
                 self._copy_ranges(self._late_set, self.local[0].data_ptr(), None, 0, 0)
         mark("finish")
         if G > 1:
-            dist.broadcast(self._res, src=last)
+            self.comm.broadcast(self._res, src=last)
             mark("results")
             if self.special_runs:
-                dist.broadcast(self._late_set[1], src=last)
+                self.comm.broadcast(self._late_set[1], src=last)
                 mark("late_bcast")
                 if not self.is_last:
                     self._copy_ranges(self._late_set, None, self._local_table.data_ptr(), len(self.local), 1)
@@ -682,11 +885,11 @@ class ShardedButterflyMerge:
             if self.want_merged:
                 if self.is_last:
                     self.merged.copy_(self.job.merged)
-                dist.broadcast(self.merged, src=last)
+                self.comm.broadcast(self.merged, src=last)
         elif self.want_merged:
             self.merged.copy_(self.job.merged)
         unpack_results(self._res, self.entries, self.source, self.status, self.flagged)
-        if G > 1 and self.fused and len(self._special_ids):
+        if G > 1:
             self._rebroadcast_mispredicted()
         mark("end")
         if tm is not None:
@@ -697,11 +900,21 @@ class ShardedButterflyMerge:
         return self
 
     def _rebroadcast_mispredicted(self):
-        """Persistent ring: the relayed tiles of special / lost shards carried the predicted
-        outcome; the shards FINISH decided otherwise (k_apply rewrote them on the last rank)
-        are sent to the other ranks and scattered into their replicas."""
-        mis = mispredicted_shards(self._special_ids, self._pred, self.source.cpu().numpy(), self._corr_kind)
+        """The relayed tiles carried the predicted outcome of every shard: the mean of fast
+        shards, k_classify's guess for special / lost ones (persistent ring).  The shards
+        decided otherwise after the exchange — special ones FINISH decided against the
+        guess, and fast ones whose mean came out non-finite (k_nonfinite: a disagreement,
+        butterfly.py:127-133,264-273) — are rewritten on the last rank, sent to the other
+        ranks and scattered into their replicas.  Every rank reads the same status, so
+        they agree on the list without communicating."""
+        status = self.status.cpu().numpy()
+        fast = np.flatnonzero(self._cls == CLS_FAST)
+        nonfinite = fast[status[fast] != L.MERGED]
+        mis = (mispredicted_shards(self._special_ids, self._pred, self.source.cpu().numpy(), self._corr_kind)
+               if self.fused and len(self._special_ids) else np.zeros(0, dtype=np.int64))
+        mis = np.union1d(mis, nonfinite).astype(np.int64)
         self.mispredicted = len(mis)
+        self.nonfinite = nonfinite
         if not len(mis):
             return
         base, rem = divmod(self.P, self.plan.n_shards)
@@ -716,7 +929,7 @@ class ShardedButterflyMerge:
         rset = self._range_set(runs)
         if self.is_last:
             self._copy_ranges(rset, self.local[0].data_ptr(), None, 0, 0)
-        dist.broadcast(rset[1], src=self.world - 1)
+        self.comm.broadcast(rset[1], src=self.world - 1)
         if not self.is_last:
             self._copy_ranges(rset, None, self._local_table.data_ptr(), len(self.local), 1)
 

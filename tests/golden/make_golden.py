@@ -81,9 +81,11 @@ def spans_for(plan, miner, failures):
 
 
 def run_case(name, n, P, seed, *, payload_seed=0, failures=(), corr=None, fallback=None,
-             ids=None, wire_ratio=1.0, tol=1e-6, store_payloads=True):
+             ids=None, wire_ratio=1.0, tol=1e-6, store_payloads=True, poison=()):
     rng = np.random.default_rng(payload_seed)
     payloads_arr = [rng.uniform(-1.0, 1.0, P) for _ in range(n)]
+    for m, e, v in poison:  # a diverged miner: NaN / +-Inf weights (fp64, so also on the wire)
+        payloads_arr[m][e] = v
     ids = ids if ids is not None else list(range(n))
     payloads = {ids[m]: payloads_arr[m] for m in range(n)}
     sorted_ids = sorted(payloads)
@@ -115,6 +117,7 @@ def run_case(name, n, P, seed, *, payload_seed=0, failures=(), corr=None, fallba
                 corruptions={str(k): list(v) for k, v in corr.items()}, fallback=fallback,
                 ids=[str(i) for i in sorted_ids], id_kind="str" if isinstance(ids[0], str) else "int",
                 wire_ratio=wire_ratio, tol=tol, meter=meter, n_objects=len(store.objects),
+                poison=[[int(m), int(e), repr(float(v))] for m, e, v in poison],
                 objects_sha256=hashlib.sha256("\n".join(sorted(store.objects)).encode()).hexdigest(),
                 payload_sha256=hashlib.sha256(wire.tobytes()).hexdigest(),
                 store_payloads=store_payloads)
@@ -163,6 +166,13 @@ def make_merges():
         run_case("crit4_small_n50", 50, 1225 * 16, 4, payload_seed=4,
                  corr={m: (NOISE, 1.5, K[0] + m, K[1]) for m in range(10)}, fallback="zeros",
                  store_payloads=False),
+        # non-finite weights: identical NaN copies score NaN, so the shard
+        # is a disagreement, both assignees are flagged and the fallback is used
+        run_case("nonfinite_nofb_n5", 5, 53, 17, poison=[(2, 7, np.nan), (0, 30, np.inf), (4, 44, -np.inf)]),
+        run_case("nonfinite_fb_n6", 6, 15 * 9 + 4, 18, failures=(1,), fallback="ramp",
+                 poison=[(0, e, np.nan) for e in range(0, 139, 9)] + [(3, 11, np.inf), (5, 11, -np.inf)]),
+        run_case("nonfinite_corrupt_n7", 7, 21 * 6 + 1, 19, corr={3: (ADD, 0.5)}, failures=(6,),
+                 poison=[(4, e, np.inf) for e in range(2, 127, 11)]),
     ]
     (OUT / "merge_cases.json").write_text(json.dumps(cases, indent=1))
 

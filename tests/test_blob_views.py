@@ -2,26 +2,22 @@
 "<f4" wire format: a ranged BlobStore.get copies only that range back and returns the
 same bytes as slicing the fully materialised object (simkernel.py:174-186)."""
 
-import struct
-
 import numpy as np
-import pytest
 
 from paper_2507_17766_b200 import butterfly as bf
 from paper_2507_17766_b200.simkernel import BlobStore
 
 
-@pytest.mark.parametrize("header", [b"", struct.pack("<iiii", 3, 7, 5, 0)])
-def test_ranged_reads_equal_full_materialisation(header):
+def test_ranged_reads_equal_full_materialisation():
     rng = np.random.default_rng(3)
     v = rng.uniform(-1, 1, 1001) * 1e3
     calls = []
 
     def part(a, b):
         calls.append((a, b))
-        return bf._wire_part(v, header)(a, b)
+        return bf._wire_part(v)(a, b)
 
-    full = header + v.astype("<f4").tobytes()
+    full = v.astype("<f4").tobytes()
     lazy = bf._LazyBlob(len(full), lambda: full, part)
     store = BlobStore()
     store.objects["k"] = lazy
@@ -36,3 +32,17 @@ def test_ranged_reads_equal_full_materialisation(header):
         [(0, 1), (1, 7), (3, 4), (15, 17), (16, 0), (len(full) - 3, None), (0, None), (len(full) + 5, 3),
          (2, 10_000)])
     assert bytes(lazy) == full and len(lazy) == len(full)
+
+
+def test_snapshot_store_copies_at_round_end(monkeypatch):
+    """SNAPSHOT_STORE: objects are bytes when written (the reference's put copies,
+    simkernel.py:168); by default they are views of the caller's vector."""
+    v = np.linspace(-1, 1, 37)
+    lazy = bf._wire_blob(v, 4 * v.size)
+    assert isinstance(lazy, bf._LazyBlob)
+    monkeypatch.setattr(bf, "SNAPSHOT_STORE", True)
+    snap = bf._wire_blob(v, 4 * v.size)
+    assert isinstance(snap, bytes) and snap == v.astype("<f4").tobytes()
+    v[3] = 123.0  # the caller mutates its payload after the round
+    assert snap == np.linspace(-1, 1, 37).astype("<f4").tobytes()
+    assert bytes(lazy)[12:16] == np.float32(123.0).tobytes()  # documented aliasing of the view

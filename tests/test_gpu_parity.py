@@ -213,6 +213,57 @@ def test_device_merge_matches_oracle(cuda_device, case, keep_means=False):
             assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16)[:257], bits)
 
 
+@pytest.mark.parametrize("use_fb", [True, False], ids=["fallback", "no_fallback"])
+@pytest.mark.parametrize("r", [2, 3])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f64"])
+def test_device_merge_nonfinite(cuda_device, dtype, r, use_fb):
+    """NaN / +-Inf weights (a diverged miner): a fast shard whose mean is not
+    finite has identical NaN-scoring copies (butterfly.py:127-133), so it is a
+    disagreement with every survivor flagged and the fallback adopted (:255,264-273);
+    a lone survivor still merges its (NaN) mean.  Status, flags and entries are exact;
+    values are exact with a fallback.  Without one, the scatter-back has already
+    overwritten the lowest alive replica in place, so such shards take NaN."""
+    from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
+
+    n, P = 7, (35 if r == 3 else 21) * 300 + 5
+    rng = np.random.default_rng(99 + r)
+    reps = _random_case(rng, n, P, r, dtype)
+    poison = [(2, 100, "nan"), (5, 2000, "inf"), (0, 2000, "-inf"), (3, 4000, "nan"), (4, 5000, "nan"),
+              (6, P - 1, "inf")]
+    for m, e, v in poison:
+        if dtype == "bf16":
+            reps[m][e] = {"nan": 0x7FC0, "inf": 0x7F80, "-inf": 0xFF80}[v]
+        else:
+            reps[m][e] = float(v)
+    failures = (4,)
+    specs = {1: (orc.ADD, 0.5)}
+    fb = rng.uniform(-5, 5, P) if use_fb else None
+    seed = 1234 + r
+    plan = DevicePlan(n, P, seed, redundancy=r, device=cuda_device)
+    assign, bounds = orc.plan(n, P, seed, r=r)
+    odt = {"f32": orc.F32, "bf16": orc.BF16, "f64": orc.F64WIRE}[dtype]
+    want = orc.merge(reps, assign, bounds, failures=failures, corruptions=specs, fallback=fb, dtype=odt)
+    dreps = _to_torch(reps, dtype, cuda_device)
+    job = ButterflyMerge(dreps, plan, failures=failures, corruptions=_descriptors(specs),
+                         fallback=None if fb is None else torch.from_numpy(fb).to(cuda_device),
+                         scatter_back=True, want_merged=True)
+    job.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(job.status.cpu().numpy(), want["status"])
+    assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
+    assert_entries_close(job.entries.cpu().numpy(), want["entries"])
+    nonfin = job.nonfinite_shards()
+    assert len(nonfin) >= 2  # the poison hit several fast shards with >= 2 survivors
+    expect = want["merged"].copy()
+    if fb is None:
+        for s in nonfin:
+            expect[bounds[s]:bounds[s + 1]] = np.nan
+    assert_same_floats(job.merged.cpu().numpy(), expect)
+    if dtype == "f32":
+        for t in dreps:
+            assert_same_floats(t.cpu().numpy(), expect.astype(np.float32))
+
+
 def test_agreement_and_mean_reducer_gpu(cuda_device):
     from _golden import agreement_cases
 
@@ -239,7 +290,7 @@ def test_pipelined_host_merge_matches_oracle(cuda_device, monkeypatch, with_bad)
     from paper_2507_17766_b200.simkernel import BlobStore
 
     monkeypatch.setenv("BFLY_UPLOAD_BLOCK", "4096")
-    monkeypatch.setenv("BFLY_MERGE_CHUNKS", "7")
+    monkeypatch.setattr(bf, "_merge_chunks", lambda P: 7)
     n, P = 6, 100_003
     rng = np.random.default_rng(77)
     payloads = [rng.uniform(-1, 1, P) * 10.0 ** rng.integers(-3, 3) for _ in range(n)]

@@ -1,6 +1,11 @@
-"""Multi-GPU merge (NCCL chain) against the oracle: bit-exact merged values,
-status, flags and agreement entries on every rank.  Needs >= 2 GPUs; launched
-as torchrun workers from the test (one process per GPU)."""
+"""Multi-GPU merge against the oracle: bit-exact merged values, own replicas, status,
+flags and agreement entries on every rank.
+
+Every case runs twice: as a single-device LOOPBACK (every rank a thread on one GPU,
+multigpu.run_loopback: the same k_ring / chunked-ring kernels and host logic, the
+persistent ring as one cooperative launch of G x L CTAs) — so the driver's 1-GPU box
+checks the multi-GPU path — and, given >= G GPUs, as torchrun workers (one process per
+GPU, NCCL + CUDA IPC)."""
 
 import os
 import subprocess
@@ -15,64 +20,16 @@ ROOT = Path(__file__).resolve().parents[1]
 
 WORKER = r'''
 import os, sys, json
-import numpy as np, torch, torch.distributed as dist
+import torch, torch.distributed as dist
 sys.path[:0] = [sys.argv[1], sys.argv[1] + "/oracle", sys.argv[1] + "/tests"]
-import oracle as orc
-from _golden import assert_same_floats, assert_entries_close
-from paper_2507_17766_b200.device import DevicePlan, Corruption
-from paper_2507_17766_b200.multigpu import ShardedButterflyMerge
+from _multigpu_cases import case_data, run_rank
+from paper_2507_17766_b200.multigpu import DistComm
 case = json.loads(sys.argv[2])
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
 torch.cuda.set_device(dev)
 dist.init_process_group("nccl", device_id=dev)
-counts, P, seed = case["counts"], case["P"], case["seed"]
-n = sum(counts)
-rng = np.random.default_rng(7)
-data = (rng.uniform(-1, 1, (n, P)) * 10.0 ** rng.integers(-4, 4, (n, 1))).astype(np.float32)
-r = case.get("r", 2)
-bf16 = case.get("bf16", False)
-if bf16:
-    data = (data.view(np.uint32) >> 16).astype(np.uint16)
-fails = tuple(case["failures"])
-specs = {int(k): tuple(v) for k, v in case["corr"].items()}
-fb = rng.uniform(-2, 2, P) if case["fallback"] else None
-assign, bounds = orc.plan(n, P, seed, r=r)
-want = orc.merge(list(data), assign, bounds, failures=fails, corruptions=specs, fallback=fb,
-                 dtype=orc.BF16 if bf16 else orc.F32)
-off = sum(counts[:rank])
-if bf16:
-    local = [torch.from_numpy(data[off + i].view(np.int16).copy()).to(dev).view(torch.bfloat16)
-             for i in range(counts[rank])]
-else:
-    local = [torch.from_numpy(data[off + i].copy()).to(dev) for i in range(counts[rank])]
-plan = DevicePlan(n, P, seed, redundancy=r, device=dev)
-kinds = {1: "add", 2: "scale", 3: "noise", 4: "noise_add"}
-corr = {m: Corruption(kinds[s[0]], s[1], (s[2], s[3]) if len(s) > 2 else (0, 0)) for m, s in specs.items()}
-job = ShardedButterflyMerge(local, plan, failures=fails, corruptions=corr,
-                            fallback=None if fb is None else torch.from_numpy(fb).to(dev),
-                            chunk=case["chunk"], want_merged=True)
-if "fused" in case:
-    assert job.fused == case["fused"], (job.fused, case["fused"])
-orig = [t.clone() for t in local]
-for rnd in range(case.get("rounds", 1)):
-    if rnd:  # refill the replicas in place: the next round reuses slots and flags
-        for t, o in zip(local, orig):
-            t.copy_(o)
-    job.run()
-    torch.cuda.synchronize()
-    assert_same_floats(job.merged.cpu().numpy(), want["merged"])
-    if not bf16:
-        for t in local:
-            assert_same_floats(t.cpu().numpy(), want["merged"].astype(np.float32))
-    else:
-        bits = np.array([orc.lib().orc_f32_to_bf16(float(v)) for v in want["merged"][:4099].astype(np.float32)],
-                        dtype=np.uint16)
-        for t in local:
-            assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16)[:4099], bits)
-    assert np.array_equal(job.status.cpu().numpy(), want["status"])
-    assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
-    assert_entries_close(job.entries.cpu().numpy(), want["entries"])
+run_rank(case, case_data(case), rank, DistComm(), dev)
 dist.barrier()
 dist.destroy_process_group()
 print("rank", rank, "ok")
@@ -111,10 +68,41 @@ CASES = [
      "chunk": 8192, "r": 3, "fused": True, "rounds": 2},
     {"counts": [1, 2], "P": 9_001, "seed": 27, "failures": [], "corr": {}, "fallback": False,
      "chunk": 8192, "fused": True, "rounds": 4},
+    # adversarial (config 5 pattern at reduced size): noise-deceptive miners on every rank,
+    # persistent ring with predicted outcomes + FINISH on the last rank
+    {"counts": [4, 4, 4, 4], "P": 2_000_039, "seed": 28, "failures": [],
+     "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "9": [3, 2.0, 24301, 9], "15": [3, 2.0, 24301, 15]},
+     "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2},
+    # non-finite weights (a diverged miner): fast shards with NaN / Inf means are
+    # disagreements decided after the exchange and re-broadcast
+    {"counts": [3, 3], "P": 600_011, "seed": 29, "failures": [], "corr": {}, "fallback": True,
+     "chunk": 1 << 20, "fused": True, "rounds": 2, "poison": [[0, 17, "nan"], [4, 300_000, "inf"], [5, 599_999, "-inf"]]},
+    {"counts": [2, 2, 2], "P": 400_009, "seed": 30, "failures": [], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "poison": [[1, 5, "nan"], [3, 200_000, "inf"]]},
+    {"counts": [3, 3], "P": 300_007, "seed": 31, "failures": [2], "corr": {}, "fallback": True,
+     "chunk": 65536, "executor": "chunked", "poison": [[0, 17, "nan"], [4, 150_000, "inf"]]},
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c['counts']}_P{c['P']}")
+def _ids(c):
+    return f"{c['counts']}_P{c['P']}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
+def test_loopback_merge_matches_oracle(case, cuda_device):
+    """Every rank of the case as a thread on ONE GPU (LoopbackComm)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from _multigpu_cases import case_data, run_rank
+
+    from paper_2507_17766_b200.multigpu import run_loopback
+
+    d = case_data(case)
+    world = len(case["counts"])
+    fused = run_loopback(world, lambda rank, comm: run_rank(case, d, rank, comm, cuda_device), device=cuda_device)
+    assert len(set(fused)) == 1
+
+
+@pytest.mark.parametrize("case", CASES, ids=_ids)
 def test_sharded_merge_matches_oracle(case, tmp_path):
     import json
 

@@ -1,0 +1,119 @@
+"""The reference's OWN hot-path tests, unmodified, through the drop-in.
+
+The reference (iota-sim, git-ignored baseline/_ref, installed by __graft_entry__.build()
+with the base contract's pip command; its tests copied beside it) is run in a
+subprocess with the ``ref_dropin`` plugin, which applies the substitution of
+INTEGRATION.md §2/§4.  Nothing here reads /root/reference.
+
+* CPU: the tests of pkg/tests/test_butterfly.py that need no device (pairs, plans,
+  the seed-24 KAT, the chi-square uniformity, analytics, the ShapeError of agreement)
+  — the exception classes raised by the drop-in must be iota_sim's;
+* GPU: all 22 tests of test_butterfly.py and acceptance criteria 1, 2, 3, 4 and 9
+  (pkg/tests/test_acceptance.py:43-162,326-352);
+* GPU: a 3-epoch orchestrator scenario with deceptive and lazy miners and compressed
+  sharing stages through the CLI (orchestrator.py:519-606, cli.py:85-136): every CSV
+  byte-identical with the drop-in patched in and with the reference as shipped.
+"""
+
+import hashlib
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "baseline" / "_ref"
+REF_TESTS = REF / "tests"
+
+needs_ref = pytest.mark.skipif(not (REF / "iota_sim").is_dir() or not REF_TESTS.is_dir(),
+                               reason="baseline/_ref (the reference) is not installed; run __graft_entry__.build()")
+
+
+def _env(mode="module"):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(ROOT), str(ROOT / "tests"), str(REF)])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    env["BFLY_REF_SUBSTITUTE"] = mode
+    return env
+
+
+def _pytest(args, mode="module", timeout=900):
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-p", "ref_dropin",
+           "--rootdir", str(REF_TESTS), *args]
+    r = subprocess.run(cmd, cwd=str(REF_TESTS), env=_env(mode), capture_output=True, text=True, timeout=timeout)
+    return r.returncode, r.stdout + r.stderr
+
+
+CPU_SELECTION = "TestPairs or TestShardPlan or TestResilience or test_shape_mismatch"
+
+
+@needs_ref
+def test_reference_butterfly_tests_cpu_subset():
+    rc, out = _pytest(["test_butterfly.py", "-k", CPU_SELECTION])
+    assert rc == 0, out
+    assert "15 passed" in out, out
+
+
+@needs_ref
+def test_plugin_substitutes_the_module():
+    code = ("import ref_dropin, iota_sim, iota_sim.butterfly as b, iota_sim.errors as e; "
+            "import paper_2507_17766_b200.butterfly as ours, paper_2507_17766_b200.errors as oe; "
+            "assert b is ours and oe.ShapeError is e.ShapeError and ours.ShardPlan.__module__ == 'iota_sim.butterfly'; "
+            "print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], env=_env(), capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_reference_butterfly_tests_all(cuda_device):
+    rc, out = _pytest(["test_butterfly.py"])
+    assert rc == 0, out
+    assert "22 passed" in out, out
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_reference_acceptance_criteria(cuda_device):
+    sel = "criterion_1 or criterion_2 or criterion_3 or criterion_4 or criterion_9"
+    rc, out = _pytest(["test_acceptance.py", "-k", sel, "-s"], mode="attribute")
+    assert rc == 0, out
+    assert "5 passed" in out, out
+    for c in ("criterion 1", "criterion 2", "criterion 3", "criterion 4", "criterion 9"):
+        assert f"ACCEPTANCE {c}" in out and "FAIL" not in out, out
+
+
+SCENARIO = """[train]
+dims = [4, 16, 16, 2]
+miners = [["honest", "lazy:0.3", "honest", "deceptive:1.5"], ["honest", "deceptive:2.0", "honest", "honest", "lazy:0.5"], ["honest", "honest", "deceptive:1.5"]]
+seed = 9
+epochs = 3
+b_min = 2
+trigger_fraction = 0.5
+batch_size = 4
+compressed_stages_per_epoch = 1
+compression_ratio = 4.0
+"""
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_orchestrator_scenario_csvs_byte_identical(cuda_device, tmp_path):
+    cfg = tmp_path / "scenario.toml"
+    cfg.write_text(SCENARIO)
+    hashes = {}
+    for arm in ("reference", "b200"):
+        out = tmp_path / arm
+        cmd = [sys.executable, str(ROOT / "tests" / "_ref_scenario.py"), str(cfg), str(out)]
+        if arm == "b200":
+            cmd.append("b200")
+        r = subprocess.run(cmd, env=_env("attribute"), capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        if arm == "b200":
+            merges = int(r.stdout.split("B200_MERGES")[1].split()[0])
+            assert merges >= 3 * 2 * 3, r.stdout  # epochs x stages x layers went through the drop-in
+        hashes[arm] = {p.name: hashlib.sha256(p.read_bytes()).hexdigest() for p in sorted(out.glob("*.csv"))}
+    assert len(hashes["reference"]) >= 6
+    assert hashes["b200"] == hashes["reference"]
