@@ -1,28 +1,34 @@
 #!/usr/bin/env python
 """Benchmark of the butterfly merge (BASELINE.json metric: params merged/sec (GB/s)).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c1..c5]
     python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
 
-Workload (weak scaling, 16 miners per GPU): each GPU holds 16 miner replicas of
-one 1B-parameter pipeline stage (fp32 wire values), redundancy 2.  N=1 is
-BASELINE config 2 (16 miners on one B200); N=4 is config 3's 64 miners of a 1B
-stage; N GPUs merge 16*N miners.  A "step" is one merge round: every shard is
-reduced over the alive replicas (fp64 sequential accumulation in miner order,
-bit-identical to the reference), redundant copies are compared, and the
-adopted slices are scattered back in place into every replica.  Inputs are
-64 GB per GPU, far larger than the 126 MB L2, so no flush is needed.
+Workload.  N=1 (default): BASELINE config 2 — 16 miner replicas of one 1B-parameter
+pipeline stage (fp32 wire values) on one B200, redundancy 2.  N>1 (default): config 3
+— the north star — 64 miners of a 1B stage spread over the N GPUs in contiguous blocks
+(64/N per GPU: strong scaling; N=8 is 8 miners per GPU).  ``--config c2`` keeps 16
+miners per GPU at any N (weak scaling); c5 is c3 (c2 at N=1) with 6 noise-deceptive
+miners; c4 is one 1.75B bf16 r=3 stage per GPU; c1 the reference default (8 x 10M).
 
-``value`` is the whole-job merge bandwidth in GB/s: sum over GPUs of the
-algorithmic bytes (every alive replica read once + every replica written once,
-4 B per parameter) divided by the round time (max over ranks).  The same
-round's params merged/s (P / t) is reported beside it.
+A "step" is one merge round: every shard is reduced over the alive replicas (fp64
+sequential accumulation in miner order, bit-identical to the reference), redundant
+copies are compared, and the adopted slices are scattered back in place into every
+replica.  Inputs are 32-128 GB per GPU, far larger than the 126 MB L2: no flush.
+
+``value`` is the whole-job merge bandwidth in GB/s: the algorithmic bytes over all GPUs
+(every alive replica read once + every replica written once, 4 B per parameter) divided
+by the round time (max over ranks).  P / t (params merged per second) is beside it.
+Multi-GPU lines carry SURVEY §8(d)'s roofline (HBM bytes per GPU at the measured copy
+peak, NVLink bytes h(G-1)Ps + (G-1)/G Ps at 900 GB/s per direction) and the NVLink bytes
+the GPUs' own counters (NVML) saw during the timed rounds.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -36,21 +42,45 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "params merged/sec (GB/s) at 1/2/4/8 B200 vs HBM/NVLink roofline and CPU ref"
 UNIT = "GB/s"
+NVLINK_SPEC_GBPS = 900.0  # per direction per GPU (NVLink 5; PAPER.md:177 cites 900 GB/s)
 
+# name: miners, whether the count is per GPU (weak) or for the whole job (strong),
+# params, replica dtype, redundancy, deceptive miners
 CONFIGS = {
-    # name: (miners per GPU, params, dtype, redundancy, deceptive miners)
-    "c1": (8, 10_000_000, "fp32", 2, 0),
-    "c2": (16, 1_000_000_000, "fp32", 2, 0),
-    "c4": (32, 1_750_000_000, "bf16", 3, 0),
-    "c5": (16, 1_000_000_000, "fp32", 2, 6),
+    "c1": dict(miners=8, per_gpu=False, params=10_000_000, dtype="fp32", r=2, bad=0),
+    "c2": dict(miners=16, per_gpu=True, params=1_000_000_000, dtype="fp32", r=2, bad=0),
+    "c3": dict(miners=64, per_gpu=False, params=1_000_000_000, dtype="fp32", r=2, bad=0),
+    "c4": dict(miners=32, per_gpu=True, params=1_750_000_000, dtype="bf16", r=3, bad=0),
+    "c5": dict(miners=64, per_gpu=False, params=1_000_000_000, dtype="fp32", r=2, bad=6),
 }
 WORKLOAD = {
     "c1": "reference default: 8 miners x 10M fp32, r=2 (BASELINE config 1)",
-    "c2": "1B-param stage, 16 miners per B200 fp32, r=2 (config 2 at N=1, config 3's 64 miners at N=4)",
+    "c2": "1B-param stage, 16 miners per B200 fp32, r=2 (BASELINE config 2 at N=1; weak scaling)",
+    "c3": "1B-param stage, 64 miners fp32 in contiguous blocks over N B200s (64/N per GPU), r=2 "
+          "(BASELINE config 3, the north star; strong scaling)",
     "c4": "14B model / 8 stages: one 1.75B-param stage per GPU, 32 miners bf16 (fp32 acc), r=3 (BASELINE config 4)",
-    "c5": "1B-param stage, 16 miners per GPU, 6 deceptive (noise), r=2 (BASELINE config 5 at N=4)",
+    "c5": "adversarial 1B-param stage: 64 miners over N GPUs (16 on one GPU), 6 noise-deceptive, r=2 "
+          "(BASELINE config 5)",
 }
 BYTES = {"fp32": 4, "bf16": 2}
+
+
+def resolve_config(name, world):
+    """(name, miners per GPU, total miners, params, dtype, r, deceptive)."""
+    if name is None:
+        name = "c2" if world == 1 else "c3"
+    c = CONFIGS[name]
+    if c["per_gpu"]:
+        n_local, n = c["miners"], c["miners"] * world
+    elif world == 1:
+        n = 16 if name in ("c3", "c5") else c["miners"]  # 64 x 4 GB does not fit one GPU
+        n_local = n
+    else:
+        n = c["miners"]
+        if n % world:
+            raise SystemExit(f"{name}: {n} miners do not split over {world} GPUs")
+        n_local = n // world
+    return name, n_local, n, c["params"], c["dtype"], c["r"], c["bad"]
 
 
 def _peaks():

@@ -224,6 +224,11 @@ int bfly_ipc_free(void* d_ptr);
  * the stream waits until (int32)(*d_flag - value) >= 0, flushing remote writes
  * when the device supports it; or writes value to *d_flag (with a memory
  * barrier) once all earlier work in the stream is done. */
+/* A CUDA stream of this process's own (non-blocking, priority as cudaStreamCreateWithPriority):
+ * the multi-GPU executors' streams wait on flags other ranks write, so they must never be
+ * shared with anything else (torch hands out pooled streams, which wrap around). */
+int bfly_stream_create(int32_t priority, void** stream);
+int bfly_stream_destroy(void* stream);
 int bfly_stream_wait_value(const uint32_t* d_flag, uint32_t value, void* stream);
 int bfly_stream_write_value(uint32_t* d_flag, uint32_t value, void* stream);
 

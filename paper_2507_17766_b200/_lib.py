@@ -48,6 +48,8 @@ EXPORTS = (
     "bfly_ipc_open",
     "bfly_ipc_close",
     "bfly_ipc_free",
+    "bfly_stream_create",
+    "bfly_stream_destroy",
     "bfly_stream_wait_value",
     "bfly_stream_write_value",
     "bfly_upload_wire",
@@ -204,6 +206,8 @@ def lib() -> ctypes.CDLL:
     L.bfly_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
     L.bfly_ipc_close.argtypes = [vp]
     L.bfly_ipc_free.argtypes = [vp]
+    L.bfly_stream_create.argtypes = [i32, ctypes.POINTER(vp)]
+    L.bfly_stream_destroy.argtypes = [vp]
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
     L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
@@ -249,3 +253,19 @@ def philox_key(seed: int, stream_id: str) -> tuple[int, int]:
     out = (ctypes.c_uint64 * 2)()
     check(lib().bfly_philox_key(str(int(seed)).encode(), stream_id.encode(), out))
     return int(out[0]), int(out[1])
+
+
+def own_stream(device, priority: int = 0):
+    """A dedicated CUDA stream (bfly_stream_create) wrapped for torch; destroyed with the
+    wrapper.  torch.cuda.Stream() draws from a fixed pool that wraps around, so two
+    "new" streams can be the same CUDA stream — fatal for streams that wait on flags."""
+    import weakref
+
+    import torch
+
+    h = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        check(lib().bfly_stream_create(int(priority), ctypes.byref(h)))
+    s = torch.cuda.ExternalStream(h.value, device=device)
+    weakref.finalize(s, lib().bfly_stream_destroy, ctypes.c_void_p(h.value))
+    return s

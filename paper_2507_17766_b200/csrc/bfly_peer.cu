@@ -109,6 +109,22 @@ int bfly_ipc_free(void* d_ptr) {
   return BFLY_OK;
 }
 
+int bfly_stream_create(int32_t priority, void** out) {
+  if (!out) return fail(BFLY_E_INVALID_ARG, "null stream out");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreateWithPriority");
+  *out = (void*)s;
+  return BFLY_OK;
+}
+
+int bfly_stream_destroy(void* stream) {
+  if (!stream) return BFLY_OK;
+  cudaError_t e = cudaStreamDestroy((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamDestroy");
+  return BFLY_OK;
+}
+
 int bfly_stream_wait_value(const uint32_t* d_flag, uint32_t value, void* stream) {
   int rc = load_driver_ops();
   if (rc) return rc;

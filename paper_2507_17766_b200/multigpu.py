@@ -240,7 +240,7 @@ def run_loopback(world: int, fn, device=None, timeout: float = 300.0) -> list:
     def body(rank):
         try:
             torch.cuda.set_device(dev)
-            with torch.cuda.stream(torch.cuda.Stream(device=dev)):
+            with torch.cuda.stream(L.own_stream(dev)):
                 results[rank] = fn(rank, LoopbackComm(group, rank))
                 torch.cuda.current_stream(dev).synchronize()
         except BaseException as e:  # noqa: BLE001 - re-raised in the caller
@@ -645,10 +645,10 @@ class ShardedButterflyMerge:
     def _setup_ring(self):
         self.layout = lay = _Region(self.chunk, self.esize)
         self._open_region(lay.total)
-        self._relay = torch.cuda.Stream(device=self.dev)
+        self._relay = L.own_stream(self.dev)
         # last rank: per-chunk late shards, high priority so a chunk's decision does not queue
         # behind the next chunk's reduce CTAs (the relay waits for it)
-        self._late = torch.cuda.Stream(device=self.dev, priority=-1)
+        self._late = L.own_stream(self.dev, priority=-1)
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk

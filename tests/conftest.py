@@ -4,6 +4,12 @@ from pathlib import Path
 
 import pytest
 
+# The single-device loopback of the multi-GPU ring runs every rank's streams on one GPU;
+# the chunked executor's streams wait on flags (cuStreamWaitValue32), which must not
+# share a hardware queue with the work that writes them: one queue per stream (set before
+# the CUDA context exists).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parents[1]
 for p in (str(ROOT), str(ROOT / "oracle")):
     if p not in sys.path:
