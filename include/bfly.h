@@ -224,6 +224,11 @@ int bfly_ipc_free(void* d_ptr);
  * the stream waits until (int32)(*d_flag - value) >= 0, flushing remote writes
  * when the device supports it; or writes value to *d_flag (with a memory
  * barrier) once all earlier work in the stream is done. */
+/* Load every kernel of the merge and of the chunked multi-GPU ring now (CUDA lazy loading
+ * would load each at its first launch, which can wait for the device: fatal when several
+ * ranks share one device and their streams already wait on each other — the loopback). */
+int bfly_preload(void);
+
 /* A CUDA stream of this process's own (non-blocking, priority as cudaStreamCreateWithPriority):
  * the multi-GPU executors' streams wait on flags other ranks write, so they must never be
  * shared with anything else (torch hands out pooled streams, which wrap around). */

@@ -48,6 +48,7 @@ EXPORTS = (
     "bfly_ipc_open",
     "bfly_ipc_close",
     "bfly_ipc_free",
+    "bfly_preload",
     "bfly_stream_create",
     "bfly_stream_destroy",
     "bfly_stream_wait_value",
@@ -255,17 +256,23 @@ def philox_key(seed: int, stream_id: str) -> tuple[int, int]:
     return int(out[0]), int(out[1])
 
 
-def own_stream(device, priority: int = 0):
-    """A dedicated CUDA stream (bfly_stream_create) wrapped for torch; destroyed with the
-    wrapper.  torch.cuda.Stream() draws from a fixed pool that wraps around, so two
-    "new" streams can be the same CUDA stream — fatal for streams that wait on flags."""
-    import weakref
+_STREAMS: dict = {}  # (device index, priority, role) -> stream handle, kept for the process lifetime
 
+
+def own_stream(device, priority: int = 0, role=None):
+    """The dedicated CUDA stream of ``role`` on ``device`` (bfly_stream_create), wrapped for
+    torch.  torch.cuda.Stream() draws from a fixed pool that wraps around, so two "new"
+    streams can be the same CUDA stream — fatal for streams that wait on flags other
+    ranks write.  One stream per (device, priority, role), created once and never
+    destroyed (torch's caching allocator remembers the stream of every block)."""
     import torch
 
-    h = ctypes.c_void_p()
-    with torch.cuda.device(device):
-        check(lib().bfly_stream_create(int(priority), ctypes.byref(h)))
-    s = torch.cuda.ExternalStream(h.value, device=device)
-    weakref.finalize(s, lib().bfly_stream_destroy, ctypes.c_void_p(h.value))
-    return s
+    dev = torch.device(device)
+    key = (dev.index, int(priority), role)
+    h = _STREAMS.get(key)
+    if h is None:
+        hv = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            check(lib().bfly_stream_create(int(priority), ctypes.byref(hv)))
+        h = _STREAMS[key] = hv.value
+    return torch.cuda.ExternalStream(h, device=dev)

@@ -1172,8 +1172,9 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   if (!a->d_assign || !a->d_failed || !a->d_corr || !a->d_status || !a->d_entries || !a->d_flagged)
     return fail(BFLY_E_INVALID_ARG, "missing required device array");
   if (a->n_alive > 0 && !a->d_src) return fail(BFLY_E_INVALID_ARG, "missing replicas");
-  if (a->n_alive == 0 && a->n_div > 0 && !a->d_acc_in && a->phase != BFLY_PHASE_FINISH)
-    return fail(BFLY_E_INVALID_ARG, "n_div without replicas");  // (FINISH reads no replica sums)
+  if (a->n_alive == 0 && a->n_div > 0 && !a->d_acc_in && a->phase != BFLY_PHASE_FINISH &&
+      a->phase != BFLY_PHASE_CHECK)
+    return fail(BFLY_E_INVALID_ARG, "n_div without replicas");  // (FINISH / CHECK read no replica sums)
   if (a->n_dst > 0 && !a->d_dst) return fail(BFLY_E_INVALID_ARG, "missing scatter-back targets");
   if (!a->d_merged && !a->d_ws) return fail(BFLY_E_INVALID_ARG, "need d_merged or d_ws");
   ScratchLayout L;
@@ -1377,6 +1378,29 @@ int bfly_tune_reduce(const bfly_merge_args_t* a, int variant, int grid_per_sm, v
   return BFLY_OK;
 }
 #endif
+
+// Load every kernel a merge round (single-GPU or a rank of the chunked ring) may launch.
+// With CUDA's lazy module loading a kernel's first launch loads it, and a load may wait
+// for the device: on ONE device running several ranks (the loopback ring) whose streams
+// already wait on each other's flags, that first launch would deadlock.
+int bfly_preload(void) {
+  const void* fns[] = {
+      (const void*)k_fill_nan, (const void*)k_classify, (const void*)k_stats, (const void*)k_decide,
+      (const void*)k_entries3, (const void*)k_apply<DF32>, (const void*)k_apply<DBF16>,
+      (const void*)k_apply<DF64W>, (const void*)k_nonfinite<DF32>, (const void*)k_nonfinite<DBF16>,
+      (const void*)k_nonfinite<DF64W>, (const void*)k_reduce<DF32, 4, 3, true>,
+      (const void*)k_reduce<DBF16, 8, 1, true>, (const void*)k_reduce<DF64W>, (const void*)k_chain<DF32, true>,
+      (const void*)k_chain<DF32, false>, (const void*)k_chain<DBF16, true>, (const void*)k_chain<DBF16, false>,
+      (const void*)k_chain<DF64W, true>, (const void*)k_chain<DF64W, false>, (const void*)k_ranges<true>,
+      (const void*)k_ranges<false>, (const void*)k_fanout, (const void*)k_fanout_bulk,
+      (const void*)k_agree_partial, (const void*)k_agree_final, (const void*)k_corrupt, (const void*)k_mean_rows};
+  for (const void* f : fns) {
+    cudaFuncAttributes at;
+    cudaError_t e = cudaFuncGetAttributes(&at, f);
+    if (e != cudaSuccess) return cuda_fail(e, "bfly_preload");
+  }
+  return BFLY_OK;
+}
 
 int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
                     double* d_acc_out, int64_t begin, int64_t end, void* stream) {

@@ -145,6 +145,7 @@ class LoopbackComm:
 
     def __init__(self, group: LoopbackGroup, rank: int):
         self.group, self.rank, self.world = group, rank, group.world
+        L.check(L.lib().bfly_preload())  # no lazy kernel load while the ranks' streams wait on each other
 
     def _exchange(self, obj) -> list:
         g = self.group
@@ -240,7 +241,7 @@ def run_loopback(world: int, fn, device=None, timeout: float = 300.0) -> list:
     def body(rank):
         try:
             torch.cuda.set_device(dev)
-            with torch.cuda.stream(L.own_stream(dev)):
+            with torch.cuda.stream(L.own_stream(dev, role=("loopback", rank))):
                 results[rank] = fn(rank, LoopbackComm(group, rank))
                 torch.cuda.current_stream(dev).synchronize()
         except BaseException as e:  # noqa: BLE001 - re-raised in the caller
@@ -645,10 +646,10 @@ class ShardedButterflyMerge:
     def _setup_ring(self):
         self.layout = lay = _Region(self.chunk, self.esize)
         self._open_region(lay.total)
-        self._relay = L.own_stream(self.dev)
+        self._relay = L.own_stream(self.dev, role=("relay", self.rank))
         # last rank: per-chunk late shards, high priority so a chunk's decision does not queue
         # behind the next chunk's reduce CTAs (the relay waits for it)
-        self._late = L.own_stream(self.dev, priority=-1)
+        self._late = L.own_stream(self.dev, priority=-1, role=("late", self.rank))
         Z = self.world - 1
         g = self.rank
         # per (chunk, slot) scatter-back tables: the last rank pushes the final chunk
@@ -772,7 +773,7 @@ class ShardedButterflyMerge:
                     if not ev.query() and op[1] not in stuck:
                         stuck[op[1]] = op
                 flags = torch.empty(len(rs.FLAGS) * NB, dtype=torch.int32, device=self.dev)
-                side = torch.cuda.Stream(device=self.dev)
+                side = L.own_stream(self.dev, role=("watch", self.rank))
                 with torch.cuda.stream(side):
                     L.lib().bfly_fanout(self._base + self.layout.flags,
                                         self._table([flags]).data_ptr(), 1, 4 * len(rs.FLAGS) * NB, side.cuda_stream)

@@ -93,3 +93,55 @@ def test_multigpu_host_collectives_gloo(world):
     out = mp.get_context("spawn").Manager().dict()  # no fork of a multi-threaded process
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert [out[r] for r in range(world)] == [1] * world
+
+
+def test_loopback_comm_exchanges_between_threads():
+    """The single-device loopback transport (multigpu.LoopbackComm): every rank's thread
+    sees every rank's object in rank order; min-reductions agree; a failing rank breaks
+    the others' barriers instead of hanging them."""
+    import threading
+
+    from paper_2507_17766_b200.multigpu import LoopbackComm, LoopbackGroup
+
+    world = 4
+    group = LoopbackGroup(world, timeout=30)
+    out = [None] * world
+
+    def body(rank):
+        comm = LoopbackComm(group, rank)
+        got = comm.all_gather_object(("rank", rank))
+        low = comm.all_reduce_min(10 - rank, None)
+        comm.barrier()
+        again = comm.all_gather_object(rank * rank)
+        out[rank] = (got, low, again)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for rank in range(world):
+        got, low, again = out[rank]
+        assert got == [("rank", r) for r in range(world)]
+        assert low == 10 - (world - 1)
+        assert again == [r * r for r in range(world)]
+
+    group = LoopbackGroup(2, timeout=30)
+    errs = [None, None]
+
+    def bad(rank):
+        comm = LoopbackComm(group, rank)
+        try:
+            if rank == 1:
+                group.barrier.abort()  # what run_loopback does when a rank raises
+                return
+            comm.barrier()
+        except threading.BrokenBarrierError as e:
+            errs[rank] = e
+
+    ts = [threading.Thread(target=bad, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=60)
+    assert isinstance(errs[0], threading.BrokenBarrierError)
