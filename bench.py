@@ -140,9 +140,91 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NVLinkCounter:
+    """NVLink bytes this GPU sent and received, from its own counters (NVML field values
+    summed over all links): read before and after the timed rounds."""
+
+    # (tx field, rx field, bytes per unit): NVLINK_COUNT_XMIT/RCV_BYTES, else the older
+    # NVLINK_THROUGHPUT_DATA_TX/RX counters (KiB)
+    FIELDS = ((202, 204, 1), (138, 139, 1024))
+    ALL_LINKS = 0xFFFFFFFF
+
+    def __init__(self, index: int):
+        self.ok, self.why = False, None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(index)
+            self.field = None
+            for tx, rx, unit in self.FIELDS:
+                if self._read_fields(tx, rx) is not None:
+                    self.field = (tx, rx, unit)
+                    break
+            self.ok = self.field is not None
+            if not self.ok:
+                self.why = "NVML NVLink byte counters unavailable on this GPU/driver"
+        except Exception as e:  # no NVML: reported, not fatal
+            self.why = f"NVML: {e}"
+
+    def _read_fields(self, tx, rx):
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, [(tx, self.ALL_LINKS), (rx, self.ALL_LINKS)])
+        if any(v.nvmlReturn != 0 for v in vals):
+            return None
+        return [int(v.value.ullVal) for v in vals]
+
+    def read(self):
+        if not self.ok:
+            return None
+        tx, rx, unit = self.field
+        v = self._read_fields(tx, rx)
+        return None if v is None else (v[0] * unit, v[1] * unit)
+
+
 # ---------------------------------------------------------------------------
-# CPU oracle timing (cpu_baseline and --impl reference)
+# CPU timing: the reference itself (baseline/_ref) and its C restatement (oracle/)
 # ---------------------------------------------------------------------------
+
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_sample(n, p_cpu, reps, warmup=1):
+    """Time the unmodified reference, iota_sim.butterfly.run_all_reduce (butterfly.py:161-295)
+    from baseline/_ref, on fp64 payloads with a fresh BlobStore per call: a list of seconds
+    per call (None when the reference is not installed)."""
+    if not (REF_DIR / "iota_sim").is_dir():
+        return None
+    sys.path.insert(0, str(REF_DIR))
+    import numpy as np
+    from iota_sim import butterfly as ref
+    from iota_sim.simkernel import BlobStore as RefStore
+
+    rng = np.random.default_rng(0)  # the reference tests' recipe (tests/test_butterfly.py:106-108)
+    payloads = {m: rng.uniform(-1.0, 1.0, p_cpu) for m in range(n)}
+    plan = ref.plan_shards(ref.enumerate_pairs(n), p_cpu, ref.BYTES_PER_WEIGHT, 0)
+    for _ in range(warmup):
+        ref.run_all_reduce(RefStore(), payloads, plan)
+    times = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        ref.run_all_reduce(RefStore(), payloads, plan)
+        times.append(time.perf_counter() - t)
+    return times
+
+
+def reference_params(n, params):
+    """The bounded sample of the workload the Python reference merges per step: P_cpu =
+    2^24 at 16 miners, scaled down with the miner count so a step stays
+    ~3 s, and never more than the workload itself (config 1 runs in full)."""
+    p = min(params, 1 << 24, max(1 << 20, (1 << 28) // max(n, 1)))
+    return params if params <= 10_000_000 else p
+
+
+def cpu_env():
+    return {"os_cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "blas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "default")}
+
 
 
 def _oracle():
@@ -209,8 +291,9 @@ def deceptive_set(n, k, seed=0):
     return sorted(int(x) for x in np.random.default_rng(seed).choice(n, k, replace=False)) if k else []
 
 
-def timed_rounds(step, args, dev):
-    """W untimed rounds, then K rounds between CUDA events on the current stream."""
+def timed_rounds(step, args, dev, nvlink=None):
+    """W untimed rounds, then K rounds between CUDA events on the current stream (and the
+    GPU's NVLink byte counters read on both sides, when given)."""
     import torch
 
     for _ in range(args.warmup):
@@ -218,17 +301,22 @@ def timed_rounds(step, args, dev):
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = None
     with ClockSampler(dev.index or 0) as clk:
         if torch.distributed.is_initialized():
             torch.distributed.barrier()
         torch.cuda.synchronize()
+        c0 = nvlink.read() if nvlink is not None else None
         t0.record(stream)
         kernel_ms = [step(timed=True) for _ in range(args.steps)]
         t1.record(stream)
         torch.cuda.synchronize()
+        c1 = nvlink.read() if nvlink is not None else None
+        if c0 is not None and c1 is not None:
+            nvl = (c1[0] - c0[0], c1[1] - c0[1])
         if torch.distributed.is_initialized():
             torch.distributed.barrier()
-    return t0.elapsed_time(t1), kernel_ms, clk.summary()
+    return t0.elapsed_time(t1), kernel_ms, clk.summary(), nvl
 
 
 def run_single(cfg, args, dev):
@@ -237,7 +325,7 @@ def run_single(cfg, args, dev):
     from paper_2507_17766_b200 import _lib as L
     from paper_2507_17766_b200.device import ButterflyMerge, Corruption, DevicePlan
 
-    n, P, dtype, r, k_bad = cfg
+    name, _, n, P, dtype, r, k_bad = cfg
     reps = make_replicas(n, P, dtype, dev)
     plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
     corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in deceptive_set(n, k_bad)}
@@ -256,7 +344,7 @@ def run_single(cfg, args, dev):
         events.append((a, b))
         return None
 
-    total_ms, _, clocks = timed_rounds(step, args, dev)
+    total_ms, _, clocks, _ = timed_rounds(step, args, dev)
     torch.cuda.synchronize()
     reduce_ms = statistics.mean(a.elapsed_time(b) for a, b in events)
     status = job.status.cpu()
@@ -294,7 +382,28 @@ def run_e2e_resident(job, args):
     return dt, h2d, d2h
 
 
-def run_e2e(n, r, args, dev, p_e2e):
+def e2e_params(n, params, requested):
+    """Parameters per payload of the end-to-end leg: the workload's own when the host can
+    hold n fp64 payloads (pinned) with room to spare, else the largest power of two that
+    fits (stated in the line)."""
+    if requested:
+        return requested, "requested"
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    need = n * params * 8
+    if need * 1.6 < avail:
+        return params, "the workload's full size"
+    p = 1 << 27
+    while p * 2 * n * 8 * 1.6 < avail and p * 2 <= params:
+        p *= 2
+    return p, f"host RAM {avail / 2**30:.0f} GiB holds {n} x {p} fp64 payloads, not {n} x {params}"
+
+
+def run_e2e(n, r, args, dev, p_e2e, why):
     """The drop-in API (butterfly.run_all_reduce) on fp64 payloads in host memory: the
     fp32 wire conversion + H2D of every payload and the D2H of the merged vector are
     inside every step."""
@@ -330,6 +439,7 @@ def run_e2e(n, r, args, dev, p_e2e):
         "h2d_bytes_per_step": n * p_e2e * 4 + S * 2 * 4 + n + n * 32,
         "d2h_bytes_per_step": p_e2e * 8 + S + n * n * 8 + n + S * 4,
         "params": p_e2e,
+        "params_why": why,
         "params_merged_per_s": p_e2e / dt,
         "ms_per_step": dt * 1e3,
         "path": "paper_2507_17766_b200.butterfly.run_all_reduce(BlobStore(), {miner: fp64 payload in pinned "
@@ -337,6 +447,18 @@ def run_e2e(n, r, args, dev, p_e2e):
         "bound": "host: %.1f GB of fp64 payloads converted to the fp32 wire on host threads, %.1f GB H2D"
                  % (n * p_e2e * 8 / 1e9, n * p_e2e * 4 / 1e9),
     }
+
+
+def contract_roofline(n, n_local, world, P, esize, hbm_peak, r=2):
+    """per GPU B_HBM = 2 n_g P s; NVLink bytes into a GPU
+    B_NVL = h (G-1) P s + (G-1)/G P s with h = 1 - C(N - N/G, r) / C(N, r); t_roof = max."""
+    b_hbm = 2 * n_local * P * esize
+    if world == 1:
+        return dict(b_hbm=b_hbm, b_nvl=0.0, t_roof=b_hbm / (hbm_peak * 1e9), bound="hbm", h=0.0)
+    h = 1.0 - math.comb(n - n // world, r) / math.comb(n, r)
+    b_nvl = h * (world - 1) * P * esize + (world - 1) / world * P * esize
+    t_h, t_n = b_hbm / (hbm_peak * 1e9), b_nvl / (NVLINK_SPEC_GBPS * 1e9)
+    return dict(b_hbm=b_hbm, b_nvl=b_nvl, t_roof=max(t_h, t_n), bound="hbm" if t_h >= t_n else "nvlink", h=h)
 
 
 def run_multi(cfg, args, rank, world):
@@ -350,53 +472,60 @@ def run_multi(cfg, args, rank, world):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     dist.init_process_group("nccl", device_id=dev)
-    n_local, P, dtype, r, k_bad = cfg
-    n = n_local * world
-    if args.max_ctas:
-        from paper_2507_17766_b200 import _lib as L
-
-        L.check(L.lib().bfly_set_max_ctas(args.max_ctas))
+    name, n_local, n, P, dtype, r, k_bad = cfg
     reps = make_replicas(n_local, P, dtype, dev, seed=rank * n_local)
     plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
     bad = deceptive_set(n, k_bad)
     corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in bad}
     job = ShardedButterflyMerge(reps, plan, corruptions=corr, chunk=args.chunk)
+    nvcount = NVLinkCounter(local_rank)
 
     def step(timed=False):
         job.run()
         return None
 
-    total_ms, _, clocks = timed_rounds(step, args, dev)
+    total_ms, _, clocks, nvl = timed_rounds(step, args, dev, nvlink=nvcount)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     t_step = total_ms / args.steps / 1e3
     esize = BYTES[dtype]
-    if job.timing:
-        job.run()
-        print(f"[rank {rank}] phases (ms): " + json.dumps({k: round(v, 3) for k, v in job.timings.items()}),
-              file=sys.stderr, flush=True)
+    # measured NVLink bytes per round: max over ranks of what a GPU received / sent
+    meas = torch.tensor([-1.0, -1.0] if nvl is None else [float(nvl[1]), float(nvl[0])], dtype=torch.float64,
+                        device=dev)
+    dist.all_reduce(meas, op=dist.ReduceOp.MAX)
     nb = job.bytes_per_round()
-    nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
-    dist.all_reduce(nvl, op=dist.ReduceOp.MAX)
+    impl_nvl = torch.tensor([nb["nvlink_in"]], dtype=torch.float64, device=dev)
+    dist.all_reduce(impl_nvl, op=dist.ReduceOp.MAX)
     lt = torch.tensor([job.launches_per_run() * args.steps], dtype=torch.int64, device=dev)
     dist.all_reduce(lt)  # every rank's kernels: the whole job's launches
     launches = int(lt.item())
+    disagree = int((job.status == 2).sum().item())
     e2e = None if args.no_e2e else run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0)
     if rank == 0:
         peaks = _peaks()
-        hbm_peak = peaks.get("hbm_gbs", 6650.0)
+        hbm_peak = peaks.get("hbm_gbs", 6550.0)
         alg = merge_bytes(n, P, esize)
         value = alg / t_step / 1e9
-        per_gpu_hbm = merge_bytes(n_local, P, esize)
-        nvl_peak = 770.0
-        t_roof = max(per_gpu_hbm / (hbm_peak * 1e9), float(nvl.item()) / (nvl_peak * 1e9))
+        roof = contract_roofline(n, n_local, world, P, esize, hbm_peak, r)
+        if roof["bound"] == "hbm":
+            achieved, peak, unit_peak = roof["b_hbm"] / t_step / 1e9, hbm_peak, "HBM copy peak (MEASURED_PEAKS.json)"
+        else:
+            achieved, peak, unit_peak = roof["b_nvl"] / t_step / 1e9, NVLINK_SPEC_GBPS, "NVLink 5 spec per direction"
+        impl_t = max(roof["b_hbm"] / (hbm_peak * 1e9), float(impl_nvl.item()) / (NVLINK_SPEC_GBPS * 1e9))
+        rx, tx = float(meas[0].item()), float(meas[1].item())
+        measured = None if rx < 0 else {
+            "rx_bytes_per_round": rx / args.steps, "tx_bytes_per_round": tx / args.steps,
+            "rx_GBps": rx / args.steps / t_step / 1e9, "tx_GBps": tx / args.steps / t_step / 1e9,
+            "rx_frac_of_spec": rx / args.steps / t_step / 1e9 / NVLINK_SPEC_GBPS,
+            "source": "NVML NVLink byte counters (all links) read before/after the timed rounds; max over ranks"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "weak" if CONFIGS[name]["per_gpu"] else "strong",
             "vs_baseline": None, "dtype": "f64" if dtype == "fp32" else "f32",
             "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
-            "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "miners_per_gpu": n_local,
+            "config": {"workload": WORKLOAD[name], "config": name, "miners": n, "miners_per_gpu": n_local,
                        "params": P, "replica_dtype": dtype, "redundancy": r, "deceptive": len(bad),
                        "parallelism": (f"miners in contiguous blocks over {world} GPUs; one persistent kernel per "
                                        f"GPU (k_ring): fp64 running sums chained rank to rank tile by tile through "
@@ -407,23 +536,25 @@ def run_multi(cfg, args, rank, world):
                                        f"up to {args.chunk}-element chunks), final vector relayed round the ring"),
                        "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n_local * P * esize / 1e9)},
             "params_merged_per_s": P / t_step,
-            "roofline": {"bound": "hbm" if per_gpu_hbm / hbm_peak > float(nvl.item()) / nvl_peak else "nvlink",
-                         "achieved": per_gpu_hbm / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": t_roof / t_step, "traffic": None,
+            "roofline": {"bound": roof["bound"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": unit_peak,
                          "kernel": ("whole round per GPU (k_ring: one persistent kernel)" if job.fused else
                                     "whole round per GPU (chain / reduce / fan-out kernels + NVLink ring)"),
-                         "t_roof_ms": t_roof * 1e3, "hbm_bytes_per_gpu": per_gpu_hbm,
-                         "nvlink_bytes_in_per_gpu": float(nvl.item()),
-                         # algorithmic NVLink bytes into the busiest rank / round time, against
-                         # the 900 GB/s per-direction spec (770 GB/s measured peer copy)
-                         "nvlink_achieved_GBps": float(nvl.item()) / t_step / 1e9,
-                         "nvlink_frac_of_spec": float(nvl.item()) / t_step / 900e9,
-                         "peaks": {"hbm_GBps": hbm_peak, "nvlink_GBps_per_direction": nvl_peak,
-                                   "source": "MEASURED_PEAKS.json hbm_gbs; NVLink 770 GB/s measured peer copy "
-                                             "(B200_PROFILING.md)"}},
+                         "contract": "SURVEY §8(d): t_roof = max(2 n_g P s / BW_HBM, "
+                                     "(h (G-1) P s + (G-1)/G P s) / 900 GB/s)",
+                         "t_roof_ms": roof["t_roof"] * 1e3, "h": roof["h"],
+                         "hbm_bytes_per_gpu": roof["b_hbm"], "nvlink_bytes_in_per_gpu": roof["b_nvl"],
+                         "impl": {"nvlink_bytes_in_per_gpu": float(impl_nvl.item()),
+                                  "note": "this implementation's exchange: fp64 running sums (8 B/param) into every "
+                                          "rank > 0 plus the final vector (s B/param) into every rank < last, "
+                                          "which keeps the reference's summation order bit for bit",
+                                  "t_roof_ms": impl_t * 1e3, "frac": impl_t / t_step}},
+            "nvlink_measured": measured if measured else {"unavailable": nvcount.why},
             "e2e": e2e, "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks,
+            "disagreement_shards": disagree,
         }
         print(json.dumps(line))
+    job.close()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -443,7 +574,7 @@ def run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0):
     from paper_2507_17766_b200.device import DevicePlan, _stream_handle
     from paper_2507_17766_b200.multigpu import ShardedButterflyMerge
 
-    P = min(args.e2e_params, 1 << 26)
+    P = min(args.e2e_params or (1 << 26), 1 << 26)
     host = []
     g = torch.Generator()
     for i in range(n_local):
@@ -490,11 +621,13 @@ def run_stages(cfg, args, rank, world):
 
     from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
 
+    distributed = world > 1
     local_rank = int(os.environ.get("LOCAL_RANK", rank))
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    dist.init_process_group("nccl", device_id=dev)
-    n, P, dtype, r, _ = cfg
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev)
+    _, n, _, P, dtype, r, _ = cfg
     reps = make_replicas(n, P, dtype, dev, seed=1000 * rank)
     plan = DevicePlan(n, P, rank, redundancy=r, device=dev)
     job = ButterflyMerge(reps, plan, scatter_back=True)
@@ -502,21 +635,23 @@ def run_stages(cfg, args, rank, world):
     def step(timed=False):
         job.run()
 
-    total_ms, _, clocks = timed_rounds(step, args, dev)
+    total_ms, _, clocks, _ = timed_rounds(step, args, dev)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item()) / args.steps / 1e3
     if rank == 0:
         esize = BYTES[dtype]
         alg = world * merge_bytes(n, P, esize)
-        hbm_peak = _peaks().get("hbm_gbs", 6650.0)
+        hbm_peak = _peaks().get("hbm_gbs", 6550.0)
         line = {
             "metric": METRIC, "value": alg / t_step / 1e9, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic uniform(-1,1) bf16 replicas (torch Philox)",
-            "config": {"workload": WORKLOAD["c4"], "miners_per_stage": n, "params_per_stage": P, "stages": world,
-                       "replica_dtype": dtype, "redundancy": r, "parallelism": "one stage per GPU (replicas only)",
+            "config": {"workload": WORKLOAD["c4"], "config": "c4", "miners_per_stage": n, "params_per_stage": P,
+                       "stages": world, "replica_dtype": dtype, "redundancy": r,
+                       "parallelism": "one stage per GPU (replicas only)",
                        "l2": "inputs %.2f GB per GPU >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
             "params_merged_per_s": world * P / t_step,
             "roofline": {"bound": "hbm", "achieved": merge_bytes(n, P, esize) / t_step / 1e9, "peak": hbm_peak,
@@ -526,36 +661,51 @@ def run_stages(cfg, args, rank, world):
             "clocks": clocks,
         }
         print(json.dumps(line))
-    dist.barrier()
-    dist.destroy_process_group()
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def run_reference(cfg, args, rank, world):
-    """--impl reference: the CPU restatement of the reference's run_all_reduce
-    (oracle/bfly_oracle.c, all host threads) on fp64 payloads — the reference API's
-    input — for a bounded sample of the same workload, one merge per step."""
+    """--impl reference: the reference's own CPU implementation of the path,
+    iota_sim.butterfly.run_all_reduce from baseline/_ref (unmodified, installed with the
+    base contract's pip command), timed on this host for a bounded sample of the same
+    workload (same miner count, P_cpu parameters), one merge per step.  Its C restatement
+    (oracle/, all host threads) is timed beside it and reported as a labelled second
+    figure.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
-    n_local, P, dtype, r, _ = cfg
-    n = n_local * world
-    p_cpu = args.cpu_params
-    for _ in range(args.warmup):
-        cpu_sample(n, p_cpu, dtype, r, dtype == "fp32")
-    times, threads = cpu_sample(n, p_cpu, dtype, r, dtype == "fp32", reps=args.steps)
-    t_step = statistics.mean(times)
-    value = merge_bytes(n, p_cpu, BYTES[dtype]) / t_step / 1e9
+    name, _, n, P, dtype, r, k_bad = cfg
+    esize = BYTES[dtype]
+    p_cpu = args.cpu_params or reference_params(n, P)
+    times = reference_sample(n, p_cpu, reps=args.steps, warmup=args.warmup) if r == 2 and dtype == "fp32" else None
+    port_times, port_threads = cpu_sample(n, p_cpu, dtype, r, dtype == "fp32", reps=max(1, min(args.steps, 5)))
+    port = {"value": merge_bytes(n, p_cpu, esize) / statistics.mean(port_times) / 1e9, "unit": UNIT,
+            "cores": port_threads, "kind": "port", "ms_per_step": statistics.mean(port_times) * 1e3,
+            "sample": f"oracle/bfly_oracle.c: C restatement of run_all_reduce (OpenMP, {port_threads} threads), "
+                      f"{n} miners x {p_cpu} params as fp64 payloads -> fp32 wire -> fp64 mean"}
+    if times is not None:
+        t_step = statistics.mean(times)
+        value = merge_bytes(n, p_cpu, esize) / t_step / 1e9
+        kind, cores = "reference", 1
+        sample = (f"iota_sim.butterfly.run_all_reduce (baseline/_ref, unmodified; numpy, 1 effective core) on "
+                  f"{n} fp64 payloads x {p_cpu} params (of the workload's {P}), fresh BlobStore per step; "
+                  f"best {min(times) * 1e3:.0f} ms")
+    else:  # bf16 / r = 3 (config 4): no reference implementation exists; the port is the arm
+        t_step = statistics.mean(port_times)
+        value, kind, cores = port["value"], "port", port_threads
+        sample = port["sample"] + " (no reference implementation of this extension config)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64" if dtype == "fp32" else "f32",
-        "data": "synthetic uniform(-1,1) payloads",
-        "config": {"workload": WORKLOAD[args.config or "c2"], "miners": n, "params": p_cpu,
-                   "sampled_from_params": P, "redundancy": r},
+        "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "weak" if CONFIGS[name]["per_gpu"] else "strong", "vs_baseline": None,
+        "dtype": "f64" if dtype == "fp32" else "f32", "data": "synthetic uniform(-1,1) payloads",
+        "config": {"workload": WORKLOAD[name], "config": name, "miners": n, "params": p_cpu,
+                   "sampled_from_params": P, "redundancy": r, "deceptive": k_bad},
         "params_merged_per_s": p_cpu / t_step,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"oracle/bfly_oracle.c restatement of run_all_reduce (OpenMP, {threads} threads), "
-                                   f"{n} miners x {p_cpu} params as fp64 payloads -> fp32 wire -> fp64 mean, "
-                                   f"one merge per step"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+                         "host": cpu_env()},
+        "port": port,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -567,35 +717,39 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: c2 on one GPU, c3 (the north star) on several")
     ap.add_argument("--params", type=int, default=None, help="override the stage size")
     ap.add_argument("--chunk", type=int, default=1 << 24)
-    ap.add_argument("--max-ctas", type=int, default=0, help="cap streaming-kernel CTAs (multi-GPU)")
-    ap.add_argument("--e2e-params", type=int, default=1 << 27)
-    ap.add_argument("--cpu-params", type=int, default=1 << 25)
+    ap.add_argument("--e2e-params", type=int, default=None, help="default: the workload's size if host RAM allows")
+    ap.add_argument("--cpu-params", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    name = args.config or "c2"
-    cfg = list(CONFIGS[name])
+    cfg = list(resolve_config(args.config, world))
     if args.params:
-        cfg[1] = args.params
+        cfg[3] = args.params
     cfg = tuple(cfg)
+    name = cfg[0]
     if args.impl == "reference":
         return run_reference(cfg, args, rank, world)
+    if name == "c4":
+        return run_stages(cfg, args, rank, world)
     if world > 1:
-        return run_stages(cfg, args, rank, world) if name == "c4" else run_multi(cfg, args, rank, world)
+        return run_multi(cfg, args, rank, world)
 
     import torch
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    n, P, dtype, r, k_bad = cfg
+    _, _, n, P, dtype, r, k_bad = cfg
     info, resident = run_single(cfg, args, dev)
     peaks = _peaks()
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = peaks.get("hbm_gbs", 6550.0)
     t_step = info["total_ms"] / args.steps / 1e3
     esize = BYTES[dtype]
     alg = (info["n_alive"] + n) * P * esize  # read every alive replica once, write every replica once
@@ -605,23 +759,35 @@ def main():
     else:
         kernel_ms, kernel_name = info["reduce_ms"], "k_reduce (event window also holds k_fill_nan + k_classify, < 10 us)"
     achieved = alg / (kernel_ms / 1e3) / 1e9
-    e2e = None if args.no_e2e else run_e2e(n, r, args, dev, args.e2e_params)
+    e2e = None
+    if not args.no_e2e:
+        p_e2e, why = e2e_params(n, P, args.e2e_params)
+        e2e = run_e2e(n, r, args, dev, p_e2e, why)
     cpu = None
     if not args.no_cpu:
-        times, threads = cpu_sample(n, args.cpu_params, dtype, r, False, reps=2)
-        secs = min(times)
-        cpu = {"value": merge_bytes(n, args.cpu_params, esize) / secs / 1e9, "unit": UNIT, "cores": threads,
-               "kind": "port", "params_merged_per_s": args.cpu_params / secs,
-               "sample": f"oracle/bfly_oracle.c (C restatement of run_all_reduce, OpenMP {threads} threads) on "
-                         f"host-resident {dtype} replicas, {n} miners x {args.cpu_params} params, best of 2 "
-                         f"({secs * 1e3:.1f} ms per merge)"}
+        p_cpu = args.cpu_params or reference_params(n, P)
+        ref_times = reference_sample(n, p_cpu, reps=2) if r == 2 and dtype == "fp32" else None
+        port_times, threads = cpu_sample(n, p_cpu, dtype, r, False, reps=2)
+        port = {"value": merge_bytes(n, p_cpu, esize) / min(port_times) / 1e9, "unit": UNIT, "cores": threads,
+                "kind": "port", "ms_per_step": min(port_times) * 1e3,
+                "sample": f"oracle/bfly_oracle.c (C restatement of run_all_reduce, OpenMP {threads} threads) on "
+                          f"host-resident {dtype} replicas, {n} miners x {p_cpu} params, best of 2"}
+        if ref_times:
+            secs = min(ref_times)
+            cpu = {"value": merge_bytes(n, p_cpu, esize) / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "params_merged_per_s": p_cpu / secs,
+                   "sample": f"iota_sim.butterfly.run_all_reduce (baseline/_ref, unmodified; 1 effective core) on "
+                             f"{n} fp64 payloads x {p_cpu} params, best of 2 ({secs * 1e3:.0f} ms per merge)",
+                   "host": cpu_env(), "port": port}
+        else:
+            cpu = port
     rt, h2d, d2h = resident
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64" if dtype == "fp32" else "f32",
         "data": "synthetic uniform(-1,1) replicas (torch Philox, seed = miner index)",
-        "config": {"workload": WORKLOAD[name], "miners": n, "params": P, "replica_dtype": dtype,
+        "config": {"workload": WORKLOAD[name], "config": name, "miners": n, "params": P, "replica_dtype": dtype,
                    "redundancy": r, "deceptive": k_bad, "parallelism": "single GPU",
                    "l2": "inputs %.2f GB >> 126 MB L2, no flush" % (n * P * esize / 1e9)},
         "params_merged_per_s": P / t_step,

@@ -159,7 +159,9 @@ def merge(replicas, assign, bounds, *, failures=(), corruptions=None, fallback=N
 def noise_values(key0: int, key1: int, amp: float, start: int, stop: int) -> np.ndarray:
     """The NOISE descriptor's values on elements [start, stop) — numpy form of
     orc_noise: word e of Philox(key).random_raw, mapped to amp * (2u - 1)."""
-    raw = np.random.Philox(key=np.array([key0, key1], dtype=np.uint64)).random_raw(stop)[start:stop]
+    bg = np.random.Philox(key=np.array([key0, key1], dtype=np.uint64))
+    bg.advance(start // 4)  # word e lives in the 4-word block e // 4 (no need to draw the words before it)
+    raw = bg.random_raw(stop - (start // 4) * 4)[start % 4:]
     unit = (raw >> np.uint64(11)).astype(np.float64) * (1.0 / 4503599627370496.0) - 1.0
     return amp * unit
 

@@ -145,7 +145,6 @@ class LoopbackComm:
 
     def __init__(self, group: LoopbackGroup, rank: int):
         self.group, self.rank, self.world = group, rank, group.world
-        L.check(L.lib().bfly_preload())  # no lazy kernel load while the ranks' streams wait on each other
 
     def _exchange(self, obj) -> list:
         g = self.group
@@ -241,6 +240,7 @@ def run_loopback(world: int, fn, device=None, timeout: float = 300.0) -> list:
     def body(rank):
         try:
             torch.cuda.set_device(dev)
+            L.check(L.lib().bfly_preload())  # no lazy kernel load while the ranks' streams wait on each other
             with torch.cuda.stream(L.own_stream(dev, role=("loopback", rank))):
                 results[rank] = fn(rank, LoopbackComm(group, rank))
                 torch.cuda.current_stream(dev).synchronize()

@@ -67,3 +67,60 @@ def test_config2_full_size_properties(cuda_device):
     torch.cuda.synchronize()
     assert torch.equal(reps[7][idx], snap)
     assert torch.equal(reps[3][: 1 << 20], reps[12][: 1 << 20])
+
+
+def test_config5_full_size_sampled_shards(cuda_device):
+    """Config 5 at full size: 16 miners x 1e9 fp32, 6 noise-deceptive
+    miners (the bench's pattern: np.random.default_rng(0).choice(16, 6), noise amplitude 2
+    keyed per miner).  Sampled shards — deceptive and honest ones — are snapshotted before
+    the round and re-decided with the oracle's primitives (butterfly.py:216-273): the
+    sequential fp64 mean in miner order, each assignee's copy (noise keyed by the global
+    element index, orc.noise_values), orc.agreement, adoption or the lowest alive
+    replica's values.  merged, status, entries and scatter-back must match bit for bit
+    (entries <= 1e-12); the closed forms C(16,2) - C(10,2) = 75 disagreements and
+    every miner flagged (each honest miner shares a shard with each deceptive one) hold."""
+    from paper_2507_17766_b200.device import ButterflyMerge, Corruption, DevicePlan
+
+    free, _ = torch.cuda.mem_get_info()
+    n, P, amp = 16, 1_000_000_000, 2.0
+    if free < (n + 6) * P * 4:
+        pytest.skip("needs ~90 GB of free HBM")
+    bad = sorted(int(x) for x in np.random.default_rng(0).choice(n, 6, replace=False))
+    keys = {m: (0x5EED, m) for m in bad}
+    g = torch.Generator(device=cuda_device)
+    reps = []
+    for m in range(n):
+        g.manual_seed(m)
+        reps.append(torch.empty(P, dtype=torch.float32, device=cuda_device).uniform_(-1, 1, generator=g))
+    plan = DevicePlan(n, P, 0, device=cuda_device)
+    assign, bounds = orc.plan(n, P, 0)
+    assert np.array_equal(plan.assign.cpu().numpy(), assign)
+    special = [s for s in range(len(assign)) if set(assign[s]) & set(bad)]
+    fast = [s for s in range(len(assign)) if s not in special]
+    rng = np.random.default_rng(5)
+    sample = sorted(set(rng.choice(special, 6, replace=False).tolist()) |
+                    set(rng.choice(fast, 3, replace=False).tolist()) | {0, len(assign) - 1})
+    snap = {s: [r[bounds[s]:bounds[s + 1]].cpu().numpy() for r in reps] for s in sample}
+    job = ButterflyMerge(reps, plan, corruptions={m: Corruption.noise(amp, keys[m]) for m in bad},
+                         scatter_back=True, want_merged=True)
+    job.run()
+    torch.cuda.synchronize()
+    status = job.status.cpu().numpy()
+    entries = job.entries.cpu().numpy()
+    assert int((status == orc.DISAGREEMENT).sum()) == 75 == len(special)
+    assert np.array_equal(np.flatnonzero(status == orc.DISAGREEMENT), np.array(special))
+    assert int(job.flagged.sum()) == n
+    for s in sample:
+        lo, hi = int(bounds[s]), int(bounds[s + 1])
+        acc = np.zeros(hi - lo)
+        for m in range(n):  # numpy's mean order: sequential fp64 sum in miner order, one divide
+            acc = acc + snap[s][m].astype(np.float64)
+        mean = acc / n
+        i, j = (int(x) for x in assign[s])
+        copy = {x: (orc.noise_values(*keys[x], amp, lo, hi) if x in bad else mean) for x in (i, j)}
+        score = orc.agreement(copy[i], copy[j])
+        want = copy[min(i, j)] if score == 1.0 else snap[s][0].astype(np.float64)
+        assert status[s] == (orc.MERGED if score == 1.0 else orc.DISAGREEMENT), s
+        assert abs(entries[i, j] - score) <= 1e-12 and entries[i, j] == entries[j, i], s
+        assert_same_floats(job.merged[lo:hi].cpu().numpy(), want)
+        assert_same_floats(reps[n - 1][lo:hi].cpu().numpy(), want.astype(np.float32))
