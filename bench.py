@@ -589,7 +589,7 @@ def run_e2e_multi(n_local, n, r, args, dev, rank, world, plan_seed=0):
     outs = [torch.empty_like(t, device="cpu").pin_memory() for t in (job.status, job.flagged, job.entries)]
 
     def step():
-        L.check(L.lib().bfly_upload_wire(h_ptrs, n_local, P, d_ptrs, threads, _stream_handle()))
+        L.check(L.lib().bfly_upload_wire(h_ptrs, n_local, P, d_ptrs, threads, 0, _stream_handle()))
         job.run()
         for o, d in zip(outs, (job.status, job.flagged, job.entries)):
             o.copy_(d, non_blocking=True)

@@ -173,29 +173,14 @@ int bfly_merge(const bfly_merge_args_t* args, void* stream);
 int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, const double* d_acc_in,
                     double* d_acc_out, int64_t begin, int64_t end, void* stream);
 
-/* Cap the grid of the streaming kernels (k_reduce, k_chain, k_fanout) at max_ctas
- * CTAs (0 = no cap, the default).  The multi-GPU merge leaves SMs to the NCCL
- * kernels that move the running sums, so transfers overlap the HBM stream. */
-int bfly_set_max_ctas(int32_t max_ctas);
-
-/* k_chain writes its fp64 sums through shared-memory staging and TMA bulk stores
- * (cp.async.bulk.global.shared::cta) when on != 0 (the default), else with 256-bit
- * SM stores.  Into a peer GPU's inbox the bulk stores are 1.5x faster (16 replicas
- * x 16M elements: 0.21 vs 0.32 ms on B200, tools/peer_bw.py). */
-int bfly_set_chain_bulk(int32_t on);
-
-/* Fan-out stores through TMA bulk copies (32 KB tiles staged in shared memory, one
- * cp.async.bulk per destination) instead of 256-bit stores; default off. */
-int bfly_set_fanout_bulk(int32_t on);
-
 /* Upload n fp64 host payloads of P elements (pageable or pinned) as fp32 wire
  * values ("<f4", butterfly.py:213) into the device buffers d_wire[i]: `threads`
- * host threads (0 = all cores) convert into a pinned staging ring while earlier
- * slots are copied, so conversion and PCIe overlap.  Returns when the last copy
- * has been issued on `stream` (the host payloads may be reused after the
- * stream reaches that point). */
+ * host threads (0 = all cores) convert blocks of `block` elements (0 = 512 Ki, 2 MB
+ * copies) into a ring of pinned staging slots while earlier slots are copied, so
+ * conversion and PCIe overlap.  Returns when the last copy has been issued on
+ * `stream` (the host payloads may be reused after the stream reaches that point). */
 int bfly_upload_wire(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
-                     int32_t threads, void* stream);
+                     int32_t threads, int64_t block, void* stream);
 
 /* The drop-in merge of host payloads as one pipeline (run_all_reduce's upload +
  * reduce stages, butterfly.py:205-240, and the copy of the merged vector back):
@@ -207,7 +192,7 @@ int bfly_upload_wire(const double* const* h_payloads, int32_t n, int64_t P, floa
  * copies those shards' merged values again). */
 int bfly_merge_host(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
                     const bfly_merge_args_t* args, double* h_merged, int32_t n_chunks, int32_t threads,
-                    void* stream);
+                    int64_t block, void* stream);
 
 /* ---- peer memory for the multi-GPU merge (one process per GPU, one node) ---- */
 /* cudaMalloc a zero-filled region and export its CUDA IPC handle (64 bytes). */

@@ -42,8 +42,6 @@ EXPORTS = (
     "bfly_chain_step",
     "bfly_fanout",
     "bfly_copy_ranges",
-    "bfly_set_max_ctas",
-    "bfly_set_chain_bulk",
     "bfly_ipc_alloc",
     "bfly_ipc_open",
     "bfly_ipc_close",
@@ -56,7 +54,6 @@ EXPORTS = (
     "bfly_upload_wire",
     "bfly_merge_host",
     "bfly_replay_check",
-    "bfly_set_fanout_bulk",
     "bfly_ipc_export",
     "bfly_ring_round",
     "bfly_ring_ops",
@@ -200,8 +197,6 @@ def lib() -> ctypes.CDLL:
     L.bfly_mean_rows.argtypes = [vp, i32, i64, vp, vp]
     L.bfly_chain_step.argtypes = [vp, i32, i32, vp, vp, i64, i64, vp]
     L.bfly_fanout.argtypes = [vp, vp, i32, i64, vp]
-    L.bfly_set_max_ctas.argtypes = [i32]
-    L.bfly_set_chain_bulk.argtypes = [i32]
     u32 = ctypes.c_uint32
     L.bfly_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
     L.bfly_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
@@ -211,11 +206,10 @@ def lib() -> ctypes.CDLL:
     L.bfly_stream_destroy.argtypes = [vp]
     L.bfly_stream_wait_value.argtypes = [vp, u32, vp]
     L.bfly_stream_write_value.argtypes = [vp, u32, vp]
-    L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, vp]
-    L.bfly_set_fanout_bulk.argtypes = [i32]
+    L.bfly_upload_wire.argtypes = [vp, i32, i64, vp, i32, i64, vp]
     L.bfly_ipc_export.argtypes = [vp, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.bfly_replay_check.argtypes = [vp, vp, vp, i32, vp, vp, vp, vp]
-    L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, vp]
+    L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, i64, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
     L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]

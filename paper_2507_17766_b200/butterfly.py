@@ -459,7 +459,7 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         # vector back run as one pipeline (bfly_merge_host) once the job exists
         pipelined = not callables
         if not pipelined:
-            L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _stream_handle()))
+            L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _UPLOAD_BLOCK, _stream_handle()))
         for m, t in zip(alive, wire):
             reps[m] = t
         unmerged_possible = len(failed) >= 2 or bool(descriptors) or bool(callables)
@@ -493,7 +493,7 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True) if early else None  # cached pinned
         L.check(L.lib().bfly_merge_host(h_ptrs, len(alive), P, d_ptrs, ctypes.byref(job._args),
                                         merged_host.data_ptr() if early else None, _merge_chunks(P), 0,
-                                        _stream_handle()))
+                                        _UPLOAD_BLOCK, _stream_handle()))
         if job.needs_finish():
             job.run(L.PHASE_FINISH)
     else:
@@ -591,6 +591,9 @@ def _render_special(job, plan, failed, descriptors, classes, host_reductions, no
         out[(s, x)] = flat[o:o + hi - lo].astype("<f4").tobytes()
         o += hi - lo
     return out
+
+
+_UPLOAD_BLOCK = 0  # elements per staging block of the host upload (0: the library's 512 Ki)
 
 
 def _merge_chunks(P: int) -> int:

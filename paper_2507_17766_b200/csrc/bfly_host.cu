@@ -33,39 +33,22 @@ namespace {
 // itself, so no thread ever waits for another.  Blocks are small enough that the
 // ring's lines are still in the host's last-level cache when the copy engine reads
 // them back: the host memory traffic stays near the 8 B/element of the fp64 read.
-int64_t env_int(const char* name, int64_t dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoll(v) : dflt;
-}
+constexpr int64_t kDefaultBlock = 1 << 19;  // 2 MB copies: tools/upload_probe.py
+constexpr int kRing = 3;                     // staging slots per worker
 
 struct Worker {
   std::vector<float*> slot;
   std::vector<cudaEvent_t> done;
-  std::vector<double*> raw;  // device ring for blocks copied as fp64 and converted on the GPU
   cudaStream_t stream = nullptr;
   cudaEvent_t fin = nullptr;
-  int64_t count = 0, raw_count = 0;
+  int64_t count = 0;
 };
 
-// fp64 payload block (copied raw) -> fp32 wire values, RNE like numpy's astype
-__global__ void k_wire(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = __double2float_rn(src[i]);
-}
-
-// One block of one payload onto the device, by this worker: converted on the host into a
-// pinned slot and copied, or (raw) copied as fp64 into a device slot and converted there.
-// Raw blocks cost 8 B of PCIe per element but no host write / re-read: mixing them in
-// balances host-memory traffic (16 B per converted element) against PCIe (4 B).
-cudaError_t upload_block(Worker& w, int ring, const double* src, float* dst, int64_t len, bool raw) {
-  if (raw) {
-    const int k = (int)(w.raw_count++ % ring);
-    cudaError_t ce = cudaMemcpyAsync(w.raw[k], src, sizeof(double) * len, cudaMemcpyHostToDevice, w.stream);
-    if (ce != cudaSuccess) return ce;
-    const int64_t grid = std::min<int64_t>((len + 255) / 256, 1024);
-    k_wire<<<(unsigned)grid, 256, 0, w.stream>>>(w.raw[k], dst, len);
-    return cudaGetLastError();
-  }
+// One block of one payload onto the device, by this worker: converted on the host into
+// its next pinned slot (once that slot's previous copy has left) and copied.  (Copying
+// some blocks raw as fp64 and converting on the GPU — PCIe traded for host-memory
+// traffic — was measured slower: profiles/r01_upload_probe_raw_blocks.log.)
+cudaError_t upload_block(Worker& w, int ring, const double* src, float* dst, int64_t len) {
   const int k = (int)(w.count++ % ring);
   cudaError_t ce = cudaEventSynchronize(w.done[k]);  // the slot's previous copy has left
   if (ce != cudaSuccess) return ce;
@@ -74,20 +57,6 @@ cudaError_t upload_block(Worker& w, int ring, const double* src, float* dst, int
   ce = cudaMemcpyAsync(dst, slot, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
   if (ce != cudaSuccess) return ce;
   return cudaEventRecord(w.done[k], w.stream);
-}
-
-// every `raw_every`-th block goes raw when all payloads are page-locked (0: never)
-int raw_every_for(const double* const* h, int32_t n) {
-  const int64_t every = env_int("BFLY_UPLOAD_RAW_EVERY", 0);  // off: measured slower (profiles/)
-  if (every <= 0) return 0;
-  for (int32_t m = 0; m < n; ++m) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, h[m]) != cudaSuccess || at.type != cudaMemoryTypeHost) {
-      cudaGetLastError();
-      return 0;
-    }
-  }
-  return (int)every;
 }
 
 struct Pool {
@@ -101,13 +70,13 @@ struct Pool {
 std::mutex g_pool_mu;
 std::vector<Pool*> g_pools;  // one per (device, shape), kept for the process lifetime
 
-int get_pool(int threads, Pool** out) {
+int get_pool(int threads, int64_t block, Pool** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  const int64_t block = env_int("BFLY_UPLOAD_BLOCK", 1 << 19);  // 2 MB copies: tools/upload_probe.py
-  const int ring = (int)env_int("BFLY_UPLOAD_RING", 3);
-  if (block < 1024 || ring < 2) return fail(BFLY_E_INVALID_ARG, "bad BFLY_UPLOAD_BLOCK / BFLY_UPLOAD_RING");
+  if (block == 0) block = kDefaultBlock;
+  const int ring = kRing;
+  if (block < 1024) return fail(BFLY_E_INVALID_ARG, "upload block must be >= 1024 elements");
   std::lock_guard<std::mutex> lk(g_pool_mu);
   for (Pool* p : g_pools)
     if (p->device == dev && p->block == block && p->ring == ring && (int)p->workers.size() >= threads) {
@@ -128,11 +97,6 @@ int get_pool(int threads, Pool** out) {
       e = cudaEventCreateWithFlags(&w.done[i], cudaEventDisableTiming);
       if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
-    w.raw.resize(ring);
-    for (int i = 0; i < ring; ++i) {
-      e = cudaMalloc((void**)&w.raw[i], sizeof(double) * block);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc raw staging");
-    }
     e = cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     e = cudaEventCreateWithFlags(&w.fin, cudaEventDisableTiming);
@@ -150,16 +114,15 @@ int get_pool(int threads, Pool** out) {
 using namespace bfly;
 
 extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
-                                int32_t threads, void* stream) {
+                                int32_t threads, int64_t block, void* stream) {
   if (!h_payloads || !d_wire || n < 0 || P < 0) return fail(BFLY_E_INVALID_ARG, "bad upload arguments");
   if (n == 0 || P == 0) return BFLY_OK;
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
   Pool* pool = nullptr;
-  int rc = get_pool(threads, &pool);
+  int rc = get_pool(threads, block, &pool);
   if (rc) return rc;
   std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
-  const int raw_every = raw_every_for(h_payloads, n);
   // the copies must not start before work already queued on the caller's stream
   // (e.g. a previous round still reading the destination buffers)
   cudaEvent_t start;
@@ -178,8 +141,7 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
     for (int64_t id = next.fetch_add(1); id < total && err.load() == BFLY_OK; id = next.fetch_add(1)) {
       const int32_t m = (int32_t)(id / per);
       const int64_t b = (id % per) * B, len = std::min<int64_t>(B, P - b);
-      const bool raw = raw_every > 0 && id % raw_every == raw_every - 1;
-      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len, raw);
+      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len);
       if (ce != cudaSuccess) {
         std::lock_guard<std::mutex> lk(err_mu);
         err_msg = cudaGetErrorString(ce);
@@ -204,17 +166,16 @@ extern "C" int bfly_upload_wire(const double* const* h_payloads, int32_t n, int6
 // workers convert and upload the next chunks (PCIe is full duplex).
 extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64_t P, float* const* d_wire,
                                const bfly_merge_args_t* args, double* h_merged, int32_t n_chunks, int32_t threads,
-                               void* stream) {
+                               int64_t block, void* stream) {
   if (!h_payloads || !d_wire || !args || n < 1 || P < 1 || n_chunks < 1)
     return fail(BFLY_E_INVALID_ARG, "bad merge-host arguments");
   if (h_merged && !args->d_merged) return fail(BFLY_E_INVALID_ARG, "h_merged needs d_merged");
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
   Pool* pool = nullptr;
-  int rc = get_pool(threads, &pool);
+  int rc = get_pool(threads, block, &pool);
   if (rc) return rc;
   std::lock_guard<std::mutex> busy(pool->busy);
   cudaStream_t st = (cudaStream_t)stream;
-  const int raw_every = raw_every_for(h_payloads, n);
   const int64_t B = pool->block;
   int64_t CL = (P + n_chunks - 1) / n_chunks;
   CL = (CL + B - 1) / B * B;  // chunk = whole blocks
@@ -266,8 +227,7 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
       const int32_t m = (int32_t)(local / nb);
       const int64_t b = (int64_t)c * CL + (local % nb) * B;
       const int64_t len = std::min<int64_t>(B, (int64_t)c * CL + chunk_len(c) - b);
-      const bool raw = raw_every > 0 && id % raw_every == raw_every - 1;
-      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len, raw);
+      cudaError_t ce = upload_block(w, pool->ring, h_payloads[m] + b, d_wire[m] + b, len);
       if (ce != cudaSuccess) set_err(ce);
     }
     pass(NC);

@@ -1102,15 +1102,13 @@ __global__ void k_mean_rows(const double* stack, int32_t rows, int64_t width, do
 
 using namespace bfly;
 
-// Optional cap on the CTAs of the streaming kernels (bfly_set_max_ctas): with one
-// resident CTA per SM it leaves SMs free for concurrent NCCL kernels.
-static int g_max_ctas = 0;
-static int g_chain_bulk = 1;  // k_chain stores through TMA bulk copies (bfly_set_chain_bulk)
-static int g_fanout_bulk = 0;  // k_fanout stores through TMA bulk copies (bfly_set_fanout_bulk)
-static int64_t cap_grid(int64_t grid) {
-  if (g_max_ctas > 0 && grid > g_max_ctas) grid = g_max_ctas;
-  return grid < 1 ? 1 : grid;
-}
+// k_chain stores its fp64 sums through shared-memory staging and TMA bulk stores: into a
+// peer GPU's inbox 1.5x faster than 256-bit SM stores (16 replicas x 16M elements: 0.21 vs
+// 0.32 ms, tools/peer_bw.py).  k_fanout uses 256-bit SM stores (its bulk variant, 32 KB
+// tiles staged in shared memory, was no faster: profiles/r01_fanout_probe.log).
+constexpr bool kChainBulk = true;
+constexpr bool kFanoutBulk = false;
+static int64_t cap_grid(int64_t grid) { return grid < 1 ? 1 : grid; }
 
 template <class D, int U = 4, int MINB = 1, bool NOU = false>
 static void launch_reduce(const Params& p, cudaStream_t st, int grid_per_sm = 8) {
@@ -1418,7 +1416,7 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, kThreads, smem, st>>>(d_src, n_src, d_acc_in, d_acc_out, begin, end);
   };
-  const bool bulk = g_chain_bulk != 0;
+  const bool bulk = kChainBulk;
   switch (dtype) {
     case BFLY_F32: bulk ? go(k_chain<DF32, true>, DF32::K, true) : go(k_chain<DF32, false>, DF32::K, false); break;
     case BFLY_BF16:
@@ -1454,26 +1452,10 @@ int bfly_copy_ranges(const void* d_full, void* d_packed, void* const* d_dst, int
   return BFLY_OK;
 }
 
-int bfly_set_chain_bulk(int32_t on) {
-  g_chain_bulk = on ? 1 : 0;
-  return BFLY_OK;
-}
-
-int bfly_set_max_ctas(int32_t max_ctas) {
-  if (max_ctas < 0) return fail(BFLY_E_INVALID_ARG, "max_ctas must be >= 0");
-  g_max_ctas = max_ctas;
-  return BFLY_OK;
-}
-
-int bfly_set_fanout_bulk(int32_t on) {
-  g_fanout_bulk = on ? 1 : 0;
-  return BFLY_OK;
-}
-
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream) {
   if (!d_src || n_dst < 0 || (n_dst > 0 && !d_dst) || nbytes < 0) return fail(BFLY_E_INVALID_ARG, "bad fanout arguments");
   if (n_dst == 0 || nbytes == 0) return BFLY_OK;
-  if (g_fanout_bulk) {
+  if (kFanoutBulk) {
     int64_t grid = nbytes / kFanTile;
     if (grid > (int64_t)sm_count() * 3) grid = (int64_t)sm_count() * 3;
     grid = cap_grid(grid);

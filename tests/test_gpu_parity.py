@@ -289,7 +289,7 @@ def test_pipelined_host_merge_matches_oracle(cuda_device, monkeypatch, with_bad)
     from paper_2507_17766_b200.device import Corruption
     from paper_2507_17766_b200.simkernel import BlobStore
 
-    monkeypatch.setenv("BFLY_UPLOAD_BLOCK", "4096")
+    monkeypatch.setattr(bf, "_UPLOAD_BLOCK", 4096)
     monkeypatch.setattr(bf, "_merge_chunks", lambda P: 7)
     n, P = 6, 100_003
     rng = np.random.default_rng(77)

@@ -1,6 +1,6 @@
 """Diagnostics of the persistent multi-GPU ring (k_ring, csrc/bfly_ring.cu).
 
-    BFLY_RING_PROFILE=1 torchrun --nproc-per-node G tools/ring_fused_probe.py [P] [miners_per_gpu]
+    torchrun --nproc-per-node G tools/ring_fused_probe.py [P] [miners_per_gpu] [profile]
 
 Times a few rounds with CUDA events (max over ranks) and prints, per rank, the
 share of the kernel's cycles each role spent waiting (mean over CTAs):
@@ -10,7 +10,6 @@ flag, stage read-out, landing), relay loader (ready flag, stage free), relay
 storer (stage full, downstream free flag, read-out, landing).
 """
 
-import ctypes
 import json
 import os
 import sys
@@ -21,7 +20,6 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 
-from paper_2507_17766_b200 import _lib as L  # noqa: E402
 from paper_2507_17766_b200.device import DevicePlan  # noqa: E402
 from paper_2507_17766_b200.multigpu import ShardedButterflyMerge  # noqa: E402
 
@@ -45,6 +43,10 @@ def main():
     plan = DevicePlan(n_local * world, P, 0, device=dev)
     job = ShardedButterflyMerge(reps, plan)
     assert job.fused
+    profile = len(sys.argv) > 3 and sys.argv[3] == "profile"
+    prof = torch.zeros(job.lanes * 24, dtype=torch.int64, device=dev) if profile else None
+    if profile:  # the descriptor's diagnostics buffer (bfly.h d_profile)
+        job._fdesc.d_profile = prof.data_ptr()
     for _ in range(2):
         job.run()
     torch.cuda.synchronize()
@@ -59,11 +61,8 @@ def main():
     ms = torch.tensor([ev[0].elapsed_time(ev[1]) / rounds], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     out = {"rank": rank, "round_ms": round(float(ms.item()), 3), "lanes": job.lanes}
-    if os.environ.get("BFLY_RING_PROFILE"):
-        n = job.lanes * 24
-        buf = (ctypes.c_ulonglong * n)()
-        L.lib().bfly_ring_fused_profile(buf, n)
-        a = np.frombuffer(buf, dtype=np.uint64).reshape(job.lanes, 24).astype(np.float64)
+    if profile:
+        a = prof.cpu().numpy().view(np.uint64).reshape(job.lanes, 24).astype(np.float64)
         tot = a[:, 7].mean()
         out["kernel_ms_at_1.9GHz"] = round(tot / 1.9e6, 3)
         out["wait_share"] = {NAMES[k]: round(a[:, k].mean() / tot, 3) for k in range(24)
