@@ -169,12 +169,23 @@ struct DF64W {
 
 // Sequential accumulation of one 32-byte vector per thread over the replica
 // table, U replicas' loads in flight before their adds (the add order stays
-// ascending, which is what parity needs).
-template <class D, int U = 4, bool NO_OUTER_UNROLL = false>
+// ascending, which is what parity needs).  FIRST: also hand back replica 0's raw
+// 32 bytes (the fallback source of special shards: no second load of them).
+template <class D, int U = 4, bool NO_OUTER_UNROLL = false, bool FIRST = false>
 __device__ __forceinline__ void accumulate_vec(typename D::Acc (&acc)[D::K], const void* const* s_src, int n,
-                                               int64_t vidx) {
+                                               int64_t vidx, V8* first = nullptr) {
   constexpr int K = D::K;
   int q = 0;
+  if constexpr (FIRST) {
+    if (n > 0) {  // replica 0 alone, kept; the rest as below
+      *first = ld_stream(reinterpret_cast<const V8*>(s_src[0]) + vidx);
+      typename D::Acc x[K];
+      D::unpack(*first, x);
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = D::add(acc[k], x[k]);
+      q = 1;
+    }
+  }
   if constexpr (NO_OUTER_UNROLL) {
 #pragma unroll 1
     for (; q + U <= n; q += U) {

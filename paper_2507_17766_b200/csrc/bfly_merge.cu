@@ -480,7 +480,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = D::zero();
       }
-      accumulate_vec<D, U, NOU>(acc, s_src, p.n_alive, vidx);
+      V8 first;  // replica 0's raw vector: the fallback values unless a fallback vector is given
+      const bool fb_first = !p.fallback && p.n_alive > 0 && fb_raw == s_src[0];
+      if (all_fast)
+        accumulate_vec<D, U, NOU>(acc, s_src, p.n_alive, vidx);
+      else
+        accumulate_vec<D, U, NOU, true>(acc, s_src, p.n_alive, vidx, &first);
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = D::mean(acc[k], p.n_div);
       const int64_t sa = all_fast ? 0 : p.bnd.shard_of(e0), sb = all_fast ? 0 : p.bnd.shard_of(e0 + K - 1);
@@ -521,7 +526,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
           for (int d = 0; d < p.n_dst; ++d) st_stream(reinterpret_cast<V8*>(s_dst[d]) + vidx, out);
         } else if (pr == kPredFallback) {
           double v[K];
-          fallback_vec<D>(p, fb_raw, vidx, v);  // read before the in-place stores below
+          if (fb_first)
+            D::unpack_raw(first, v);  // streamed in by the accumulation above
+          else
+            fallback_vec<D>(p, fb_raw, vidx, v);  // read before the in-place stores below
           if (p.merged && (c == kLost || merged_apart)) {
 #pragma unroll
             for (int k = 0; k < K; k += 4) st_f64x4(p.merged + e0 + k, v[k], v[k + 1], v[k + 2], v[k + 3]);
