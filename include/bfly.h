@@ -83,7 +83,9 @@ typedef struct bfly_merge_args {
   const bfly_corruption_t* d_corr;/* [N] per-miner corruption (kind NONE if honest) */
   void* const* d_dst;             /* [n_dst] scatter-back targets (in place), or NULL */
   int32_t n_dst;
-  int32_t pad0;
+  int32_t stat_tile;              /* elements per statistics tile of the special shards' pair
+                                     statistics (0 = the reduce kernel's tile); the persistent
+                                     ring sets its own tile (bfly_ring_fused_stat_tile) */
   const double* d_fallback;       /* [P] fallback weights, or NULL (butterfly.py:169,268-273) */
   double* d_merged;               /* [P] fp64 merged vector, or NULL                */
   double* d_ws;                   /* [P] fp64 means of special (corrupted) shards; may be
@@ -304,6 +306,10 @@ int32_t bfly_ring_fused_lanes(int32_t dtype);
 int bfly_ring_fused_layout(int32_t lanes, int32_t nb, int32_t dtype, int64_t* off_fin, int64_t* off_flags,
                            int64_t* total);
 int bfly_ring_fused(const bfly_ring_fused_desc_t* desc, void* stream);
+/* Elements per k_ring tile when the last rank accumulates the special shards' pair
+ * statistics inside the kernel (set bfly_merge_args_t.stat_tile to it for the round's
+ * FINISH), or 0 when this dtype's tiles are too small to (fp64 payloads). */
+int32_t bfly_ring_fused_stat_tile(int32_t dtype);
 /* Single-device loopback: `world` ranks of one ring on THIS device, in one cooperative
  * launch of world x lanes CTAs (CTA c serves lane c % lanes of rank c / lanes).  descs[g]
  * is rank g's descriptor exactly as bfly_ring_fused takes it, with the regions being

@@ -27,6 +27,7 @@ EXPORTS = (
     "bfly_ring_fused_lanes",
     "bfly_ring_fused_layout",
     "bfly_ring_fused_loopback",
+    "bfly_ring_fused_stat_tile",
     "bfly_version",
     "bfly_last_error",
     "bfly_n_shards",
@@ -84,7 +85,7 @@ class MergeArgs(ctypes.Structure):
         ("d_corr", ctypes.c_void_p),
         ("d_dst", ctypes.c_void_p),
         ("n_dst", ctypes.c_int32),
-        ("pad0", ctypes.c_int32),
+        ("stat_tile", ctypes.c_int32),
         ("d_fallback", ctypes.c_void_p),
         ("d_merged", ctypes.c_void_p),
         ("d_ws", ctypes.c_void_p),
@@ -218,6 +219,8 @@ def lib() -> ctypes.CDLL:
     L.bfly_ring_fused_layout.argtypes = [i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.bfly_ring_fused.argtypes = [ctypes.POINTER(RingFusedDesc), vp]
     L.bfly_ring_fused_loopback.argtypes = [vp, i32, vp]
+    L.bfly_ring_fused_stat_tile.argtypes = [i32]
+    L.bfly_ring_fused_stat_tile.restype = i32
     for name in EXPORTS:  # fail at load time if the export table is incomplete
         getattr(L, name)
     _lib = L

@@ -93,6 +93,13 @@ struct RingSpecial {
   bool merged_apart = false;      // merged is not the workspace
   uint32_t* nonfin_any = nullptr; // some fast shard's mean is not finite (then nonfin[s] = 1)
   uint8_t* nonfin = nullptr;
+  // pair statistics of special tiles accumulated inside the kernel (kPredFuse shards,
+  // whole tiles of one shard): one partial per (shard, tile) slot, done[tile] = 1
+  const int32_t* assign = nullptr;
+  const bfly_corruption_t* corr = nullptr;
+  double* stats = nullptr;
+  uint8_t* done = nullptr;
+  int64_t stile = 0;
 };
 
 // An IEEE double that is neither NaN nor +-Inf (exponent field not all ones).

@@ -25,6 +25,7 @@
 
 #include "bfly_internal.cuh"
 #include "bfly_elem.cuh"
+#include "bfly_stats.cuh"
 
 namespace bfly {
 
@@ -82,8 +83,6 @@ __device__ __forceinline__ void mark_nonfinite(const Params& p, int64_t s) {
 __device__ __forceinline__ int64_t fin_shard(const Params& p, unsigned i) {
   return p.slist ? (int64_t)p.slist[i] : p.sbeg + i;
 }
-
-__device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000LL); }
 
 // numpy DOUBLE_pairwise_sum over the alive replicas at element e (width-1 shards).
 template <class D>
@@ -258,25 +257,6 @@ __device__ __forceinline__ double corrupt_value(const bfly_corruption_t& c, doub
   }
 }
 
-__device__ __forceinline__ double max_nan(double a, double b) {
-  return (isnan(a) || isnan(b)) ? nan64() : fmax(a, b);
-}
-
-struct PairStat {
-  double mx, ab, aa, bb;
-};
-
-__device__ __forceinline__ PairStat warp_combine(PairStat s) {
-#pragma unroll
-  for (int off = 16; off; off >>= 1) {
-    s.mx = max_nan(s.mx, __shfl_xor_sync(0xffffffffu, s.mx, off));
-    s.ab = __dadd_rn(s.ab, __shfl_xor_sync(0xffffffffu, s.ab, off));
-    s.aa = __dadd_rn(s.aa, __shfl_xor_sync(0xffffffffu, s.aa, off));
-    s.bb = __dadd_rn(s.bb, __shfl_xor_sync(0xffffffffu, s.bb, off));
-  }
-  return s;
-}
-
 // CTA-wide fixed-order combine; result valid in thread 0.
 __device__ PairStat block_combine(PairStat s) {
   __shared__ PairStat part[kThreads / 32];
@@ -360,37 +340,6 @@ __device__ __forceinline__ unsigned load_group(const double* ws, int64_t e0, int
     }
   }
   return valid;
-}
-
-// Copies of four consecutive elements e0..e0+3 (e0 % 4 == 0) of a device-computable
-// corruption: one Philox4x64 block of noise words.
-__device__ __forceinline__ void corrupt4(const bfly_corruption_t& c, const double* m, int64_t e0, double* out) {
-  switch (c.kind) {
-    case BFLY_CORR_ADD:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) out[i] = __dadd_rn(m[i], c.a);
-      return;
-    case BFLY_CORR_SCALE:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) out[i] = __dmul_rn(m[i], c.a);
-      return;
-    case BFLY_CORR_NOISE:
-    case BFLY_CORR_NOISE_ADD: {
-      Philox4x64 ctr;
-      ctr.v[0] = (uint64_t)(e0 >> 2) + 1;
-      ctr.v[1] = ctr.v[2] = ctr.v[3] = 0;
-      const Philox4x64 o = philox4x64_10(ctr, c.key0, c.key1);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double noise = __dmul_rn(c.a, noise_unit(o.v[j]));
-        out[j] = c.kind == BFLY_CORR_NOISE ? noise : __dadd_rn(m[j], noise);
-      }
-      return;
-    }
-    default:
-#pragma unroll
-      for (int i = 0; i < 4; ++i) out[i] = m[i];
-  }
 }
 
 // Statistics of one vector (K means at e0, e0 % 4 == 0) for the copy pair (ca, cb).
@@ -554,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
       }
       // a whole tile of one special shard with two device-computable copies: its
       // pair statistics now, from the means in registers (k_stats skips the tile)
-      if (!all_fast && s_lo == s_hi && (p.pred[s_lo] & kPredFuse)) {
+      if (!all_fast && s_lo == s_hi && (p.pred[s_lo] & kPredFuse) && p.stile == TILE) {
         const int32_t* mem = p.assign + s_lo * 2;
         const PairStat st = block_combine(pair_stats_vec<D>(acc, e0, p.corr[mem[0]], p.corr[mem[1]]));
         if (threadIdx.x == 0) {
@@ -1217,6 +1166,11 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.pred = sc + L.off_pred;
   p.done = sc + L.off_done;
   p.stile = (int64_t)kThreads * (a->dtype == BFLY_F32 ? DF32::K : a->dtype == BFLY_BF16 ? DBF16::K : DF64W::K);
+  if (a->stat_tile != 0) {  // the persistent ring's tile (its kernel writes the partials)
+    if (a->stat_tile < kMinStatTile || a->stat_tile % kMinStatTile)
+      return fail(BFLY_E_INVALID_ARG, "stat_tile must be a multiple of " + std::to_string(kMinStatTile));
+    p.stile = a->stat_tile;
+  }
   p.source = a->d_source ? a->d_source : (int32_t*)(sc + L.off_source);
   p.stats = (double*)(sc + L.off_stats);
   p.scores = (double*)(sc + L.off_scores);
@@ -1267,6 +1221,11 @@ int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out)
     out->merged_apart = p.merged && p.merged != p.ws;
     out->nonfin_any = p.nonfin_any;
     out->nonfin = p.nonfin;
+    out->assign = p.assign;
+    out->corr = p.corr;
+    out->stats = p.stats;
+    out->done = p.done;
+    out->stile = p.stile;
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nn = (int64_t)p.n * p.n;

@@ -51,6 +51,7 @@
 
 #include "bfly_elem.cuh"
 #include "bfly_internal.cuh"
+#include "bfly_stats.cuh"
 
 namespace bfly {
 
@@ -116,7 +117,9 @@ struct RingGeom {
   static constexpr int OFF_REL = OFF_OUT + kNO * OUT_SLOT;
   static constexpr int OFF_BAR = OFF_REL + kNR * FIN_SLOT;
   static constexpr int N_BAR = 2 * kNS + 2 * kNA + 2 * kNO + 2 * kNR + 2 * kNT;
-  static constexpr int OFF_PTR = OFF_BAR + 8 * (N_BAR + kNT + kNR + 4);
+  // per-warp partial pair statistics of a fused special tile (double-buffered by step)
+  static constexpr int OFF_STAT = OFF_BAR + 8 * (N_BAR + kNT + kNR + 4);
+  static constexpr int OFF_PTR = OFF_STAT + 2 * (kRingCompute / 32) * 32;
 };
 
 // ---------------------------------------------------------------------------
@@ -382,6 +385,30 @@ __device__ __forceinline__ void fallback_vec16(const RingParams& p, int64_t e0, 
   }
 }
 
+// Pair statistics of one thread's KE means at e0 (e0 % 4 == 0) for the copy pair (ca, cb).
+template <class D>
+__device__ __forceinline__ PairStat ring_pair_stats(const typename D::Acc* acc, int64_t e0,
+                                                    const bfly_corruption_t& ca, const bfly_corruption_t& cb) {
+  constexpr int KE = RingGeom<D>::KE;
+  PairStat st{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int h = 0; h < KE / 4; ++h) {
+    double m[4], x[4], y[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) m[j] = D::widen(acc[4 * h + j]);
+    corrupt4(ca, m, e0 + 4 * h, x);
+    corrupt4(cb, m, e0 + 4 * h, y);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      st.mx = max_nan(st.mx, fabs(__dsub_rn(x[j], y[j])));
+      st.ab = fma(x[j], y[j], st.ab);
+      st.aa = fma(x[j], x[j], st.aa);
+      st.bb = fma(y[j], y[j], st.bb);
+    }
+  }
+  return st;
+}
+
 // A fast shard's mean came out NaN / Inf at e (a replica holds one): FINISH decides the
 // shard (k_nonfinite, bfly_merge.cu) after the kernel.  Rare, so one check per thread.
 __device__ __forceinline__ void ring_mark_nonfinite(const RingParams& p, int64_t e) {
@@ -610,6 +637,33 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
             need_fb |= p.sp.cls[sh] != kFast && (p.sp.pred[sh] & kPredMask) == kPredFallback;
           }
           if (need_fb) fallback_vec16<D>(p, e0, fb);
+          // a whole tile of one special shard with two device-computable copies: its pair
+          // statistics now, from the means in registers (FINISH's k_stats skips the tile)
+          const int64_t s_lo = p.sp.bnd.shard_of(t0);
+          if (p.sp.stile == G::TE && p.sp.bnd.shard_of(t0 + G::TE - 1) == s_lo && (p.sp.pred[s_lo] & kPredFuse)) {
+            const int32_t* mem = p.sp.assign + s_lo * 2;
+            PairStat st = ring_pair_stats<D>(acc, e0, p.sp.corr[mem[0]], p.sp.corr[mem[1]]);
+            st = warp_combine(st);
+            PairStat* part = reinterpret_cast<PairStat*>(sm + G::OFF_STAT) + (i & 1) * (kRingCompute / 32);
+            if (lead) part[tid >> 5] = st;
+            asm volatile("bar.sync 1, %0;" ::"n"(kRingCompute) : "memory");  // the compute warps only
+            if (tid == 0) {
+              PairStat t = part[0];
+#pragma unroll
+              for (int w = 1; w < kRingCompute / 32; ++w) {
+                t.mx = max_nan(t.mx, part[w].mx);
+                t.ab = __dadd_rn(t.ab, part[w].ab);
+                t.aa = __dadd_rn(t.aa, part[w].aa);
+                t.bb = __dadd_rn(t.bb, part[w].bb);
+              }
+              double* o = p.sp.stats + (tile + s_lo) * 4;  // slot (tile, shard), r = 2: one pair
+              o[0] = t.mx;
+              o[1] = t.ab;
+              o[2] = t.aa;
+              o[3] = t.bb;
+              p.sp.done[tile] = 1;
+            }
+          }
           // the means of a special shard to the workspace in one vector store
           const bool ws_vec = sk[0] == sk[KE - 1] && p.sp.cls[sk[0]] == kSpecial && KE % 2 == 0;
           if (ws_vec) {
@@ -1066,6 +1120,15 @@ int32_t bfly_ring_fused_lanes(int32_t dtype) {
     case BFLY_BF16: return ring_lanes_for<DBF16>();
     case BFLY_F64WIRE: return ring_lanes_for<DF64W>();
     default: return 0;
+  }
+}
+
+int32_t bfly_ring_fused_stat_tile(int32_t dtype) {
+  auto fusable = [](int te) { return te >= kMinStatTile && te % kMinStatTile == 0 ? te : 0; };
+  switch (dtype) {
+    case BFLY_F32: return fusable(RingGeom<DF32>::TE);
+    case BFLY_BF16: return fusable(RingGeom<DBF16>::TE);
+    default: return 0;  // fp64 payloads: 512-element tiles, below the smallest statistics tile
   }
 }
 

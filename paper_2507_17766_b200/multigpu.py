@@ -639,6 +639,9 @@ class ShardedButterflyMerge:
         d.d_dst = self._local_table.data_ptr()
         if self.is_last:
             d.d_merged = self.job.merged.data_ptr() if self.job.merged is not None else None
+            # the kernel accumulates the special shards' pair statistics per k_ring tile
+            # (FINISH then only covers the tiles it could not: shard edges, r = 3, fp64)
+            self.job._args.stat_tile = int(lib.bfly_ring_fused_stat_tile(self.dtype))
             d.merge_args = ctypes.pointer(self.job._args)
             d.special = int(len(self._special_ids) > 0)
         self._fdesc = d
