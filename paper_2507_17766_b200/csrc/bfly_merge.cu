@@ -437,7 +437,11 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
         accumulate_vec<D, U, NOU, true>(acc, s_src, p.n_alive, vidx, &first);
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = D::mean(acc[k], p.n_div);
-      const int64_t sa = all_fast ? 0 : p.bnd.shard_of(e0), sb = all_fast ? 0 : p.bnd.shard_of(e0 + K - 1);
+      // the vector's shard: known per tile unless the tile straddles a shard boundary (no
+      // 64-bit divisions per vector then)
+      const bool one_shard = s_lo == s_hi;
+      const int64_t sa = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0));
+      const int64_t sb = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0 + K - 1));
       const uint8_t c = all_fast ? (uint8_t)kFast : (sa == sb ? p.cls[sa] : (uint8_t)0xff);
       if (c == kFast) {
         if (p.merged) {
