@@ -479,6 +479,12 @@ def run_multi(cfg, args, rank, world):
     corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in bad}
     job = ShardedButterflyMerge(reps, plan, corruptions=corr, chunk=args.chunk)
     nvcount = NVLinkCounter(local_rank)
+    phases = None
+    if args.timing:  # one extra round with CUDA events between the phases (diagnostics, untimed)
+        job.timing = True
+        job.run()
+        phases = {k: round(v, 3) for k, v in job.timings.items()}
+        job.timing = False
 
     def step(timed=False):
         job.run()
@@ -553,7 +559,11 @@ def run_multi(cfg, args, rank, world):
             "e2e": e2e, "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks,
             "disagreement_shards": disagree,
         }
+        if phases:
+            line["phases_ms_rank0"] = phases
         print(json.dumps(line))
+    if phases and rank == world - 1:
+        print(f"[rank {rank}] phases (ms): " + json.dumps(phases), file=sys.stderr, flush=True)
     job.close()
     dist.barrier()
     dist.destroy_process_group()
@@ -725,6 +735,7 @@ def main():
     ap.add_argument("--cpu-params", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--timing", action="store_true", help="multi-GPU: per-phase times of one extra round")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -321,6 +321,13 @@ int bfly_ring_fused_loopback(const bfly_ring_fused_desc_t* descs, int32_t world,
 /* Copy nbytes from d_src into each of n_dst device buffers (scatter-back fan-out). */
 int bfly_fanout(const void* d_src, void* const* d_dst, int32_t n_dst, int64_t nbytes, void* stream);
 
+/* For every shard s with d_mask[s] != 0 and d_status[s] == BFLY_DISAGREEMENT: element e of
+ * the shard := d_fallback[e] (NULL: NaN) in each of the n_dst replicas.  Multi-GPU ranks
+ * other than the last apply the last rank's decision on fast shards whose mean was not
+ * finite (butterfly.py:127-133,264-273) to their own replicas — no host round trip. */
+int bfly_fill_shards(const uint8_t* d_status, const uint8_t* d_mask, const double* d_fallback, void* const* d_dst,
+                     int32_t n_dst, int32_t dtype, int64_t payload_len, int64_t n_shards, void* stream);
+
 /* Element ranges between a full-length vector and a packed buffer:
  * scatter == 0: d_packed[off_r + i] = d_full[lo_r + i];
  * scatter == 1: d_dst[k][lo_r + i] = d_packed[off_r + i] for every k.

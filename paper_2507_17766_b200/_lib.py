@@ -43,6 +43,7 @@ EXPORTS = (
     "bfly_chain_step",
     "bfly_fanout",
     "bfly_copy_ranges",
+    "bfly_fill_shards",
     "bfly_ipc_alloc",
     "bfly_ipc_open",
     "bfly_ipc_close",
@@ -213,6 +214,7 @@ def lib() -> ctypes.CDLL:
     L.bfly_merge_host.argtypes = [vp, i32, i64, vp, ctypes.POINTER(MergeArgs), vp, i32, i32, i64, vp]
     L.bfly_ring_round.argtypes = [ctypes.POINTER(RingDesc), u32]
     L.bfly_ring_ops.argtypes = [i32, i32, i32, i32, u32, i32, vp, i32]
+    L.bfly_fill_shards.argtypes = [vp, vp, vp, vp, i32, i32, i64, i64, vp]
     L.bfly_copy_ranges.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, vp]
     L.bfly_ring_fused_lanes.argtypes = [i32]
     L.bfly_ring_fused_lanes.restype = i32

@@ -982,6 +982,30 @@ __global__ void __launch_bounds__(kThreads) k_nonfinite(Params p) {
   }
 }
 
+// Multi-GPU ranks other than the last: after the per-shard results arrive, the fast
+// shards the last rank decided a disagreement (non-finite means, k_nonfinite) get the
+// fallback values — the given fallback, or NaN (the relay has overwritten the lowest alive
+// replica) — in every local replica, without a host round trip.
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_fill_shards(const uint8_t* status, const uint8_t* mask,
+                                                          const double* fallback, void* const* dst, int n_dst,
+                                                          Bounds bnd, int64_t cps) {
+  extern __shared__ __align__(16) const void* s_ptr[];
+  void** s_dst = const_cast<void**>(s_ptr);
+  stage_pointers(nullptr, s_dst, nullptr, 0, dst, n_dst, 0);
+  const int64_t items = bnd.S * cps;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t s = it / cps, ch = it % cps;
+    if (!mask[s] || status[s] != BFLY_DISAGREEMENT) continue;
+    const int64_t lo = bnd.start(s) + ch * kChunk, hi_s = bnd.start(s) + bnd.len(s);
+    const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
+    for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
+      const double v = fallback ? fallback[e] : nan64();
+      for (int d = 0; d < n_dst; ++d) D::store(s_dst[d], e, v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // standalone agreement and mean_reducer
 // ---------------------------------------------------------------------------
@@ -1362,12 +1386,42 @@ int bfly_preload(void) {
       (const void*)k_chain<DF32, false>, (const void*)k_chain<DBF16, true>, (const void*)k_chain<DBF16, false>,
       (const void*)k_chain<DF64W, true>, (const void*)k_chain<DF64W, false>, (const void*)k_ranges<true>,
       (const void*)k_ranges<false>, (const void*)k_fanout, (const void*)k_fanout_bulk,
-      (const void*)k_agree_partial, (const void*)k_agree_final, (const void*)k_corrupt, (const void*)k_mean_rows};
+      (const void*)k_agree_partial, (const void*)k_agree_final, (const void*)k_corrupt, (const void*)k_mean_rows,
+      (const void*)k_fill_shards<DF32>, (const void*)k_fill_shards<DBF16>, (const void*)k_fill_shards<DF64W>};
   for (const void* f : fns) {
     cudaFuncAttributes at;
     cudaError_t e = cudaFuncGetAttributes(&at, f);
     if (e != cudaSuccess) return cuda_fail(e, "bfly_preload");
   }
+  return BFLY_OK;
+}
+
+int bfly_fill_shards(const uint8_t* d_status, const uint8_t* d_mask, const double* d_fallback, void* const* d_dst,
+                     int32_t n_dst, int32_t dtype, int64_t payload_len, int64_t n_shards, void* stream) {
+  if (!d_status || !d_mask || n_dst < 0 || (n_dst > 0 && !d_dst) || n_shards < 1 || payload_len < n_shards)
+    return fail(BFLY_E_INVALID_ARG, "bad fill-shards arguments");
+  if (n_dst == 0) return BFLY_OK;
+  Bounds bnd;
+  bnd.init(payload_len, n_shards);
+  const int64_t cps = (bnd.base + (bnd.rem ? 1 : 0) + kChunk - 1) / kChunk;
+  int64_t grid = n_shards * cps;
+  if (grid > (int64_t)sm_count() * 2) grid = (int64_t)sm_count() * 2;
+  const size_t smem = sizeof(void*) * (size_t)n_dst;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (dtype) {
+    case BFLY_F32:
+      k_fill_shards<DF32><<<(unsigned)grid, kThreads, smem, st>>>(d_status, d_mask, d_fallback, d_dst, n_dst, bnd, cps);
+      break;
+    case BFLY_BF16:
+      k_fill_shards<DBF16><<<(unsigned)grid, kThreads, smem, st>>>(d_status, d_mask, d_fallback, d_dst, n_dst, bnd, cps);
+      break;
+    case BFLY_F64WIRE:
+      k_fill_shards<DF64W><<<(unsigned)grid, kThreads, smem, st>>>(d_status, d_mask, d_fallback, d_dst, n_dst, bnd, cps);
+      break;
+    default: return fail(BFLY_E_INVALID_ARG, "bad dtype");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "bfly_fill_shards launch");
   return BFLY_OK;
 }
 

@@ -498,6 +498,9 @@ class ShardedButterflyMerge:
         # (only such a shard could, with non-finite means, fall back unpredicted).
         self._cls, self._pred = classify_host(assign, failures, corrupted, len(self.alive))
         self._special_ids = np.flatnonzero(self._cls != CLS_FAST)
+        # fast shards: the other ranks apply the last rank's non-finite decisions on device
+        self._fast_mask = torch.from_numpy((self._cls == CLS_FAST).astype(np.uint8)).to(self.dev)
+        self._fallback = None if fallback is None else fallback.to(self.dev, torch.float64).contiguous()
         honest_major = bool(np.any((self._cls == CLS_SPECIAL) & (self._pred == PRED_MEAN)))
         self.fused = bool(G > 1 and self.P // plan.n_shards >= 2 and executor == "auto"
                           and not (self._needs_fb and (self.fb_owner == G - 1 or honest_major)))
@@ -893,7 +896,14 @@ class ShardedButterflyMerge:
         elif self.want_merged:
             self.merged.copy_(self.job.merged)
         unpack_results(self._res, self.entries, self.source, self.status, self.flagged)
-        if G > 1:
+        if G > 1 and not self.is_last:
+            # fast shards the last rank decided a disagreement (non-finite means): the
+            # fallback (or NaN) into this rank's replicas, on the device
+            L.check(L.lib().bfly_fill_shards(self.status.data_ptr(), self._fast_mask.data_ptr(),
+                                             self._fallback.data_ptr() if self._fallback is not None else None,
+                                             self._local_table.data_ptr(), len(self.local), self.dtype, self.P,
+                                             self.plan.n_shards, _stream_handle()))
+        if G > 1 and self.fused and len(self._special_ids):
             self._rebroadcast_mispredicted()
         mark("end")
         if tm is not None:
@@ -904,21 +914,14 @@ class ShardedButterflyMerge:
         return self
 
     def _rebroadcast_mispredicted(self):
-        """The relayed tiles carried the predicted outcome of every shard: the mean of fast
-        shards, k_classify's guess for special / lost ones (persistent ring).  The shards
-        decided otherwise after the exchange — special ones FINISH decided against the
-        guess, and fast ones whose mean came out non-finite (k_nonfinite: a disagreement,
-        butterfly.py:127-133,264-273) — are rewritten on the last rank, sent to the other
-        ranks and scattered into their replicas.  Every rank reads the same status, so
-        they agree on the list without communicating."""
-        status = self.status.cpu().numpy()
-        fast = np.flatnonzero(self._cls == CLS_FAST)
-        nonfinite = fast[status[fast] != L.MERGED]
-        mis = (mispredicted_shards(self._special_ids, self._pred, self.source.cpu().numpy(), self._corr_kind)
-               if self.fused and len(self._special_ids) else np.zeros(0, dtype=np.int64))
-        mis = np.union1d(mis, nonfinite).astype(np.int64)
+        """Persistent ring: the relayed tiles of special / lost shards carried the predicted
+        outcome; the shards FINISH decided otherwise (k_apply rewrote them on the last rank)
+        are sent to the other ranks and scattered into their replicas.  Every rank reads
+        the same per-shard results, so they agree on the list without communicating.
+        (Fast shards decided a disagreement — non-finite means — need no data: every rank
+        writes the fallback itself, bfly_fill_shards.)"""
+        mis = mispredicted_shards(self._special_ids, self._pred, self.source.cpu().numpy(), self._corr_kind)
         self.mispredicted = len(mis)
-        self.nonfinite = nonfinite
         if not len(mis):
             return
         base, rem = divmod(self.P, self.plan.n_shards)
