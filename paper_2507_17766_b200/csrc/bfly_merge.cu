@@ -992,6 +992,11 @@ __global__ void __launch_bounds__(kThreads) k_fill_shards(const uint8_t* status,
                                                           Bounds bnd, int64_t cps) {
   extern __shared__ __align__(16) const void* s_ptr[];
   void** s_dst = const_cast<void**>(s_ptr);
+  // almost always nothing to do: one parallel pass over the shards decides (the per-item
+  // loop below would walk S x cps dependent loads per CTA)
+  int any = 0;
+  for (int64_t s = threadIdx.x; s < bnd.S; s += blockDim.x) any |= mask[s] && status[s] == BFLY_DISAGREEMENT;
+  if (!__syncthreads_or(any)) return;
   stage_pointers(nullptr, s_dst, nullptr, 0, dst, n_dst, 0);
   const int64_t items = bnd.S * cps;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -1405,7 +1410,7 @@ int bfly_fill_shards(const uint8_t* d_status, const uint8_t* d_mask, const doubl
   bnd.init(payload_len, n_shards);
   const int64_t cps = (bnd.base + (bnd.rem ? 1 : 0) + kChunk - 1) / kChunk;
   int64_t grid = n_shards * cps;
-  if (grid > (int64_t)sm_count() * 2) grid = (int64_t)sm_count() * 2;
+  if (grid > (int64_t)sm_count()) grid = (int64_t)sm_count();
   const size_t smem = sizeof(void*) * (size_t)n_dst;
   cudaStream_t st = (cudaStream_t)stream;
   switch (dtype) {
