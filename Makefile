@@ -11,8 +11,14 @@ LIB := $(PKG)/libbfly.so
 
 all: $(LIB) oracle
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+HOSTSRC := $(PKG)/csrc/bfly_convert.cpp
+HOSTOBJ := build/bfly_convert.o
+
+$(HOSTOBJ): $(HOSTSRC)
+	g++ -O3 -fPIC -Wall -c -o $@ $<
+
+$(LIB): $(SRCS) $(HDRS) $(HOSTOBJ)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) $(HOSTOBJ) 2> build/ptxas.log || (cat build/ptxas.log; false)
 
 oracle:
 	$(MAKE) -s -C oracle
@@ -25,6 +31,6 @@ clean:
 
 # tuning build (not the product): adds bfly_tune_reduce for tools/tune_reduce.py
 tune: build/libbfly_tune.so
-build/libbfly_tune.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -DBFLY_TUNING -shared -o $@ $(SRCS) 2> build/ptxas_tune.log || (cat build/ptxas_tune.log; false)
+build/libbfly_tune.so: $(SRCS) $(HDRS) $(HOSTOBJ)
+	$(NVCC) $(NVFLAGS) -DBFLY_TUNING -shared -o $@ $(SRCS) $(HOSTOBJ) 2> build/ptxas_tune.log || (cat build/ptxas_tune.log; false)
 .PHONY: tune

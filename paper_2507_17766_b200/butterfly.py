@@ -287,17 +287,22 @@ class _LazyBlob:
     __hash__ = None
 
 
-def _wire_part(values):
-    """Ranged reader of ``values.astype("<f4")`` for a 1-D float vector (numpy or a
-    tensor): only the elements under [start, stop) are converted."""
+def _wire_part(values, header: bytes = b""):
+    """Ranged reader of ``header + values.astype("<f4")`` for a 1-D float vector (numpy or
+    a tensor): only the elements under [start, stop) are converted."""
+    h = len(header)
 
     def part(start: int, stop: int) -> bytes:
-        e0, e1 = start // 4, (stop + 3) // 4
-        chunk = values[e0:e1]
-        if isinstance(chunk, torch.Tensor):
-            chunk = chunk.detach().to("cpu", torch.float64).numpy()
-        raw = np.asarray(chunk, dtype=np.float64).astype("<f4").tobytes()
-        return raw[start - 4 * e0:stop - 4 * e0]
+        out = header[start:stop] if start < h else b""
+        a, b = max(start, h) - h, stop - h
+        if b > a:
+            e0, e1 = a // 4, (b + 3) // 4
+            chunk = values[e0:e1]
+            if isinstance(chunk, torch.Tensor):
+                chunk = chunk.detach().to("cpu", torch.float64).numpy()
+            raw = np.asarray(chunk, dtype=np.float64).astype("<f4").tobytes()
+            out += raw[a - 4 * e0:b - 4 * e0]
+        return out
     return part
 
 
@@ -435,10 +440,8 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     if fallback is not None and len(fallback) != P:
         raise ShapeError("fallback length does not match payloads")
     dev = _require_cuda()
-    _, agreement_type, result_type = _types_of(plan)
     failed = set(int(m) for m in failures if 0 <= int(m) < n)
     alive = [m for m in range(n) if m not in failed]
-    bpw = plan.bytes_per_weight
 
     descriptors = {m: c for m, c in corruptions.items() if isinstance(c, Corruption) and m not in failed}
     callables = {m: c for m, c in corruptions.items() if not isinstance(c, Corruption) and m not in failed}
@@ -499,22 +502,13 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
     else:
         job.run(L.PHASE_ALL)
 
-    status_codes = job.status.cpu().numpy()
-    corrupted = set(descriptors) | set(callables)
-    classes = _classes(plan, failed, corrupted)
-    # fast shards whose mean is NaN / Inf somewhere: both (identical) copies score NaN
-    # (butterfly.py:127-133), so the shard falls back (:264-273) — from the fp64 payload
-    # of the lowest alive miner when no fallback was given
-    nonfinite = [s for s, c in enumerate(classes) if c == "fast" and status_codes[s] != L.MERGED]
-    nonfinite_means = {}
-    if nonfinite:
-        nonfinite_means = _nonfinite_means(plan, reps, alive, nonfinite)
-        if fb is None and alive:
-            src = payloads[miners[alive[0]]]
-            job.set_fallback(_to_device_f64(src if hosts is None else hosts[0], dev))
-            job.run(L.PHASE_CHECK)
-            early = False  # merged changed after the streamed copy: copy it again
-
+    if nonfinite_fallback_needed(job, plan, failed, set(descriptors) | set(callables)) and fb is None and alive:
+        # fast shards whose mean is NaN / Inf somewhere fall back (butterfly.py:127-133,
+        # 264-273) — to the fp64 payload of the lowest alive miner when no fallback was given
+        src = payloads[miners[alive[0]]]
+        job.set_fallback(_to_device_f64(src if hosts is None else hosts[0], dev))
+        job.run(L.PHASE_CHECK)
+        early = False  # merged changed after the streamed copy: copy it again
     if _device_merged:  # stage glue (stage.py): the merged weights stay in HBM
         merged = job.merged
     else:
@@ -523,19 +517,35 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
             merged_host.copy_(job.merged, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         merged = merged_host.numpy()  # the array keeps the pinned tensor alive
+    return _settle(store, plan, miners, payloads, reps, alive, failed, key_prefix, job, descriptors, callables,
+                   host_reductions, merged)
+
+
+def nonfinite_fallback_needed(job, plan, failed: set, corrupted: set) -> bool:
+    """Did some fast shard come out a disagreement (a non-finite mean)?  Reads the status."""
+    status = job.status.cpu().numpy()
+    classes = _classes(plan, failed, corrupted)
+    return any(c == "fast" and status[s] != L.MERGED for s, c in enumerate(classes))
+
+
+def _settle(store, plan, miners, payloads, reps, alive, failed, prefix, job, descriptors, callables,
+            host_reductions, merged):
+    """The round's results back to the host and into the store (butterfly.py:242-295):
+    per-shard status, agreement matrix, flags; the re-uploaded reductions that differ from
+    ``merged`` rendered to host bytes; the closed-form meter.  Returns the MergeResult of
+    the plan's module.  No reference to the job's device memory survives the call."""
+    _, agreement_type, result_type = _types_of(plan)
+    n = plan.pair_set.n_miners
+    status_codes = job.status.cpu().numpy()
+    classes = _classes(plan, failed, set(descriptors) | set(callables))
+    nonfinite = [s for s, c in enumerate(classes) if c == "fast" and status_codes[s] != L.MERGED]
+    nonfinite_means = _nonfinite_means(plan, reps, alive, nonfinite) if nonfinite else {}
     entries = job.entries.cpu().numpy()
     flagged_idx = np.flatnonzero(job.flagged.cpu().numpy())
     sources = job.source.cpu().numpy()
-
-    # reductions that differ from merged: corrupted copies (device descriptors) and the
-    # means of non-finite shards, rendered to host "<f4" bytes now (no device memory of
-    # this round stays referenced once the call returns)
     rendered = _render_special(job, plan, failed, descriptors, classes, host_reductions, nonfinite_means)
-    del job, reps
-    # -- blob store: objects + closed-form meter (butterfly.py:205-288) -----
-    _account_store(store, plan, miners, payloads, alive, failed, key_prefix, bpw, merged, status_codes, sources,
-                   host_reductions, rendered)
-
+    _account_store(store, plan, miners, payloads, alive, failed, prefix, plan.bytes_per_weight, merged, status_codes,
+                   sources, host_reductions, rendered)
     return result_type(
         merged=merged,
         shard_status=[L.STATUS_NAMES[c] for c in status_codes],

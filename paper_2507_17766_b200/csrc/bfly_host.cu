@@ -24,6 +24,8 @@
 
 #include "bfly_internal.cuh"
 
+extern "C" void bfly_host_f64_to_f32(const double* src, float* dst, int64_t n);  // bfly_convert.cpp
+
 namespace bfly {
 
 namespace {
@@ -53,7 +55,7 @@ cudaError_t upload_block(Worker& w, int ring, const double* src, float* dst, int
   cudaError_t ce = cudaEventSynchronize(w.done[k]);  // the slot's previous copy has left
   if (ce != cudaSuccess) return ce;
   float* slot = w.slot[k];
-  for (int64_t i = 0; i < len; ++i) slot[i] = (float)src[i];  // RNE, as numpy's astype
+  bfly_host_f64_to_f32(src, slot, len);  // RNE, as numpy's astype (bfly_convert.cpp)
   ce = cudaMemcpyAsync(dst, slot, sizeof(float) * len, cudaMemcpyHostToDevice, w.stream);
   if (ce != cudaSuccess) return ce;
   return cudaEventRecord(w.done[k], w.stream);

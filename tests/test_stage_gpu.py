@@ -4,7 +4,9 @@ tests/golden/make_stage_golden.py recorded, from a 3-epoch reference scenario (4
 layers of miners incl. deceptive, dropout, lazy and a joiner; compressed + sync
 stages), every `_merge_stage` call's inputs and outputs.  Replaying each stage on
 device-resident weights must give bit-identical new global weights, every miner's
-weights after adoption, identical per-actor meters and the same stage duration.
+weights after adoption, identical per-actor meters and the same stage duration — with
+the deceptive miners' GPU noise or the orchestrator's own numpy callables (host path),
+and with the stage's layers launched as one CUDA graph or one by one.
 """
 
 import json
@@ -32,7 +34,8 @@ def test_stage_dropouts_match_reference():
 
 
 @pytest.mark.gpu
-def test_stage_merges_match_reference(cuda_device):
+@pytest.mark.parametrize("deceptive,graph", [("noise", True), ("noise", False), ("reference", True)])
+def test_stage_merges_match_reference(cuda_device, deceptive, graph):
     from paper_2507_17766_b200.simkernel import BlobStore, TransferMeter
     from paper_2507_17766_b200.stage import RosterEntry, StageLayer, merge_stage
 
@@ -52,7 +55,8 @@ def test_stage_merges_match_reference(cuda_device):
             store.meter[actor] = TransferMeter(up, down)
         dur = merge_stage(store, layers, seed=rec["seed"], epoch=rec["epoch"], stage_label=rec["stage"],
                           compressed=rec["compressed"], b_min=rec["b_min"], compression_ratio=rec["ratio"],
-                          bandwidth_bps=rec["bandwidth_bps"], dropped=set(rec["dropped"]))
+                          bandwidth_bps=rec["bandwidth_bps"], dropped=set(rec["dropped"]),
+                          deceptive=deceptive, graph=graph)
         for L, layer in enumerate(layers):
             assert_same_floats(layer.synced.cpu().numpy(), arr[f"s{idx}_L{L}_global"])
             for m in rec["layers"][L]["roster"]:
