@@ -192,30 +192,38 @@ BFLY_HD int64_t rank_combination(int32_t n, int32_t r, const int32_t* members) {
 // Closed-form shard bounds: divmod(P, S), first `rem` shards one longer.
 struct Bounds {
   int64_t P, S, base, rem;
-  double inv_long, inv_base;  // 1 / (base + 1), 1 / base: shard_of without 64-bit integer division
   BFLY_HD void init(int64_t p, int64_t s) {
     P = p;
     S = s;
     base = p / s;
     rem = p % s;
-    inv_long = 1.0 / (double)(base + 1);
-    inv_base = base > 0 ? 1.0 / (double)base : 0.0;
   }
   BFLY_HD int64_t start(int64_t s) const { return s * base + (s < rem ? s : rem); }
   BFLY_HD int64_t len(int64_t s) const { return base + (s < rem ? 1 : 0); }
-  // floor(n / d) from an fp64 reciprocal: for n < 2^51 the estimate is off by at most one,
-  // which the integer check corrects (a 64-bit division costs ~70 instructions on the GPU)
-  BFLY_HD static int64_t div_floor(int64_t n, int64_t d, double inv) {
-    int64_t q = (int64_t)((double)n * inv);
-    if (q * d > n)
-      --q;
-    else if ((q + 1) * d <= n)
-      ++q;
-    return q;
-  }
   BFLY_HD int64_t shard_of(int64_t e) const {
     const int64_t big = rem * (base + 1);
-    return e < big ? div_floor(e, base + 1, inv_long) : rem + div_floor(e - big, base, inv_base);
+    return e < big ? e / (base + 1) : rem + (e - big) / base;
+  }
+};
+
+// The shard of increasing element positions without a 64-bit division per lookup (one
+// costs ~70 instructions on the GPU): a thread walking its tiles in ascending order keeps
+// the current shard and steps forward; only the first lookup (or a step back) divides.
+struct ShardCursor {
+  int64_t s = -1, lo = 0, hi = 0;  // current shard and its element range [lo, hi)
+  BFLY_HD int64_t at(const Bounds& b, int64_t e) {
+    if (s < 0 || e < lo) {
+      s = b.shard_of(e);
+      lo = b.start(s);
+      hi = lo + b.len(s);
+      return s;
+    }
+    while (e >= hi) {
+      ++s;
+      lo = hi;
+      hi = lo + b.len(s);
+    }
+    return s;
   }
 };
 

@@ -406,12 +406,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   const bool may_width1 = p.bnd.base == 1;
   const int64_t tile_lo = p.ebeg / TILE, tile_hi = (p.eend + TILE - 1) / TILE;
 
+  ShardCursor cursor;  // this CTA's tiles ascend: the shard lookups step forward
   for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
     const int64_t t0 = max(tile * TILE, p.ebeg);
     const int64_t t1 = min(tile * TILE + TILE, p.eend);
     // per tile: vector path unless a width-1 shard needs numpy's pairwise order;
     // all-fast tiles skip the per-vector class lookup
-    const int64_t s_lo = p.bnd.shard_of(t0), s_hi = p.bnd.shard_of(t1 - 1);
+    const int64_t s_lo = cursor.at(p.bnd, t0), s_hi = cursor.at(p.bnd, t1 - 1);
     bool vec = aligned && (t1 - t0 == TILE);
     bool all_fast = vec;
     for (int64_t s = s_lo; vec && s <= s_hi; ++s) {
@@ -440,8 +441,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
       // the vector's shard: known per tile unless the tile straddles a shard boundary (no
       // 64-bit divisions per vector then)
       const bool one_shard = s_lo == s_hi;
-      const int64_t sa = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0));
-      const int64_t sb = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0 + K - 1));
+      int64_t sa = s_lo, sb = s_lo;  // (a straddling tile: walk forward from its first shard)
+      if (!all_fast && !one_shard) {
+        while (p.bnd.start(sa + 1) <= e0) ++sa;
+        sb = sa;
+        while (p.bnd.start(sb + 1) <= e0 + K - 1) ++sb;
+      }
       const uint8_t c = all_fast ? (uint8_t)kFast : (sa == sb ? p.cls[sa] : (uint8_t)0xff);
       if (c == kFast) {
         if (p.merged) {

@@ -339,13 +339,20 @@ __device__ __forceinline__ uint4 pack16d(const double* v) {
   return make_uint4(w.w[0], w.w[1], w.w[2], w.w[3]);
 }
 
-// Special / lost shards on the last rank (p.special): does the tile at t0 lie in fast
-// shards only?  (Shards are far longer than a tile: one or two lookups.)
-__device__ __forceinline__ bool tile_fast(const RingParams& p, int64_t t0, int64_t te) {
-  const int64_t s_lo = p.sp.bnd.shard_of(t0), s_hi = p.sp.bnd.shard_of(min(t0 + te - 1, p.P - 1));
-  for (int64_t s = s_lo; s <= s_hi; ++s)
-    if (p.sp.cls[s] != kFast) return false;
-  return true;
+// Special / lost shards on the last rank (p.special): the shards [lo, hi] the tile at t0
+// covers (a lane's tiles ascend, so the cursor only steps forward), and whether they are
+// all fast.  (Shards are far longer than a tile: one or two of them.)
+struct TileShards {
+  int64_t lo, hi;
+  bool fast;
+};
+__device__ __forceinline__ TileShards tile_shards(const RingParams& p, ShardCursor& cur, int64_t t0, int64_t te) {
+  TileShards t;
+  t.lo = cur.at(p.sp.bnd, t0);
+  t.hi = cur.at(p.sp.bnd, min(t0 + te - 1, p.P - 1));
+  t.fast = true;
+  for (int64_t s = t.lo; s <= t.hi; ++s) t.fast = t.fast && p.sp.cls[s] == kFast;
+  return t;
 }
 
 // The value element e leaves the last rank with, as k_reduce writes it (emit_predicted,
@@ -563,8 +570,10 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
   pf.flush();
 }
 
-// COMPUTE warps: running sums (chain) or sum and mean (REDUCE) of the lane's tiles
-template <class D, bool REDUCE>
+// COMPUTE warps: running sums (chain) or sum and mean (REDUCE) of the lane's tiles.
+// FUSE (last rank, fuse_stats): also the special shards' pair statistics — a separate
+// instantiation, so the plain kernel keeps its lean register allocation.
+template <class D, bool REDUCE, bool FUSE = false>
 __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char* sm, const void** s_src,
                              void** s_dst) {
   using G = RingGeom<D>;
@@ -575,6 +584,7 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
   const bool lead = (tid & 31) == 0;
   const bool has_in = p.g > 0;
   int64_t rs = 0;
+  ShardCursor cursor;  // the shards of this lane's (ascending) tiles
   Prof pf(p, threadIdx.x == 0 ? 4 : -1);
   if (threadIdx.x) pf.out = nullptr;
   for (int64_t i = 0;; ++i) {
@@ -623,12 +633,14 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
       if constexpr (REDUCE) {
 #pragma unroll
         for (int k = 0; k < KE; ++k) acc[k] = D::mean(acc[k], p.n_div);
-        if (p.special && !tile_fast(p, t0, G::TE)) {  // predicted outcomes (k_classify) of special / lost shards
+        const TileShards ts = p.special ? tile_shards(p, cursor, t0, G::TE) : TileShards{0, 0, true};
+        if (!ts.fast) {  // predicted outcomes (k_classify) of special / lost shards
           double v[KE], fb[KE];
           const int64_t e0 = t0 + tid * KE;
-          // the shard of each element: one division, then boundary compares
+          // the shard of each element: forward from the tile's first shard
           int64_t sk[KE];
-          int64_t sh = p.sp.bnd.shard_of(e0), nxt = p.sp.bnd.start(sh + 1);
+          int64_t sh = ts.lo, nxt = p.sp.bnd.start(sh + 1);
+          while (e0 >= nxt) nxt = p.sp.bnd.start(++sh + 1);
           bool need_fb = false;
 #pragma unroll
           for (int k = 0; k < KE; ++k) {
@@ -639,8 +651,8 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
           if (need_fb) fallback_vec16<D>(p, e0, fb);
           // a whole tile of one special shard with two device-computable copies: its pair
           // statistics now, from the means in registers (FINISH's k_stats skips the tile)
-          const int64_t s_lo = p.sp.bnd.shard_of(t0);
-          if (p.sp.stile == G::TE && p.sp.bnd.shard_of(t0 + G::TE - 1) == s_lo && (p.sp.pred[s_lo] & kPredFuse)) {
+          const int64_t s_lo = ts.lo;
+          if (FUSE && ts.hi == s_lo && (p.sp.pred[s_lo] & kPredFuse)) {
             const int32_t* mem = p.sp.assign + s_lo * 2;
             PairStat st = ring_pair_stats<D>(acc, e0, p.sp.corr[mem[0]], p.sp.corr[mem[1]]);
             st = warp_combine(st);
@@ -947,7 +959,7 @@ __device__ void ring_publisher(const RingParams& p, const Lane& ln, unsigned cha
 }
 
 // One CTA = one lane of one rank: the roles above, dispatched by warp.
-template <class D>
+template <class D, bool FUSE>
 __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
   extern __shared__ __align__(1024) unsigned char sm[];
   using G = RingGeom<D>;
@@ -1000,7 +1012,7 @@ __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
   if (w < kWLoad) {
     const long long t_start = clock64();
     if (last)
-      ring_compute<D, true>(p, ln, sm, s_src, s_dst);
+      ring_compute<D, true, FUSE>(p, ln, sm, s_src, s_dst);
     else
       ring_compute<D, false>(p, ln, sm, s_src, s_dst);
     if (p.prof && threadIdx.x == 0) {
@@ -1031,9 +1043,9 @@ __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
 // copy the compiler keeps in registers / local memory): reading them from the parameter
 // bank instead (__grid_constant__) measured 1.4% slower per round (4 GPUs, C3:
 // 20.98 vs 20.69 ms, tools/_ab4.sh).
-template <class D>
+template <class D, bool FUSE = false>
 __global__ void __launch_bounds__(kRingThreads, 1) k_ring(RingParams p) {
-  ring_body<D>(p, (int)blockIdx.x);
+  ring_body<D, FUSE>(p, (int)blockIdx.x);
 }
 
 // Single-device loopback: every rank of the ring on this GPU, CTA c is lane c % L of
@@ -1042,11 +1054,11 @@ constexpr int kMaxLoop = 8;
 struct RingLoopParams {
   RingParams r[kMaxLoop];
 };
-template <class D>
+template <class D, bool FUSE = false>
 __global__ void __launch_bounds__(kRingThreads, 1) k_ring_loop(const __grid_constant__ RingLoopParams lp) {
   const int L = lp.r[0].L;
   const RingParams p = lp.r[blockIdx.x / L];  // this rank's parameters, copied as k_ring has them
-  ring_body<D>(p, (int)(blockIdx.x % L));
+  ring_body<D, FUSE>(p, (int)(blockIdx.x % L));
 }
 
 template <class D>
@@ -1066,25 +1078,28 @@ template <class D>
 static int ring_lanes_for() {
   int per_sm = 0;
   const size_t smem = ring_smem_bytes<D>(kRingMaxPtrs, 0);
-  cudaFuncSetAttribute(k_ring<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring<D>, kRingThreads, smem) != cudaSuccess)
+  cudaFuncSetAttribute(k_ring<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring<D, false>, kRingThreads, smem) != cudaSuccess)
     return 0;
   return per_sm * sm_count();
 }
+
+// the last rank fuses the pair statistics when its FINISH uses this kernel's tiles
+static bool ring_fuses(const RingParams& p, int te) { return p.special && p.sp.stile == te; }
 
 template <class D>
 static int ring_launch(RingParams p, cudaStream_t st) {
   if (p.n_src + p.n_dst > kRingMaxPtrs) return fail(BFLY_E_UNSUPPORTED, "fused ring: too many local replicas");
   p.T = (p.P + RingGeom<D>::TE - 1) / RingGeom<D>::TE;
   const size_t smem = ring_smem_bytes<D>(p.n_src, p.n_dst);
-  cudaFuncSetAttribute(k_ring<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const void* kern = ring_fuses(p, RingGeom<D>::TE) ? (const void*)k_ring<D, true> : (const void*)k_ring<D, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring<D>, kRingThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRingThreads, smem);
   if ((int64_t)per_sm * sm_count() < p.L)
     return fail(BFLY_E_UNSUPPORTED, "fused ring: " + std::to_string(p.L) + " CTAs cannot be co-resident");
   void* args[] = {&p};
-  cudaError_t e =
-      cudaLaunchCooperativeKernel((const void*)k_ring<D>, dim3((unsigned)p.L), dim3(kRingThreads), args, smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)p.L), dim3(kRingThreads), args, smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_ring cooperative launch");
   return BFLY_OK;
 }
@@ -1099,15 +1114,16 @@ static int ring_launch_loop(RingLoopParams& lp, int G, cudaStream_t st) {
     max_ptrs = max_ptrs > p.n_src + p.n_dst ? max_ptrs : p.n_src + p.n_dst;
   }
   const size_t smem = ring_smem_bytes<D>(max_ptrs, 0);
-  cudaFuncSetAttribute(k_ring_loop<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const void* kern = ring_fuses(lp.r[G - 1], RingGeom<D>::TE) ? (const void*)k_ring_loop<D, true>
+                                                               : (const void*)k_ring_loop<D, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ring_loop<D>, kRingThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRingThreads, smem);
   const int64_t ctas = (int64_t)G * lp.r[0].L;
   if ((int64_t)per_sm * sm_count() < ctas)
     return fail(BFLY_E_UNSUPPORTED, "fused ring loopback: " + std::to_string(ctas) + " CTAs cannot be co-resident");
   void* args[] = {&lp};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_ring_loop<D>, dim3((unsigned)ctas), dim3(kRingThreads),
-                                              args, smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)ctas), dim3(kRingThreads), args, smem, st);
   if (e != cudaSuccess) return cuda_fail(e, "k_ring_loop cooperative launch");
   return BFLY_OK;
 }

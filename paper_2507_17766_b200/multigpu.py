@@ -423,14 +423,20 @@ class ShardedButterflyMerge:
     executor     "auto" (the persistent ring whenever it applies) or "chunked".
     per_chunk_finish  chunked ring: the last rank decides each chunk's special shards
                  before relaying it (False: all after the ring; diagnostics).
+    fuse_stats   persistent ring: the last rank's compute warps accumulate the special
+                 shards' pair statistics (instead of k_stats after the kernel, on every
+                 SM).  Off by default: the Philox noise of the corrupted copies makes the
+                 last rank's compute warps the round's critical path.
     debug / timing    diagnostics of the chunked ring (per-op watchdog, timeline) and
                  per-phase CUDA-event times of a round (``.timings``).
     """
 
     def __init__(self, local: list, plan, *, failures=(), corruptions=None, fallback=None,
                  want_merged: bool = False, tolerance: float = 1e-6, chunk: int = 1 << 24, comm=None,
-                 executor: str = "auto", per_chunk_finish: bool = True, debug: int = 0, timing: bool = False):
+                 executor: str = "auto", per_chunk_finish: bool = True, debug: int = 0, timing: bool = False,
+                 fuse_stats: bool = False):
         self.comm = comm if comm is not None else DistComm()
+        self.fuse_stats = bool(fuse_stats)
         self.rank = self.comm.rank
         self.world = G = self.comm.world
         if executor not in ("auto", "chunked"):
@@ -642,9 +648,10 @@ class ShardedButterflyMerge:
         d.d_dst = self._local_table.data_ptr()
         if self.is_last:
             d.d_merged = self.job.merged.data_ptr() if self.job.merged is not None else None
-            # the kernel accumulates the special shards' pair statistics per k_ring tile
-            # (FINISH then only covers the tiles it could not: shard edges, r = 3, fp64)
-            self.job._args.stat_tile = int(lib.bfly_ring_fused_stat_tile(self.dtype))
+            # fuse_stats: the kernel accumulates the special shards' pair statistics per
+            # k_ring tile (FINISH then only covers the tiles it could not: shard edges,
+            # r = 3, fp64)
+            self.job._args.stat_tile = int(lib.bfly_ring_fused_stat_tile(self.dtype)) if self.fuse_stats else 0
             d.merge_args = ctypes.pointer(self.job._args)
             d.special = int(len(self._special_ids) > 0)
         self._fdesc = d

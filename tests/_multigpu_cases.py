@@ -63,7 +63,7 @@ def run_rank(case, d, rank, comm, dev) -> int:
     job = ShardedButterflyMerge(local, plan, failures=d["fails"], corruptions=corr,
                                 fallback=None if fb is None else torch.from_numpy(fb).to(dev),
                                 chunk=case["chunk"], want_merged=True, comm=comm,
-                                executor=case.get("executor", "auto"))
+                                executor=case.get("executor", "auto"), fuse_stats=case.get("fuse_stats", False))
     if "fused" in case:
         assert job.fused == case["fused"], (job.fused, case["fused"])
     orig = [t.clone() for t in local]

@@ -73,6 +73,10 @@ CASES = [
     {"counts": [4, 4, 4, 4], "P": 2_000_039, "seed": 28, "failures": [],
      "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "9": [3, 2.0, 24301, 9], "15": [3, 2.0, 24301, 15]},
      "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2},
+    # the same with the pair statistics accumulated inside k_ring (fuse_stats)
+    {"counts": [3, 5], "P": 2_000_029, "seed": 32, "failures": [],
+     "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "7": [1, 0.0]},
+     "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2, "fuse_stats": True},
     # non-finite weights (a diverged miner): fast shards with NaN / Inf means are
     # disagreements decided after the exchange and re-broadcast
     {"counts": [3, 3], "P": 600_011, "seed": 29, "failures": [], "corr": {}, "fallback": True,
