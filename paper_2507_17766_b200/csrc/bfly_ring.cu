@@ -355,6 +355,20 @@ __device__ __forceinline__ TileShards tile_shards(const RingParams& p, ShardCurs
   return t;
 }
 
+// Last rank: a whole tile that holds a shard predicted to fall back to the lowest alive
+// miner's replica (usually on another GPU).  The loader bulk-loads that replica's tile
+// over NVLink into a stage (the relay stages: the last rank has no relay) ahead of the
+// compute warps, which would otherwise stall on a remote load per tile.
+__device__ __forceinline__ bool fb_prefetch_on(const RingParams& p) {
+  return p.special && p.g == p.G - 1 && !p.sp.fallback && p.sp.fb_src;
+}
+__device__ __forceinline__ bool tile_wants_fb(const RingParams& p, const TileShards& t) {
+  bool want = false;
+  for (int64_t s = t.lo; s <= t.hi; ++s)
+    want = want || (p.sp.cls[s] != kFast && (p.sp.pred[s] & kPredMask) == kPredFallback);
+  return want;
+}
+
 // The value element e leaves the last rank with, as k_reduce writes it (emit_predicted,
 // bfly_merge.cu): the mean for fast shards and for shards predicted to adopt it, the
 // fallback for shards predicted to fall back; a shard without a prediction carries the
@@ -363,6 +377,18 @@ template <class D>
 __device__ __forceinline__ double fallback_one(const RingParams& p, int64_t e) {
   return p.sp.fallback ? p.sp.fallback[e]
                        : (p.sp.fb_src ? D::raw(p.sp.fb_src, e) : __longlong_as_double(0x7ff8000000000000LL));
+}
+
+// KE fallback values from 16 raw bytes of a replica (dtype D), rounded as it stores them
+template <class D>
+__device__ __forceinline__ void fallback_unpack16(const uint4& w, double* fb) {
+  V8 v;
+  v.w[0] = w.x, v.w[1] = w.y, v.w[2] = w.z, v.w[3] = w.w;
+  v.w[4] = v.w[5] = v.w[6] = v.w[7] = 0;
+  double t[8 * 4 / RingGeom<D>::ESIZE > 0 ? 8 * 4 / RingGeom<D>::ESIZE : 1];
+  D::unpack_raw(v, t);
+#pragma unroll
+  for (int k = 0; k < RingGeom<D>::KE; ++k) fb[k] = t[k];
 }
 
 // The fallback values of a thread's KE elements (from e0, 16-byte aligned in the replica),
@@ -518,6 +544,9 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
   const uint64_t pol = policy_evict_first();
   uint64_t known = 0;
   int64_t rs = 0;  // replica stage uses so far
+  const bool fb_pref = fb_prefetch_on(p);
+  ShardCursor cursor;
+  int64_t fu = 0;  // fallback tiles prefetched so far (last rank)
   Prof pf(p, 0);
   for (int64_t i = 0;; ++i) {
     const uint64_t j = ln.base_c + (uint64_t)i;
@@ -541,6 +570,17 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
     if (tile < 0) break;
     const int64_t t0 = tile * G::TE;
     const int64_t n = min((int64_t)G::TE, p.P - t0);
+    if (fb_pref && n == G::TE) {
+      const TileShards ts = tile_shards(p, cursor, t0, G::TE);
+      if (!ts.fast && tile_wants_fb(p, ts)) {
+        const int f = (int)(fu % kNR);
+        if (fu >= kNR) mbar_wait(p, B.rel_empty + f, (unsigned)((fu / kNR - 1) & 1));
+        mbar_expect_tx(B.rel_full + f, (unsigned)G::FIN_BYTES);
+        bulk_load(sm + G::OFF_REL + f * G::FIN_SLOT + 16, (const unsigned char*)p.sp.fb_src + t0 * G::ESIZE,
+                  (unsigned)G::FIN_BYTES, B.rel_full + f);
+        ++fu;
+      }
+    }
     for (int q0 = 0; n == G::TE && q0 < p.n_src; q0 += kRB, ++rs) {
       const int s = (int)(rs % kNS);
       const int64_t u = rs / kNS;
@@ -585,6 +625,8 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
   const bool has_in = p.g > 0;
   int64_t rs = 0;
   ShardCursor cursor;  // the shards of this lane's (ascending) tiles
+  const bool fb_pref = REDUCE && fb_prefetch_on(p);
+  int64_t fu = 0;  // prefetched fallback tiles consumed so far
   Prof pf(p, threadIdx.x == 0 ? 4 : -1);
   if (threadIdx.x) pf.out = nullptr;
   for (int64_t i = 0;; ++i) {
@@ -648,7 +690,17 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
             sk[k] = sh;
             need_fb |= p.sp.cls[sh] != kFast && (p.sp.pred[sh] & kPredMask) == kPredFallback;
           }
-          if (need_fb) fallback_vec16<D>(p, e0, fb);
+          if (fb_pref && tile_wants_fb(p, ts)) {  // the loader brought the fallback tile in
+            const int f = (int)(fu % kNR);
+            mbar_wait(p, B.rel_full + f, (unsigned)((fu / kNR) & 1));
+            const uint4 w = *reinterpret_cast<const uint4*>(sm + G::OFF_REL + f * G::FIN_SLOT + 16 + tid * 16);
+            __syncwarp();
+            if (lead) mbar_arrive(B.rel_empty + f);
+            ++fu;
+            fallback_unpack16<D>(w, fb);
+          } else if (need_fb) {
+            fallback_vec16<D>(p, e0, fb);
+          }
           // a whole tile of one special shard with two device-computable copies: its pair
           // statistics now, from the means in registers (FINISH's k_stats skips the tile)
           const int64_t s_lo = ts.lo;
@@ -986,9 +1038,9 @@ __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
       mbar_init(B.out_full + o, warps);
       mbar_init(B.out_empty + o, 1);  // the storer
     }
-    for (int s = 0; s < kNR; ++s) {
+    for (int s = 0; s < kNR; ++s) {  // relay stages; on the last rank: fallback tiles
       mbar_init(B.rel_full + s, 1);
-      mbar_init(B.rel_empty + s, 1);
+      mbar_init(B.rel_empty + s, p.g == p.G - 1 ? warps : 1);
     }
     for (int k = 0; k < kNT; ++k) {
       mbar_init(B.tile_full + k, 1);   // the loader
