@@ -75,9 +75,19 @@ struct Params {
 // in the reference's agreement (max|a-b| = NaN, butterfly.py:127-133), so with two or
 // more survivors the shard is a disagreement (:255,264-267).  k_reduce only marks it;
 // k_nonfinite decides it.
-__device__ __forceinline__ void mark_nonfinite(const Params& p, int64_t s) {
-  p.nonfin[s] = 1;
-  *p.nonfin_any = 1u;
+// (rare: out of line, and with plain values — a reference to the parameters would move
+// them to local memory)
+__device__ __noinline__ void mark_nonfinite_shard(uint8_t* nonfin, uint32_t* any, int64_t s) {
+  nonfin[s] = 1;
+  *any = 1u;
+}
+__device__ __noinline__ void mark_nonfinite_elem(uint8_t* nonfin, uint32_t* any, Bounds bnd, int64_t e) {
+  nonfin[bnd.shard_of(e)] = 1;
+  *any = 1u;
+}
+__device__ __forceinline__ void mark_nonfinite(const Params& p, int64_t s) { mark_nonfinite_shard(p.nonfin, p.nonfin_any, s); }
+__device__ __forceinline__ void mark_nonfinite_at(const Params& p, int64_t e) {
+  mark_nonfinite_elem(p.nonfin, p.nonfin_any, p.bnd, e);
 }
 
 __device__ __forceinline__ int64_t fin_shard(const Params& p, unsigned i) {
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
         if (!fin) {  // rare: a replica holds NaN / Inf here
 #pragma unroll
           for (int k = 0; k < K; ++k)
-            if (!finite64(D::widen(acc[k]))) mark_nonfinite(p, p.bnd.shard_of(e0 + k));
+            if (!finite64(D::widen(acc[k]))) mark_nonfinite_at(p, e0 + k);
         }
       } else if (c != 0xff) {  // one special or lost shard
         if (c == kSpecial) {  // the mean waits in the workspace for k_stats / k_apply

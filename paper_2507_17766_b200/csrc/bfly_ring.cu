@@ -442,12 +442,23 @@ __device__ __forceinline__ PairStat ring_pair_stats(const typename D::Acc* acc, 
   return st;
 }
 
-// A fast shard's mean came out NaN / Inf at e (a replica holds one): FINISH decides the
-// shard (k_nonfinite, bfly_merge.cu) after the kernel.  Rare, so one check per thread.
-__device__ __forceinline__ void ring_mark_nonfinite(const RingParams& p, int64_t e) {
+// A fast shard's mean came out NaN / Inf (a replica holds one): FINISH decides the shard
+// (k_nonfinite, bfly_merge.cu) after the kernel.  Rare: out of line, so the division of
+// the shard lookup stays out of the compute loop (inlined, the checks cost the adversarial
+// round 1.5 ms on 4 GPUs).
+__device__ __noinline__ void ring_mark_nonfinite_vals(uint8_t* nonfin, uint32_t* any, Bounds bnd, int64_t e0,
+                                                      double m0, double m1, double m2, double m3, int n) {
+  const double m[4] = {m0, m1, m2, m3};
+  for (int k = 0; k < n && k < 4; ++k)
+    if (!finite64(m[k])) nonfin[bnd.shard_of(e0 + k)] = 1;  // (special shards: ignored)
+  *any = 1u;
+}
+// the KE (<= 8) means of a thread starting at e0
+__device__ __forceinline__ void ring_mark_nonfinite(const RingParams& p, int64_t e0, const double* m, int n) {
   if (!p.sp.nonfin) return;
-  p.sp.nonfin[p.sp.bnd.shard_of(e)] = 1;
-  *p.sp.nonfin_any = 1u;
+  for (int k = 0; k < n; k += 4)
+    ring_mark_nonfinite_vals(p.sp.nonfin, p.sp.nonfin_any, p.sp.bnd, e0 + k, m[k], k + 1 < n ? m[k + 1] : 0.0,
+                             k + 2 < n ? m[k + 2] : 0.0, k + 3 < n ? m[k + 3] : 0.0, n - k);
 }
 
 template <class D>
@@ -457,7 +468,6 @@ __device__ __forceinline__ double final_value(const RingParams& p, int64_t e, do
   const uint8_t c = p.sp.cls[s];
   if (c == kFast) {
     if (p.merged) p.merged[e] = mean;
-    if (!finite64(mean)) ring_mark_nonfinite(p, e);
     return mean;
   }
   if (c == kSpecial && !ws_done) p.sp.ws[e] = mean;
@@ -673,8 +683,19 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
         if (lead) mbar_arrive(B.rep_empty + s);
       }
       if constexpr (REDUCE) {
+        // one branch-free test per thread: is any of its means NaN / Inf?
+        bool nonfin = false;
 #pragma unroll
-        for (int k = 0; k < KE; ++k) acc[k] = D::mean(acc[k], p.n_div);
+        for (int k = 0; k < KE; ++k) {
+          acc[k] = D::mean(acc[k], p.n_div);
+          nonfin |= !finite64(D::widen(acc[k]));
+        }
+        if (nonfin) {
+          double m[KE];
+#pragma unroll
+          for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
+          ring_mark_nonfinite(p, t0 + tid * KE, m, KE);
+        }
         const TileShards ts = p.special ? tile_shards(p, cursor, t0, G::TE) : TileShards{0, 0, true};
         if (!ts.fast) {  // predicted outcomes (k_classify) of special / lost shards
           double v[KE], fb[KE];
@@ -749,14 +770,7 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
             for (int k = 0; k < KE; ++k) m[k] = D::widen(acc[k]);
           }
           *reinterpret_cast<uint4*>(out + tid * 16) = pack16<D>(acc);
-          bool fin = true;
-#pragma unroll
-          for (int k = 0; k < KE; ++k) fin = fin && finite64(D::widen(acc[k]));
-          if (!fin) {
-#pragma unroll
-            for (int k = 0; k < KE; ++k)
-              if (!finite64(D::widen(acc[k]))) ring_mark_nonfinite(p, t0 + tid * KE + k);
-          }
+
         }
       } else {
 #pragma unroll
@@ -769,12 +783,15 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
         if constexpr (REDUCE) {
           v = D::mean(v, p.n_div);
           double f;
+          if (!finite64(D::widen(v))) {
+            const double m = D::widen(v);
+            ring_mark_nonfinite(p, t0 + e, &m, 1);
+          }
           if (p.special) {
             f = final_value<D>(p, t0 + e, D::widen(v));
           } else {
             f = D::widen(v);
             if (p.merged) p.merged[t0 + e] = f;
-            if (!finite64(f)) ring_mark_nonfinite(p, t0 + e);
           }
           for (int d = 0; d < p.n_dst; ++d) D::store(s_dst[d], t0 + e, f);
           D::store(out, e, f);
