@@ -36,7 +36,7 @@ namespace bfly {
 struct Params {
   int32_t n, r, n_alive, n_dst, npairs;
   int64_t P, S, cps;
-  Bounds bnd;
+  FastBounds bnd;
   const int32_t* assign;
   const void* const* src;
   const uint8_t* failed;
@@ -75,13 +75,12 @@ struct Params {
 // in the reference's agreement (max|a-b| = NaN, butterfly.py:127-133), so with two or
 // more survivors the shard is a disagreement (:255,264-267).  k_reduce only marks it;
 // k_nonfinite decides it.
-// (rare: out of line, and with plain values — a reference to the parameters would move
-// them to local memory)
-__device__ __noinline__ void mark_nonfinite_shard(uint8_t* nonfin, uint32_t* any, int64_t s) {
+// (k_reduce inlines these; k_ring keeps its marking out of line, bfly_ring.cu)
+__device__ __forceinline__ void mark_nonfinite_shard(uint8_t* nonfin, uint32_t* any, int64_t s) {
   nonfin[s] = 1;
   *any = 1u;
 }
-__device__ __noinline__ void mark_nonfinite_elem(uint8_t* nonfin, uint32_t* any, Bounds bnd, int64_t e) {
+__device__ __forceinline__ void mark_nonfinite_elem(uint8_t* nonfin, uint32_t* any, Bounds bnd, int64_t e) {
   nonfin[bnd.shard_of(e)] = 1;
   *any = 1u;
 }
@@ -416,13 +415,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
   const bool may_width1 = p.bnd.base == 1;
   const int64_t tile_lo = p.ebeg / TILE, tile_hi = (p.eend + TILE - 1) / TILE;
 
-  ShardCursor cursor;  // this CTA's tiles ascend: the shard lookups step forward
   for (int64_t tile = tile_lo + blockIdx.x; tile < tile_hi; tile += gridDim.x) {
     const int64_t t0 = max(tile * TILE, p.ebeg);
     const int64_t t1 = min(tile * TILE + TILE, p.eend);
     // per tile: vector path unless a width-1 shard needs numpy's pairwise order;
-    // all-fast tiles skip the per-vector class lookup
-    const int64_t s_lo = cursor.at(p.bnd, t0), s_hi = cursor.at(p.bnd, t1 - 1);
+    // all-fast tiles skip the per-vector class lookup.  (Measured: the fp64-reciprocal
+    // lookups here beat a forward-walking ShardCursor by 1 ms on the adversarial round.)
+    const int64_t s_lo = p.bnd.shard_of(t0), s_hi = p.bnd.shard_of(t1 - 1);
     bool vec = aligned && (t1 - t0 == TILE);
     bool all_fast = vec;
     for (int64_t s = s_lo; vec && s <= s_hi; ++s) {
@@ -451,12 +450,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_reduce(Params p) {
       // the vector's shard: known per tile unless the tile straddles a shard boundary (no
       // 64-bit divisions per vector then)
       const bool one_shard = s_lo == s_hi;
-      int64_t sa = s_lo, sb = s_lo;  // (a straddling tile: walk forward from its first shard)
-      if (!all_fast && !one_shard) {
-        while (p.bnd.start(sa + 1) <= e0) ++sa;
-        sb = sa;
-        while (p.bnd.start(sb + 1) <= e0 + K - 1) ++sb;
-      }
+      const int64_t sa = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0));
+      const int64_t sb = all_fast ? 0 : (one_shard ? s_lo : p.bnd.shard_of(e0 + K - 1));
       const uint8_t c = all_fast ? (uint8_t)kFast : (sa == sb ? p.cls[sa] : (uint8_t)0xff);
       if (c == kFast) {
         if (p.merged) {
