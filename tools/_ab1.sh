@@ -1,6 +1,6 @@
 mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu --timeout 400 -p no:cacheprovider -rf -x > gpurun_out/pytest_gpu_r2l.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu_r2l.log
 for i in 1 2; do
-  for v in ab_v1 ab_v2 ab_v3 .; do
-    (cd $v && timeout 600 python bench.py --config c5 --no-e2e --no-cpu --steps 10 > $GRAFT_REPO_ROOT/gpurun_out/ab1_$(basename $v)_c5_$i.json 2>&1)
-  done
+  timeout 600 python bench.py --config c5 --no-e2e --no-cpu --steps 10 > gpurun_out/ab1_cur_c5_$i.json 2>&1
+  timeout 600 python bench.py --no-e2e --no-cpu --steps 10 > gpurun_out/ab1_cur_c2_$i.json 2>&1
 done
