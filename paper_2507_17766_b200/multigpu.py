@@ -954,21 +954,25 @@ class ShardedButterflyMerge:
         return [(op, self._t0.elapsed_time(ev)) for op, ev in self._marks]
 
     def launches_per_run(self) -> int:
-        """Our kernels per round on this rank (bench.py gpu_launches)."""
-        fin = 3 + (1 if self.plan_r > 2 else 0)  # k_stats, k_decide, [k_entries3], k_apply
+        """Our kernels per round on this rank (bench.py gpu_launches); the re-broadcast of
+        mispredicted shards (none in the benchmarked rounds) is not counted."""
+        # FINISH: k_nonfinite, k_stats, k_decide, [k_entries3], k_apply; CHECK: k_nonfinite
+        fin = 4 + (1 if self.plan_r > 2 else 0)
         if self.world == 1:
-            return 2 + self.K + (fin if self.job.needs_finish() else 0)
-        if self.fused:  # k_ring (+ k_fill_nan, k_classify [, FINISH for r = 3] on the last rank)
-            return 3 + (fin if self.job.needs_finish() else 0) if self.is_last else 1
+            return 2 + self.K + (fin if self.job.needs_finish() else 1)
+        if self.fused:  # k_ring; the last rank adds k_fill_nan, k_classify and FINISH or CHECK,
+            # the others k_fill_shards
+            return 3 + (fin if self.job.needs_finish() else 1) if self.is_last else 2
         if self.is_last:
-            n = 2 + self.K  # k_fill_nan + k_classify, then one k_reduce per chunk
+            n = 2 + self.K + 1  # k_fill_nan + k_classify, one k_reduce per chunk, k_nonfinite (last chunk)
             if self._late_mode:
                 n += fin * sum(1 for b, e in self._finish_ranges if e > b)
                 n += fin if self.straddlers else 0
             n += 2 if self._fb_buf is not None else 0  # straddlers' fallback ranges: gather + scatter
             n += 1 if self.special_runs else 0  # late ranges packed for the broadcast
             return n
-        return 2 * self.K + (1 if self.special_runs else 0)  # k_chain + k_fanout per chunk
+        # k_chain + k_fanout per chunk, [late ranges scattered], k_fill_shards
+        return 2 * self.K + (1 if self.special_runs else 0) + 1
 
     def bytes_per_round(self) -> dict:
         """Algorithmic HBM and NVLink bytes of this rank for one round."""

@@ -192,3 +192,51 @@ def test_fused_ring_rejects_bad_descriptors():
         call(world=17)
     with pytest.raises(NotImplementedError):
         call(world=8, nb=70)  # 7 x (8 + 70) + 1 > 512 schedule words per lane
+
+
+def test_round2_entry_points_check_arguments_before_cuda():
+    """The round-2 entry points reject bad arguments with the mapped status before any
+    CUDA call (so on a machine without a GPU too)."""
+    import ctypes
+
+    from paper_2507_17766_b200 import _lib as L
+
+    lib = L.lib()
+    descs = (L.RingFusedDesc * 2)()
+    assert lib.bfly_ring_fused_loopback(descs, 1, None) == L.E_INVALID_ARG  # world < 2
+    assert lib.bfly_ring_fused_loopback(descs, 9, None) == L.E_INVALID_ARG  # world > 8
+    descs[0].rank, descs[1].rank = 0, 0  # rank 1 mislabelled
+    descs[0].world = descs[1].world = 2
+    assert lib.bfly_ring_fused_loopback(descs, 2, None) == L.E_INVALID_ARG
+    assert b"disagree" in lib.bfly_last_error()
+    assert lib.bfly_fill_shards(None, None, None, None, 1, L.F32, 100, 10, None) == L.E_INVALID_ARG
+    assert lib.bfly_permutation_host(-1, 0, 0, None) == L.E_INVALID_ARG
+    out = (ctypes.c_int64 * 5)()
+    assert lib.bfly_permutation_host(5, 1, 2, out) == L.OK
+    assert sorted(out) == [0, 1, 2, 3, 4]
+    assert lib.bfly_ring_fused_stat_tile(L.F64WIRE) == 0
+    assert lib.bfly_ring_fused_stat_tile(L.F32) % 1024 == 0
+    out_s = ctypes.c_void_p()
+    assert lib.bfly_stream_create(0, None) == L.E_INVALID_ARG
+
+
+def test_plan_shards_custom_pair_set_matches_reference():
+    """A caller-built PairSet (a subset of pairs, another order) is permuted as the
+    reference permutes it, pairs[order[s]] (butterfly.py:98-100)."""
+    import importlib
+
+    import pytest
+
+    try:
+        ref = importlib.import_module("iota_sim.butterfly")
+    except ImportError:
+        pytest.skip("the reference (baseline/_ref) is not installed")
+    from paper_2507_17766_b200 import butterfly as bf
+
+    for pairs, P, seed in [(((0, 1), (2, 3), (0, 2)), 30, 5), (((3, 4), (0, 1), (1, 4), (0, 3), (2, 3)), 101, 2**63 + 7),
+                           (tuple((i, j) for i in range(6) for j in range(i + 1, 6))[::-1], 77, 11)]:
+        ps = ref.PairSet(6, pairs)
+        want = ref.plan_shards(ps, P, 4, seed)
+        got = bf.plan_shards(ps, P, 4, seed)
+        assert got.assignment == want.assignment and got.bounds == want.bounds
+        assert type(got) is type(want)

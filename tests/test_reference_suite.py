@@ -117,3 +117,48 @@ def test_orchestrator_scenario_csvs_byte_identical(cuda_device, tmp_path):
         hashes[arm] = {p.name: hashlib.sha256(p.read_bytes()).hexdigest() for p in sorted(out.glob("*.csv"))}
     assert len(hashes["reference"]) >= 6
     assert hashes["b200"] == hashes["reference"]
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_broadcastable_callable_outputs_match_reference(cuda_device):
+    """A corruption callable returning a scalar: a lone survivor's scalar is
+    broadcast into merged (numpy assignment, butterfly.py:263); two survivors whose outputs
+    have different shapes raise ShapeError in agreement (:125-126); equal-shape scalars
+    are compared and adopted.  The drop-in against the reference itself, in-process."""
+    import numpy as np
+
+    sys.path.append(str(REF))
+    import iota_sim.butterfly as ref
+    from iota_sim.errors import ShapeError as RefShapeError
+    from iota_sim.simkernel import BlobStore as RefStore
+
+    from paper_2507_17766_b200 import butterfly as bf
+
+    def run(mod, n, P, seed, failures, corr):
+        rng = np.random.default_rng(seed)
+        payloads = {m: rng.uniform(-1, 1, P) for m in range(n)}
+        plan = ref.plan_shards(ref.enumerate_pairs(n), P, 4, seed)
+        store = RefStore()
+        res = mod.run_all_reduce(store, payloads, plan, failures=frozenset(failures), corruptions=corr)
+        meter = {a: (m.bytes_uploaded, m.bytes_downloaded) for a, m in store.meter.items()}
+        return res, meter, {k: bytes(v) for k, v in store.objects.items()}
+
+    cases = [
+        (3, 31, 1, {0, 1}, {2: lambda red: np.float64(3.0)}),          # lone survivor: broadcast
+        (2, 17, 2, set(), {0: lambda red: np.float64(5.0), 1: lambda red: np.float64(5.0)}),  # equal scalars
+        (2, 17, 3, set(), {0: lambda red: np.full(1, 2.0), 1: lambda red: np.full(1, 2.5)}),   # (1,) copies disagree
+    ]
+    for n, P, seed, failures, corr in cases:
+        want, wmeter, wobj = run(ref, n, P, seed, failures, corr)
+        got, gmeter, gobj = run(bf, n, P, seed, failures, corr)
+        assert np.array_equal(np.asarray(got.merged).view(np.uint64), np.asarray(want.merged).view(np.uint64))
+        assert got.shard_status == want.shard_status and got.flagged == want.flagged
+        assert np.array_equal(np.isnan(got.agreement_matrix.entries), np.isnan(want.agreement_matrix.entries))
+        m = ~np.isnan(want.agreement_matrix.entries)
+        assert np.allclose(got.agreement_matrix.entries[m], want.agreement_matrix.entries[m], rtol=0, atol=1e-12)
+        assert gmeter == wmeter and gobj == wobj
+    # different shapes on the two survivors: ShapeError from both (the reference's class)
+    for mod in (ref, bf):
+        with pytest.raises(RefShapeError):
+            run(mod, 3, 31, 4, set(), {2: lambda red: np.float64(3.0)})
