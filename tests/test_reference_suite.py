@@ -147,7 +147,7 @@ def test_broadcastable_callable_outputs_match_reference(cuda_device):
     cases = [
         (3, 31, 1, {0, 1}, {2: lambda red: np.float64(3.0)}),          # lone survivor: broadcast
         (2, 17, 2, set(), {0: lambda red: np.float64(5.0), 1: lambda red: np.float64(5.0)}),  # equal scalars
-        (2, 17, 3, set(), {0: lambda red: np.full(1, 2.0), 1: lambda red: np.full(1, 2.5)}),   # (1,) copies disagree
+        (2, 17, 3, set(), {0: lambda red: np.full(1, 2.0), 1: lambda red: np.full(1, -2.0)}),  # (1,) copies disagree
     ]
     for n, P, seed, failures, corr in cases:
         want, wmeter, wobj = run(ref, n, P, seed, failures, corr)
