@@ -172,7 +172,8 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
   if (!h_payloads || !d_wire || !args || n < 1 || P < 1 || n_chunks < 1)
     return fail(BFLY_E_INVALID_ARG, "bad merge-host arguments");
   if (h_merged && !args->d_merged) return fail(BFLY_E_INVALID_ARG, "h_merged needs d_merged");
-  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  // the calling thread issues the reduce of each chunk: the workers take the other cores
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency() - 1);
   Pool* pool = nullptr;
   int rc = get_pool(threads, block, &pool);
   if (rc) return rc;
@@ -200,6 +201,8 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
   cudaEventRecord(start, st);
   std::unique_ptr<std::atomic<int>[]> queued(new std::atomic<int>[NC]);
   for (int c = 0; c < NC; ++c) queued[c].store(0);
+  std::mutex q_mu;
+  std::condition_variable q_cv;  // a worker finished queueing a chunk (the caller sleeps, not spins)
   std::atomic<int64_t> next{0};
   std::atomic<int> err{BFLY_OK};
   std::string err_msg;
@@ -217,7 +220,10 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
     auto pass = [&](int upto) {  // mark chunks [cur, upto) queued on this worker's stream
       for (; cur < upto; ++cur) {
         cudaEventRecord(ev[(size_t)t * NC + cur], w.stream);
-        queued[cur].fetch_add(1);
+        if (queued[cur].fetch_add(1) + 1 == threads) {
+          std::lock_guard<std::mutex> lk(q_mu);
+          q_cv.notify_one();
+        }
       }
     };
     for (int64_t id = next.fetch_add(1); id < total; id = next.fetch_add(1)) {
@@ -244,7 +250,10 @@ extern "C" int bfly_merge_host(const double* const* h_payloads, int32_t n, int64
   a.n_shard_list = 0;
   int result = BFLY_OK;
   for (int c = 0; c < NC; ++c) {
-    while (queued[c].load() < threads) std::this_thread::yield();
+    {
+      std::unique_lock<std::mutex> lk(q_mu);
+      q_cv.wait(lk, [&] { return queued[c].load() >= threads; });
+    }
     if (result != BFLY_OK || err.load() != BFLY_OK) continue;
     for (int t = 0; t < threads; ++t) cudaStreamWaitEvent(st, ev[(size_t)t * NC + c], 0);
     a.elem_begin = (int64_t)c * CL;
