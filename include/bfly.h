@@ -177,7 +177,7 @@ int bfly_chain_step(const void* const* d_src, int32_t n_src, int32_t dtype, cons
 
 /* Upload n fp64 host payloads of P elements (pageable or pinned) as fp32 wire
  * values ("<f4", butterfly.py:213) into the device buffers d_wire[i]: `threads`
- * host threads (0 = all cores) convert blocks of `block` elements (0 = 512 Ki, 2 MB
+ * host threads (0 = all cores) convert blocks of `block` elements (0 = 384 Ki, 1.5 MB
  * copies) into a ring of pinned staging slots while earlier slots are copied, so
  * conversion and PCIe overlap.  Returns when the last copy has been issued on
  * `stream` (the host payloads may be reused after the stream reaches that point). */

@@ -603,7 +603,7 @@ def _render_special(job, plan, failed, descriptors, classes, host_reductions, no
     return out
 
 
-_UPLOAD_BLOCK = 0  # elements per staging block of the host upload (0: the library's 512 Ki)
+_UPLOAD_BLOCK = 0  # elements per staging block of the host upload (0: the library default, 384 Ki)
 
 
 def _merge_chunks(P: int) -> int:

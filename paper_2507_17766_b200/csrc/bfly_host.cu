@@ -35,7 +35,7 @@ namespace {
 // itself, so no thread ever waits for another.  Blocks are small enough that the
 // ring's lines are still in the host's last-level cache when the copy engine reads
 // them back: the host memory traffic stays near the 8 B/element of the fp64 read.
-constexpr int64_t kDefaultBlock = 1 << 19;  // 2 MB copies: tools/upload_probe.py
+constexpr int64_t kDefaultBlock = 3 << 17;  // 1.5 MB copies: best of tools/e2e_probe.py (profiles/r02_e2e_probe.log)
 constexpr int kRing = 3;                     // staging slots per worker
 
 struct Worker {
