@@ -89,6 +89,15 @@ class Corruption:
     "noise_add" (mean + a * (2u - 1)), where u is word e of Philox4x64-10 keyed
     by ``key`` for global element e — counter-based, so miners sharing a key
     (colluders) produce identical copies.
+
+    Portability of the decision: the reference adopts a pair of copies when
+    ``agreement == 1.0``, which holds when max|a - b| <= tolerance OR when the clamped
+    cosine rounds to exactly 1.0.  The second clause depends on the order of the dot
+    products (the reference's BLAS ddot; fixed-order trees here), so for copies (nearly)
+    parallel to the honest mean — a positive ``scale``, an ``add`` tiny against the mean,
+    one noise key at two amplitudes — the GPU and the reference may decide differently.
+    Decisions are bit-exact for corruptions that move the copy off that direction
+    (``noise``, ``noise_add`` / ``add`` beyond the tolerance, a negative ``scale``).
     """
 
     kind: str
