@@ -116,6 +116,7 @@ class _LayerMerge:
     def __init__(self, layer: StageLayer, seed: int, epoch: int, stage_label: str, b_min: int, dropped: set,
                  deceptive: str):
         self.layer = layer
+        self.stage_label = stage_label
         self.roster = [m for m in layer.roster if m.active]
         self.qualifying = [m for m in self.roster if m.batches_done >= b_min and m.miner_id not in dropped]
         self.L = L = layer.layer_index
@@ -234,8 +235,6 @@ def merge_stage(store, layers: list, *, seed: int, epoch: int, stage_label: str,
     store.wire_ratio = compression_ratio if compressed else 1.0
     try:
         parts = [_LayerMerge(layer, seed, epoch, stage_label, b_min, dropped, deceptive) for layer in layers]
-        for part in parts:
-            part.stage_label = stage_label
         _run_device_merges([p.job for p in parts if p.job is not None], graph)
         for part in parts:
             part.settle(store)

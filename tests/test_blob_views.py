@@ -46,3 +46,26 @@ def test_snapshot_store_copies_at_round_end(monkeypatch):
     v[3] = 123.0  # the caller mutates its payload after the round
     assert snap == np.linspace(-1, 1, 37).astype("<f4").tobytes()
     assert bytes(lazy)[12:16] == np.float32(123.0).tobytes()  # documented aliasing of the view
+
+
+def test_lone_qualifier_blob_has_the_serialized_header():
+    """A layer with one qualifying miner publishes serialize_weights' header + "<f4" weights
+    (orchestrator.py:528-540, model.py:147-154); ranged reads span the header boundary."""
+    import struct
+
+    from paper_2507_17766_b200 import stage
+    from paper_2507_17766_b200.simkernel import BlobStore
+
+    import torch
+
+    w = torch.linspace(-2, 2, 23, dtype=torch.float64)  # (HBM in the stage; the CPU works the same)
+    layer = stage.StageLayer(roster=[stage.RosterEntry("a"), stage.RosterEntry("b")], weights={"a": w},
+                             synced=w, layer_index=3, shape=(1, 22))
+    store = BlobStore()
+    stage._lone_blob(store, "p", layer, "a", w, layer.roster, 3, w.size)
+    full = struct.pack("<iiii", 3, 22, 1, 0) + w.numpy().astype("<f4").tobytes()
+    blob = store.objects["p/miner/a/weights"]
+    for a, b in [(0, 5), (10, 21), (16, 20), (3, len(full)), (0, len(full))]:
+        assert blob[a:b] == full[a:b], (a, b)
+    assert bytes(blob) == full
+    assert store.meter["a"].bytes_uploaded == len(full) and store.meter["b"].bytes_downloaded == len(full)
