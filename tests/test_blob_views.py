@@ -62,7 +62,7 @@ def test_lone_qualifier_blob_has_the_serialized_header():
     layer = stage.StageLayer(roster=[stage.RosterEntry("a"), stage.RosterEntry("b")], weights={"a": w},
                              synced=w, layer_index=3, shape=(1, 22))
     store = BlobStore()
-    stage._lone_blob(store, "p", layer, "a", w, layer.roster, 3, w.size)
+    stage._lone_blob(store, "p", layer, "a", w, layer.roster, 3, w.numel())
     full = struct.pack("<iiii", 3, 22, 1, 0) + w.numpy().astype("<f4").tobytes()
     blob = store.objects["p/miner/a/weights"]
     for a, b in [(0, 5), (10, 21), (16, 20), (3, len(full)), (0, len(full))]:
