@@ -759,9 +759,23 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
                            "d"(D::widen(acc[k + 1]))
                            : "memory");
           }
+          if (ts.lo == ts.hi) {  // the whole tile in one special / lost shard: no per-element lookups
+            const uint8_t c = p.sp.cls[ts.lo], pr = p.sp.pred[ts.lo] & kPredMask;
+            const bool fb_out = pr == kPredFallback;
+            // merged gets the final value where final_value would write it
+            const bool to_merged = p.merged && (fb_out ? (c == kLost || p.sp.merged_apart)
+                                                       : (pr == kPredMean && p.sp.merged_apart));
 #pragma unroll
-          for (int k = 0; k < KE; ++k)
-            v[k] = final_value<D>(p, e0 + k, D::widen(acc[k]), need_fb ? fb + k : nullptr, sk[k], ws_vec);
+            for (int k = 0; k < KE; ++k) v[k] = fb_out ? fb[k] : D::widen(acc[k]);
+            if (to_merged) {
+#pragma unroll
+              for (int k = 0; k < KE; ++k) p.merged[e0 + k] = v[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < KE; ++k)
+              v[k] = final_value<D>(p, e0 + k, D::widen(acc[k]), need_fb ? fb + k : nullptr, sk[k], ws_vec);
+          }
           *reinterpret_cast<uint4*>(out + tid * 16) = pack16d<D>(v);
         } else {
           if (p.merged) {
