@@ -736,9 +736,7 @@ __global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* cons
 
 // Pair statistics of the special shards' tiles k_reduce did not cover (tiles shared
 // by two shards, partial tiles at element-range edges, r = 3, host copies).
-__global__ void __launch_bounds__(kThreads) k_stats(Params p) {
-  const int64_t s = fin_shard(p, blockIdx.x);
-  if (p.cls[s] != kSpecial) return;
+__device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
   const int64_t start = p.bnd.start(s), hi_s = start + p.bnd.len(s);
   const int32_t* mem = p.assign + s * p.r;
   bool alive[kMaxR];
@@ -747,11 +745,11 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
     alive[k] = !p.failed[mem[k]];
     c[k] = p.corr[mem[k]];
   }
-  // the CTAs of a shard take its tiles in turn (blockIdx.y, stride gridDim.y) and
-  // skip the ones k_reduce already covered (done[]); one slot per tile, so the order of
-  // the work does not matter
+  // the parts of a shard take its tiles in turn (part y, stride ny) and skip the ones the
+  // reduce already covered (done[]); one slot per tile, so the order of the work does not
+  // matter
   const int64_t t_first = start / p.stile, t_last = (hi_s - 1) / p.stile;
-  for (int64_t t = t_first + (int64_t)blockIdx.y; t <= t_last; t += (int64_t)gridDim.y) {
+  for (int64_t t = t_first + y; t <= t_last; t += ny) {
     if (p.done[t]) continue;  // uniform across the CTA
     const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
     const int64_t g_lo = lo & ~(int64_t)7;
@@ -782,6 +780,16 @@ __global__ void __launch_bounds__(kThreads) k_stats(Params p) {
           o[3] = st.bb;
         }
       }
+  }
+}
+
+// A persistent grid walks (shard, part) items: most shards are fast and cost one byte
+// load, not a CTA launch each (2016 shards x 64 parts at 64 miners).
+__global__ void __launch_bounds__(kThreads) k_stats(Params p, int ny) {
+  const int64_t items = (int64_t)p.n_fin * ny;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t s = fin_shard(p, (unsigned)(it / ny));
+    if (p.cls[s] == kSpecial) stats_part(p, s, (int)(it % ny), ny);
   }
 }
 
@@ -875,14 +883,9 @@ __global__ void k_entries3(Params p) {
 }
 
 template <class D>
-__global__ void __launch_bounds__(kThreads) k_apply(Params p) {
-  extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
-  const int64_t s = fin_shard(p, blockIdx.x);
+__device__ void apply_chunk(const Params& p, void* const* s_dst, bool aligned, int64_t s, int64_t ch) {
   const uint8_t c = p.cls[s];
-  if (c == kFast) return;
-  void** s_dst = const_cast<void**>(s_ptr);
-  const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, (uintptr_t)p.merged);
-  const int64_t lo = p.bnd.start(s) + (int64_t)blockIdx.y * kChunk;
+  const int64_t lo = p.bnd.start(s) + ch * kChunk;
   const int64_t hi_s = p.bnd.start(s) + p.bnd.len(s);
   const int64_t hi = lo + kChunk < hi_s ? lo + kChunk : hi_s;
   const int32_t src_m = p.source[s];
@@ -937,6 +940,19 @@ __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
         for (int d = 0; d < n_dst; ++d) D::store(s_dst[d], e0 + i, v[i]);
       }
     }
+  }
+}
+
+// A persistent grid walks (shard, chunk) items; fast shards are skipped with one byte load.
+template <class D>
+__global__ void __launch_bounds__(kThreads) k_apply(Params p) {
+  extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
+  void** s_dst = const_cast<void**>(s_ptr);
+  const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, (uintptr_t)p.merged);
+  const int64_t items = (int64_t)p.n_fin * p.cps;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t s = fin_shard(p, (unsigned)(it / p.cps));
+    if (p.cls[s] != kFast) apply_chunk<D>(p, s_dst, aligned, s, it % p.cps);
   }
 }
 
@@ -1145,7 +1161,9 @@ template <class D>
 static void launch_apply(const Params& p, cudaStream_t st) {
   const size_t smem = sizeof(void*) * (size_t)(p.n_dst > 0 ? p.n_dst : 1);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_apply<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_apply<D><<<dim3((unsigned)p.n_fin, (unsigned)p.cps), kThreads, smem, st>>>(p);
+  int64_t grid = (int64_t)p.n_fin * p.cps;
+  if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+  k_apply<D><<<(unsigned)(grid < 1 ? 1 : grid), kThreads, smem, st>>>(p);
 }
 
 extern "C" {
@@ -1327,7 +1345,9 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
     // up to 64 CTAs per shard: a shard whose tiles were not covered by k_reduce (the
     // multi-GPU persistent ring computes no statistics) spreads over the GPU
     const int64_t ny = tps < 64 ? tps : 64;
-    k_stats<<<dim3(ns, (unsigned)ny), kThreads, 0, st>>>(p);
+    int64_t sgrid = (int64_t)ns * ny;
+    if (sgrid > (int64_t)sm_count() * 8) sgrid = (int64_t)sm_count() * 8;
+    k_stats<<<(unsigned)(sgrid < 1 ? 1 : sgrid), kThreads, 0, st>>>(p, (int)ny);
     k_decide<<<ns, 32, 0, st>>>(p);
     if (p.r > 2) {
       const int64_t nn = (int64_t)p.n * p.n;
