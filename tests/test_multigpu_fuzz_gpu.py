@@ -43,14 +43,14 @@ print("rank", rank, "ok", fused_seen, "fused of", n_cases)
 '''
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_multigpu_fuzz_loopback(world, cuda_device):
     """The same seeded cases with every rank a thread on ONE GPU (multigpu.run_loopback)."""
     from _multigpu_cases import fuzz_case, fuzz_rank
 
     from paper_2507_17766_b200.multigpu import run_loopback
 
-    n_cases = {2: 24, 3: 12, 4: 12}[world]
+    n_cases = {2: 24, 3: 12, 4: 12, 8: 6}[world]
     fused_seen = 0
     for case in range(n_cases):
         c = fuzz_case(case, world)

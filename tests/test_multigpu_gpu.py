@@ -73,6 +73,12 @@ CASES = [
     {"counts": [4, 4, 4, 4], "P": 2_000_039, "seed": 28, "failures": [],
      "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "9": [3, 2.0, 24301, 9], "15": [3, 2.0, 24301, 15]},
      "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2},
+    # eight ranks (config 3's G = 8 layout at reduced size): honest and adversarial
+    {"counts": [2] * 8, "P": 1_500_007, "seed": 33, "failures": [], "corr": {}, "fallback": False,
+     "chunk": 1 << 20, "fused": True, "rounds": 3},
+    {"counts": [2] * 8, "P": 1_200_011, "seed": 34, "failures": [5],
+     "corr": {"1": [3, 2.0, 24301, 1], "9": [3, 2.0, 24301, 9], "14": [3, 2.0, 24301, 14]},
+     "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2},
     # the same with the pair statistics accumulated inside k_ring (fuse_stats)
     {"counts": [3, 5], "P": 2_000_029, "seed": 32, "failures": [],
      "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "7": [1, 0.0]},
