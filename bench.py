@@ -477,7 +477,9 @@ def run_multi(cfg, args, rank, world):
     plan = DevicePlan(n, P, 0, redundancy=r, device=dev)
     bad = deceptive_set(n, k_bad)
     corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in bad}
-    job = ShardedButterflyMerge(reps, plan, corruptions=corr, chunk=args.chunk, fuse_stats=args.fuse_stats)
+    tuning = json.loads(args.ring_tuning) if args.ring_tuning else None
+    job = ShardedButterflyMerge(reps, plan, corruptions=corr, chunk=args.chunk, fuse_stats=args.fuse_stats,
+                                ring_tuning=tuning)
     nvcount = NVLinkCounter(local_rank)
     phases = None
     if args.timing:  # one extra round with CUDA events between the phases (diagnostics, untimed)
@@ -737,6 +739,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--timing", action="store_true", help="multi-GPU: per-phase times of one extra round")
     ap.add_argument("--fuse-stats", action="store_true", help="multi-GPU: pair statistics inside k_ring")
+    ap.add_argument("--ring-tuning", default=None, help='multi-GPU experiments, e.g. \'{"slots": 12, "lag": 2}\'')
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -427,6 +427,9 @@ class ShardedButterflyMerge:
                  shards' pair statistics (instead of k_stats after the kernel, on every
                  SM).  Off by default: the Philox noise of the corrupted copies makes the
                  last rank's compute warps the round's critical path.
+    ring_tuning  persistent ring experiments: {"slots": inbox slots per lane (default
+                 FUSED_NB), "lag": publication lag 1..3, "pub_every": publish every k-th
+                 step} (bfly.h; defaults are the measured best).
     debug / timing    diagnostics of the chunked ring (per-op watchdog, timeline) and
                  per-phase CUDA-event times of a round (``.timings``).
     """
@@ -434,9 +437,10 @@ class ShardedButterflyMerge:
     def __init__(self, local: list, plan, *, failures=(), corruptions=None, fallback=None,
                  want_merged: bool = False, tolerance: float = 1e-6, chunk: int = 1 << 24, comm=None,
                  executor: str = "auto", per_chunk_finish: bool = True, debug: int = 0, timing: bool = False,
-                 fuse_stats: bool = False):
+                 fuse_stats: bool = False, ring_tuning: dict | None = None):
         self.comm = comm if comm is not None else DistComm()
         self.fuse_stats = bool(fuse_stats)
+        self.ring_tuning = dict(ring_tuning or {})
         self.rank = self.comm.rank
         self.world = G = self.comm.world
         if executor not in ("auto", "chunked"):
@@ -637,10 +641,13 @@ class ShardedButterflyMerge:
         if self.lanes < 1:
             raise RuntimeError("fused ring: no co-resident lanes on this device")
         o = [ctypes.c_int64() for _ in range(3)]
-        L.check(lib.bfly_ring_fused_layout(self.lanes, FUSED_NB, self.dtype, *[ctypes.byref(x) for x in o]))
+        nb = self.ring_tuning.get("slots", FUSED_NB)
+        L.check(lib.bfly_ring_fused_layout(self.lanes, nb, self.dtype, *[ctypes.byref(x) for x in o]))
         self._open_region(o[2].value)
         d = L.RingFusedDesc()
-        d.rank, d.world, d.lanes, d.nb, d.dtype = self.rank, self.world, self.lanes, FUSED_NB, self.dtype
+        d.rank, d.world, d.lanes, d.nb, d.dtype = self.rank, self.world, self.lanes, nb, self.dtype
+        d.lag = int(self.ring_tuning.get("lag", 0))
+        d.pub_every = int(self.ring_tuning.get("pub_every", 0))
         d.n_src, d.n_dst, d.n_div = len(self.local_alive), len(self.local), len(self.alive)
         d.payload_len = self.P
         d.peer_base = ctypes.cast(self._peer_arr, ctypes.c_void_p)
