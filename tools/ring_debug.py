@@ -1,10 +1,10 @@
-"""Run one small multi-GPU merge with the ring watchdog on (BFLY_DEBUG_RING=1)."""
+"""Run one small multi-GPU merge with the ring watchdog on (debug=1: the watchdog of the chunked executor)."""
 import os
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-os.environ.setdefault("BFLY_DEBUG_RING", "1")
+
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -20,7 +20,7 @@ chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 4096 * 2
 nloc = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 local = [torch.rand(P, device=dev) for _ in range(nloc)]
 plan = DevicePlan(nloc * world, P, 0, device=dev)
-job = ShardedButterflyMerge(local, plan, chunk=chunk)
+job = ShardedButterflyMerge(local, plan, chunk=chunk, executor="chunked", debug=1)
 print(f"[rank {rank}] K={job.K} debug={job.debug}", flush=True)
 for r in range(3):
     job.run()

@@ -1,4 +1,4 @@
-"""Per-op completion times of one multi-GPU round (Python executor, BFLY_DEBUG_RING=3).
+"""Per-op completion times of one multi-GPU round (chunked executor issued from Python, debug=3).
 
     torchrun --nproc-per-node 4 tools/ring_timeline.py [--params 1e9] [--bad 6] [--miners-per-gpu 16]
 
@@ -13,7 +13,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-os.environ["BFLY_DEBUG_RING"] = "3"
+
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -35,7 +35,7 @@ n = nl * world
 local = make_replicas(nl, P, "fp32", dev, seed=rank * nl)
 plan = DevicePlan(n, P, 0, device=dev)
 corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in deceptive_set(n, a.bad)}
-job = ShardedButterflyMerge(local, plan, corruptions=corr)
+job = ShardedButterflyMerge(local, plan, corruptions=corr, executor="chunked", debug=3)
 for _ in range(3):
     job.run()
 tl = [[op[0], op[1], op[2], ms] for op, ms in job.timeline()]
