@@ -359,3 +359,40 @@ def test_captured_round_replays_match_oracle(cuda_device):
         assert np.array_equal(job.status.cpu().numpy(), want["status"])
         assert np.array_equal(job.flagged.cpu().numpy(), want["flagged"])
         assert_same_floats(dreps[0].cpu().numpy(), want["merged"].astype(np.float32))
+
+
+def test_store_snapshot_and_no_device_references(cuda_device, monkeypatch):
+    """Store ownership: by default the objects are views of the caller's payloads
+    and of the returned merged vector — no object keeps the round's device memory alive;
+    with SNAPSHOT_STORE every object is bytes when the call returns (simkernel.py:168)."""
+    import gc
+    import weakref
+
+    from paper_2507_17766_b200 import butterfly as bf
+    from paper_2507_17766_b200.device import ButterflyMerge, Corruption
+    from paper_2507_17766_b200.simkernel import BlobStore
+
+    n, P = 5, 10_007
+    rng = np.random.default_rng(8)
+    payloads = {f"m{k}": rng.uniform(-1, 1, P) for k in range(n)}
+    plan = bf.plan_shards(bf.enumerate_pairs(n), P, bf.BYTES_PER_WEIGHT, 3)
+    jobs = []
+    real_init = ButterflyMerge.__init__
+
+    def spy(self, *a, **k):
+        real_init(self, *a, **k)
+        jobs.append(weakref.ref(self))
+
+    monkeypatch.setattr(ButterflyMerge, "__init__", spy)
+    store = BlobStore()
+    res = bf.run_all_reduce(store, payloads, plan, corruptions={1: Corruption.noise(1.0, (2, 3))})
+    gc.collect()
+    assert jobs and all(j() is None for j in jobs), "a store object keeps the device job alive"
+    want = {k: bytes(v) for k, v in store.objects.items()}
+    monkeypatch.setattr(bf, "SNAPSHOT_STORE", True)
+    store2 = BlobStore()
+    res2 = bf.run_all_reduce(store2, payloads, plan, corruptions={1: Corruption.noise(1.0, (2, 3))})
+    assert all(isinstance(v, bytes) for v in store2.objects.values())
+    payloads["m0"][:] = 0.0  # the caller reuses its buffer: the snapshot does not change
+    assert {k: bytes(v) for k, v in store2.objects.items()} == want
+    assert_same_floats(res.merged, res2.merged)
