@@ -12,7 +12,8 @@ INTEGRATION.md §2/§4.  Nothing here reads /root/reference.
   (pkg/tests/test_acceptance.py:43-162,326-352);
 * GPU: a 3-epoch orchestrator scenario with deceptive and lazy miners and compressed
   sharing stages through the CLI (orchestrator.py:519-606, cli.py:85-136): every CSV
-  byte-identical with the drop-in patched in and with the reference as shipped.
+  byte-identical with the drop-in patched in and with the reference as shipped;
+* GPU: the reference's whole shipped suite (158 tests) with the attribute patch.
 """
 
 import hashlib
@@ -162,3 +163,15 @@ def test_broadcastable_callable_outputs_match_reference(cuda_device):
     for mod in (ref, bf):
         with pytest.raises(RefShapeError):
             run(mod, 3, 31, 4, set(), {2: lambda red: np.float64(3.0)})
+
+
+@pytest.mark.gpu
+@needs_ref
+def test_reference_whole_suite_through_dropin(cuda_device):
+    """Every test file the reference ships (pkg/tests: butterfly, acceptance, orchestrator,
+    CLI, validator, incentives, CLASP, simkernel, model, backends) — 158 tests — with the
+    drop-in patched in by attribute, so every merge the orchestrator
+    makes in those tests runs on the GPU."""
+    rc, out = _pytest([], mode="attribute", timeout=1800)
+    assert rc == 0, out[-6000:]
+    assert "158 passed" in out, out[-3000:]
