@@ -41,8 +41,16 @@ BFLY_HD Philox4x64 philox4x64_10(Philox4x64 c, uint64_t k0, uint64_t k1) {
 #pragma unroll
   for (int round = 0; round < 10; ++round) {
     if (round) {
+#if defined(__CUDA_ARCH__)
+      // opaque adds: the round keys are recomputed in every call instead of being hoisted
+      // out of the caller's element loop as 40 loop-invariant registers per key (which
+      // halved k_stats' occupancy, or spilled under a register cap)
+      asm volatile("add.u64 %0, %0, %1;" : "+l"(k0) : "l"(0x9E3779B97F4A7C15ULL));
+      asm volatile("add.u64 %0, %0, %1;" : "+l"(k1) : "l"(0xBB67AE8584CAA73BULL));
+#else
       k0 += 0x9E3779B97F4A7C15ULL;
       k1 += 0xBB67AE8584CAA73BULL;
+#endif
     }
     uint64_t hi0, lo0, hi1, lo1;
     mulhilo64(0xD2E7470EE14C6C93ULL, c.v[0], &hi0, &lo0);

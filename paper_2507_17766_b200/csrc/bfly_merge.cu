@@ -281,6 +281,30 @@ __device__ PairStat block_combine(PairStat s) {
   return s;
 }
 
+// The same combine through shared memory only (a fixed-order tree of barriers, no
+// shuffles): for loops whose convergence the compiler cannot prove, where warp
+// shuffles would be emulated collectively (WARPSYNC loops, extra live registers).
+__device__ PairStat block_combine_smem(PairStat s) {
+  __shared__ PairStat part[kThreads];
+  __syncthreads();  // the previous combine's readers are done
+  part[threadIdx.x] = s;
+  __syncthreads();
+#pragma unroll 1
+  for (int w = kThreads / 2; w; w >>= 1) {
+    if (threadIdx.x < w) {
+      PairStat u = part[threadIdx.x];
+      const PairStat v = part[threadIdx.x + w];
+      u.mx = max_nan(u.mx, v.mx);
+      u.ab = __dadd_rn(u.ab, v.ab);
+      u.aa = __dadd_rn(u.aa, v.aa);
+      u.bb = __dadd_rn(u.bb, v.bb);
+      part[threadIdx.x] = u;
+    }
+    __syncthreads();
+  }
+  return part[0];
+}
+
 // agreement decision from combined statistics (butterfly.py:127-133)
 __device__ __forceinline__ double score_of(const PairStat& s, double tol) {
   if (!isnan(s.mx) && s.mx <= tol) return 1.0;
@@ -349,6 +373,35 @@ __device__ __forceinline__ unsigned load_group(const double* ws, int64_t e0, int
     }
   }
   return valid;
+}
+
+// ws[e0..e0+3]: one 32-byte vector when the group is whole, masked scalars otherwise
+__device__ __forceinline__ unsigned load_group4(const double* ws, int64_t e0, int64_t lo, int64_t hi, double* m) {
+  if (e0 >= lo && e0 + 4 <= hi) {
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(m[0]), "=d"(m[1]), "=d"(m[2]), "=d"(m[3])
+                 : "l"(ws + e0));
+    return 0xf;
+  }
+  unsigned valid = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool in = e0 + i >= lo && e0 + i < hi;
+    m[i] = in ? ws[e0 + i] : 0.0;
+    valid |= (unsigned)in << i;
+  }
+  return valid;
+}
+
+// corrupt4 plus the caller-supplied copies of host callables (valid elements only)
+__device__ __forceinline__ void corrupt4h(const bfly_corruption_t& c, const double* m, int64_t e0, unsigned valid,
+                                          const double* host_copies, int slot, int64_t P, double* out) {
+  if (c.kind == BFLY_CORR_HOST) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[i] = (valid >> i) & 1 ? host_copies[(int64_t)slot * P + e0 + i] : 0.0;
+    return;
+  }
+  corrupt4(c, m, e0, out);
 }
 
 // Statistics of one vector (K means at e0, e0 % 4 == 0) for the copy pair (ca, cb).
@@ -739,12 +792,6 @@ __global__ void __launch_bounds__(kThreads) k_fanout(const void* src, void* cons
 __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
   const int64_t start = p.bnd.start(s), hi_s = start + p.bnd.len(s);
   const int32_t* mem = p.assign + s * p.r;
-  bool alive[kMaxR];
-  bfly_corruption_t c[kMaxR];
-  for (int k = 0; k < p.r; ++k) {
-    alive[k] = !p.failed[mem[k]];
-    c[k] = p.corr[mem[k]];
-  }
   // the parts of a shard take its tiles in turn (part y, stride ny) and skip the ones the
   // reduce already covered (done[]); one slot per tile, so the order of the work does not
   // matter
@@ -752,26 +799,31 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
   for (int64_t t = t_first + y; t <= t_last; t += ny) {
     if (p.done[t]) continue;  // uniform across the CTA
     const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
-    const int64_t g_lo = lo & ~(int64_t)7;
+    const int64_t g_lo = lo & ~(int64_t)3;
     for (int a = 0; a < p.r; ++a)
       for (int b = a + 1; b < p.r; ++b) {
-        if (!alive[a] || !alive[b]) continue;
+        if (p.failed[mem[a]] || p.failed[mem[b]]) continue;
+        // the two descriptors in registers (a runtime-indexed local array lives on the stack)
+        const bfly_corruption_t ca = p.corr[mem[a]], cb = p.corr[mem[b]];
         PairStat st{0.0, 0.0, 0.0, 0.0};
-        for (int64_t e0 = g_lo + 8 * (int64_t)threadIdx.x; e0 < hi; e0 += 8 * kThreads) {
-          double m[8], x[8], y[8];
-          const unsigned valid = load_group(p.ws, e0, lo, hi, m);
-          corrupt8(c[a], m, e0, valid, p.host_copies, a, p.P, x);
-          corrupt8(c[b], m, e0, valid, p.host_copies, b, p.P, y);
+        // four elements (one Philox block per noisy copy) per thread and step: few live
+        // registers, so 4 CTAs per SM hide the Philox dependency chains
+#pragma unroll 1
+        for (int64_t e0 = g_lo + 4 * (int64_t)threadIdx.x; e0 < hi; e0 += 4 * kThreads) {
+          double m[4], x[4], z[4];
+          const unsigned valid = load_group4(p.ws, e0, lo, hi, m);
+          corrupt4h(ca, m, e0, valid, p.host_copies, a, p.P, x);
+          corrupt4h(cb, m, e0, valid, p.host_copies, b, p.P, z);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < 4; ++i) {
             if (!((valid >> i) & 1)) continue;
-            st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
-            st.ab = fma(x[i], y[i], st.ab);
+            st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], z[i])));
+            st.ab = fma(x[i], z[i], st.ab);
             st.aa = fma(x[i], x[i], st.aa);
-            st.bb = fma(y[i], y[i], st.bb);
+            st.bb = fma(z[i], z[i], st.bb);
           }
         }
-        st = block_combine(st);
+        st = block_combine_smem(st);
         if (threadIdx.x == 0) {
           double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
           o[0] = st.mx;
@@ -785,7 +837,7 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
 
 // A persistent grid walks (shard, part) items: most shards are fast and cost one byte
 // load, not a CTA launch each (2016 shards x 64 parts at 64 miners).
-__global__ void __launch_bounds__(kThreads) k_stats(Params p, int ny) {
+__global__ void __launch_bounds__(kThreads, 4) k_stats(Params p, int ny) {
   const int64_t items = (int64_t)p.n_fin * ny;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t s = fin_shard(p, (unsigned)(it / ny));

@@ -71,6 +71,8 @@ constexpr int kSR = 512;          // tile schedule ring per lane (rank 0 -> ever
 constexpr int kMaxG = 16;         // ranks the persistent ring supports
 constexpr int kMaxLag = 3;        // a step is published p.lag (1..3) steps later, when its bytes have landed
 constexpr int kTileBytes = 4096;  // one replica's share of a tile
+constexpr int kNQ = 32;           // FUSE: special tiles the compute warps may lead the stats warps by
+constexpr int kStatWarps = 2;     // FUSE: the last rank's (otherwise idle) relay warps
 
 struct RingParams {
   int g, G, L, NB;
@@ -117,9 +119,10 @@ struct RingGeom {
   static constexpr int OFF_REL = OFF_OUT + kNO * OUT_SLOT;
   static constexpr int OFF_BAR = OFF_REL + kNR * FIN_SLOT;
   static constexpr int N_BAR = 2 * kNS + 2 * kNA + 2 * kNO + 2 * kNR + 2 * kNT;
-  // per-warp partial pair statistics of a fused special tile (double-buffered by step)
+  // FUSE: the stats queue (compute warps -> the last rank's stats warps): kNQ full
+  // barriers, kNQ (tile, shard) entries, progress + admit words, the stats partials (x2)
   static constexpr int OFF_STAT = OFF_BAR + 8 * (N_BAR + kNT + kNR + 4);
-  static constexpr int OFF_PTR = OFF_STAT + 2 * (kRingCompute / 32) * 32;
+  static constexpr int OFF_PTR = OFF_STAT + 24 * kNQ + 16 + 2 * kStatWarps * 32;
 };
 
 // ---------------------------------------------------------------------------
@@ -620,6 +623,113 @@ __device__ void ring_loader(const RingParams& p, const Lane& ln, unsigned char* 
   pf.flush();
 }
 
+// FUSE stats queue in shared memory: kNQ full barriers (the compute warps arrive after
+// their workspace stores: release.cta), kNQ (tile, shard) entries, the stats warps'
+// progress (entries finished) and the compute warps' enqueue decision.
+struct StatQ {
+  uint64_t* full;
+  volatile int64_t* ent;
+  volatile int64_t* progress;
+  volatile int* admit;
+  PairStat* part;  // [2][kStatWarps]
+  __device__ explicit StatQ(unsigned char* q)
+      : full(reinterpret_cast<uint64_t*>(q)),
+        ent(reinterpret_cast<volatile int64_t*>(q + 8 * kNQ)),
+        progress(reinterpret_cast<volatile int64_t*>(q + 24 * kNQ)),
+        admit(reinterpret_cast<volatile int*>(q + 24 * kNQ + 8)),
+        part(reinterpret_cast<PairStat*>(q + 24 * kNQ + 16)) {}
+};
+
+// Compute warps: offer special tile `tile` (one shard `shard`, means in the workspace) to
+// the stats warps as entry q.  Never waits: a full queue (the stats warps behind) leaves
+// the tile to FINISH's k_stats, so the stats can only take work off the ring's tail,
+// never slow its HBM stream.  Returns whether the tile was queued (uniform across the
+// compute warps: thread 0 decides, one named barrier).  tile -1 (the end marker) waits
+// for a free entry.
+__device__ __forceinline__ bool stats_offer(const RingParams& p, unsigned char* qmem, int64_t q, int64_t tile,
+                                            int64_t shard) {
+  const StatQ Q(qmem);
+  if (tile < 0) {
+    while (q - *Q.progress >= kNQ) __nanosleep(64);
+  } else {
+    if (threadIdx.x == 0) *Q.admit = q - *Q.progress < kNQ;
+    asm volatile("bar.sync 1, %0;" ::"n"(kRingCompute) : "memory");  // the compute warps only
+    const bool ok = *Q.admit;
+    asm volatile("bar.sync 1, %0;" ::"n"(kRingCompute) : "memory");  // admit read before the next write
+    if (!ok) return false;
+  }
+  const int k = (int)(q % kNQ);
+  if (threadIdx.x == 0) {
+    Q.ent[2 * k] = tile;
+    Q.ent[2 * k + 1] = shard;
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(Q.full + k);
+  return true;
+}
+
+// STATS warps (the last rank's two relay warps, FUSE): pair statistics of the queued
+// special tiles from the means in the workspace — the work FINISH's k_stats would do
+// after the kernel (Philox-bound: ~1.4 ms at config 5 on 4 GPUs), overlapped with the
+// HBM-bound ring.  One slot per (tile, shard), done[tile] = 1, as k_stats writes them.
+template <class D>
+__device__ void ring_stats(const RingParams& p, unsigned char* sm) {
+  using G = RingGeom<D>;
+  const StatQ Q(sm + G::OFF_STAT);
+  const int t = (int)threadIdx.x - kWRLoad * 32;  // 0 .. 63
+  const int w = t >> 5;
+  for (int64_t j = 0;; ++j) {
+    const int k = (int)(j % kNQ);
+    mbar_wait(p, Q.full + k, (unsigned)((j / kNQ) & 1));
+    const int64_t tile = Q.ent[2 * k], s = Q.ent[2 * k + 1];
+    if (tile < 0) break;
+    // (the entry is copied: thread 0 frees it only after the whole tile, below)
+    const int32_t* mem = p.sp.assign + s * 2;
+    const bfly_corruption_t ca = p.sp.corr[mem[0]], cb = p.sp.corr[mem[1]];
+    PairStat st{0.0, 0.0, 0.0, 0.0};
+    const int64_t t0 = tile * G::TE;
+#pragma unroll 1
+    for (int64_t e0 = t0 + 4 * t; e0 < t0 + G::TE; e0 += 4 * 32 * kStatWarps) {
+      double m[4], x[4], y[4];
+      // written by this CTA's compute warps before their release-arrive: a plain
+      // (coherent) load, not the non-coherent path
+      asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(m[0]), "=d"(m[1]) : "l"(p.sp.ws + e0) : "memory");
+      asm volatile("ld.global.v2.f64 {%0,%1}, [%2];" : "=d"(m[2]), "=d"(m[3]) : "l"(p.sp.ws + e0 + 2) : "memory");
+      corrupt4(ca, m, e0, x);
+      corrupt4(cb, m, e0, y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
+        st.ab = fma(x[i], y[i], st.ab);
+        st.aa = fma(x[i], x[i], st.aa);
+        st.bb = fma(y[i], y[i], st.bb);
+      }
+    }
+    st = warp_combine(st);
+    PairStat* part = Q.part + (j & 1) * kStatWarps;
+    if ((t & 31) == 0) part[w] = st;
+    asm volatile("bar.sync 2, %0;" ::"n"(32 * kStatWarps) : "memory");  // the stats warps only
+    if (t == 0) {
+      PairStat u = part[0];
+#pragma unroll
+      for (int v = 1; v < kStatWarps; ++v) {
+        u.mx = max_nan(u.mx, part[v].mx);
+        u.ab = __dadd_rn(u.ab, part[v].ab);
+        u.aa = __dadd_rn(u.aa, part[v].aa);
+        u.bb = __dadd_rn(u.bb, part[v].bb);
+      }
+      double* o = p.sp.stats + (tile + s) * 4;  // slot (tile, shard), r = 2: one pair
+      o[0] = u.mx;
+      o[1] = u.ab;
+      o[2] = u.aa;
+      o[3] = u.bb;
+      p.sp.done[tile] = 1;
+      __threadfence_block();
+      *Q.progress = j + 1;  // entry k is free again
+    }
+  }
+}
+
 // COMPUTE warps: running sums (chain) or sum and mean (REDUCE) of the lane's tiles.
 // FUSE (last rank, fuse_stats): also the special shards' pair statistics — a separate
 // instantiation, so the plain kernel keeps its lean register allocation.
@@ -637,12 +747,16 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
   ShardCursor cursor;  // the shards of this lane's (ascending) tiles
   const bool fb_pref = REDUCE && fb_prefetch_on(p);
   int64_t fu = 0;  // prefetched fallback tiles consumed so far
+  int64_t nq = 0;  // FUSE: special tiles handed to the stats warps
   Prof pf(p, threadIdx.x == 0 ? 4 : -1);
   if (threadIdx.x) pf.out = nullptr;
   for (int64_t i = 0;; ++i) {
     mbar_wait(p, B.tile_full + (int)(i % kNT), (unsigned)((i / kNT) & 1));
     const int64_t tile = B.tile_of[i % kNT];
-    if (tile < 0) break;
+    if (tile < 0) {
+      if constexpr (FUSE) stats_offer(p, sm + G::OFF_STAT, nq, -1, 0);  // the stats warps' end marker
+      break;
+    }
     const int64_t t0 = tile * G::TE;
     const int64_t n = min((int64_t)G::TE, p.P - t0);
     const int a = (int)(i % kNA);
@@ -722,33 +836,6 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
           } else if (need_fb) {
             fallback_vec16<D>(p, e0, fb);
           }
-          // a whole tile of one special shard with two device-computable copies: its pair
-          // statistics now, from the means in registers (FINISH's k_stats skips the tile)
-          const int64_t s_lo = ts.lo;
-          if (FUSE && ts.hi == s_lo && (p.sp.pred[s_lo] & kPredFuse)) {
-            const int32_t* mem = p.sp.assign + s_lo * 2;
-            PairStat st = ring_pair_stats<D>(acc, e0, p.sp.corr[mem[0]], p.sp.corr[mem[1]]);
-            st = warp_combine(st);
-            PairStat* part = reinterpret_cast<PairStat*>(sm + G::OFF_STAT) + (i & 1) * (kRingCompute / 32);
-            if (lead) part[tid >> 5] = st;
-            asm volatile("bar.sync 1, %0;" ::"n"(kRingCompute) : "memory");  // the compute warps only
-            if (tid == 0) {
-              PairStat t = part[0];
-#pragma unroll
-              for (int w = 1; w < kRingCompute / 32; ++w) {
-                t.mx = max_nan(t.mx, part[w].mx);
-                t.ab = __dadd_rn(t.ab, part[w].ab);
-                t.aa = __dadd_rn(t.aa, part[w].aa);
-                t.bb = __dadd_rn(t.bb, part[w].bb);
-              }
-              double* o = p.sp.stats + (tile + s_lo) * 4;  // slot (tile, shard), r = 2: one pair
-              o[0] = t.mx;
-              o[1] = t.ab;
-              o[2] = t.aa;
-              o[3] = t.bb;
-              p.sp.done[tile] = 1;
-            }
-          }
           // the means of a special shard to the workspace in one vector store
           const bool ws_vec = sk[0] == sk[KE - 1] && p.sp.cls[sk[0]] == kSpecial && KE % 2 == 0;
           if (ws_vec) {
@@ -758,6 +845,12 @@ __device__ void ring_compute(const RingParams& p, const Lane& ln, unsigned char*
               asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(w + k), "d"(D::widen(acc[k])),
                            "d"(D::widen(acc[k + 1]))
                            : "memory");
+          }
+          // a whole tile of one special shard with two device-computable copies: its means
+          // are in the workspace now; the stats warps take its pair statistics from there
+          // (FINISH's k_stats skips the tile), off the compute warps' critical path
+          if (FUSE && ts.hi == ts.lo && (p.sp.pred[ts.lo] & kPredFuse) && ws_vec) {
+            if (stats_offer(p, sm + G::OFF_STAT, nq, tile, ts.lo)) ++nq;
           }
           if (ts.lo == ts.hi) {  // the whole tile in one special / lost shard: no per-element lookups
             const uint8_t c = p.sp.cls[ts.lo], pr = p.sp.pred[ts.lo] & kPredMask;
@@ -1077,6 +1170,11 @@ __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
       mbar_init(B.tile_full + k, 1);   // the loader
       mbar_init(B.tile_empty + k, 1);  // the storer
     }
+    if (FUSE) {
+      const StatQ Q(sm + RingGeom<D>::OFF_STAT);
+      for (int k = 0; k < kNQ; ++k) mbar_init(Q.full + k, warps);  // every compute warp
+      *Q.progress = 0;
+    }
     B.mail[0] = ln.base_c;
     B.mail[1] = ln.base_r;
     B.mail[2] = B.mail[3] = 0;
@@ -1113,7 +1211,9 @@ __device__ __forceinline__ void ring_body(const RingParams& p, int lane) {
     }
   } else if (w == kWPub) {
     if (lead) ring_publisher<D>(p, ln, sm);
-  } else if (!last) {
+  } else if (last) {
+    if (FUSE && (w == kWRLoad || w == kWRStore)) ring_stats<D>(p, sm);
+  } else {
     if (w == kWRLoad) {
       if (lead) ring_relay_loader<D>(p, ln, sm);
     } else {

@@ -423,10 +423,11 @@ class ShardedButterflyMerge:
     executor     "auto" (the persistent ring whenever it applies) or "chunked".
     per_chunk_finish  chunked ring: the last rank decides each chunk's special shards
                  before relaying it (False: all after the ring; diagnostics).
-    fuse_stats   persistent ring: the last rank's compute warps accumulate the special
-                 shards' pair statistics (instead of k_stats after the kernel, on every
-                 SM).  Off by default: the Philox noise of the corrupted copies makes the
-                 last rank's compute warps the round's critical path.
+    fuse_stats   persistent ring: the last rank's idle relay warps compute the special
+                 shards' pair statistics during the ring (tiles offered through a
+                 shared-memory queue), instead of k_stats after the kernel on every SM.
+                 Off by default: FINISH shrinks 1.4 -> 0.3 ms but the queue slows the
+                 last rank's compute warps (4 GPUs: a net loss; 2 GPUs: a gain).
     ring_tuning  persistent ring experiments: {"slots": inbox slots per lane (default
                  FUSED_NB), "lag": publication lag 1..3, "pub_every": publish every k-th
                  step} (bfly.h; defaults are the measured best).
@@ -655,9 +656,9 @@ class ShardedButterflyMerge:
         d.d_dst = self._local_table.data_ptr()
         if self.is_last:
             d.d_merged = self.job.merged.data_ptr() if self.job.merged is not None else None
-            # fuse_stats: the kernel accumulates the special shards' pair statistics per
-            # k_ring tile (FINISH then only covers the tiles it could not: shard edges,
-            # r = 3, fp64)
+            # fuse_stats: the kernel's stats warps compute the special shards' pair
+            # statistics per k_ring tile (FINISH then covers only the rest: shard edges,
+            # tiles the queue could not take, r = 3)
             self.job._args.stat_tile = int(lib.bfly_ring_fused_stat_tile(self.dtype)) if self.fuse_stats else 0
             d.merge_args = ctypes.pointer(self.job._args)
             d.special = int(len(self._special_ids) > 0)

@@ -107,6 +107,19 @@ def fuzz_case(case_idx: int, world: int) -> dict:
         m = int(rng.choice([x for x in range(n) if x not in fails]))
         corr[m] = (orc.ADD, 0.5)
     seed = int(rng.integers(0, 2**31))
+    # round 2: noise-deceptive miners (shared keys = colluders) and the stats warps
+    # (fuse_stats), from their own stream so the earlier cases keep their draws
+    rng2 = np.random.default_rng(5000 + case_idx)
+    fuse_stats = bool(rng2.random() < 0.4)
+    if rng2.random() < 0.3:
+        # one amplitude per case: two pure-noise copies of one key with different amplitudes
+        # would be exactly proportional, a cosine of 1 up to the summation order (a tie
+        # numpy's own order decides)
+        amp = float(rng2.choice([1e-9, 0.5, 2.0]))
+        alive = [x for x in range(n) if x not in fails and x not in corr]
+        for m in rng2.choice(alive, min(len(alive), int(rng2.integers(1, 3))), replace=False):
+            kind3 = int(rng2.choice([orc.NOISE, orc.NOISE_ADD]))
+            corr[int(m)] = (kind3, amp, 77, int(rng2.integers(0, 2)))
     data = (rng.uniform(-1, 1, (n, P)) * 10.0 ** rng.integers(-3, 3, (n, 1))).astype(np.float32)
     if kind == "bf16":
         data = (data.view(np.uint32) >> 16).astype(np.uint16)
@@ -119,7 +132,7 @@ def fuzz_case(case_idx: int, world: int) -> dict:
     assign, bounds = orc.plan(n, P, seed, r=r)
     want = orc.merge(list(data), assign, bounds, failures=tuple(fails), corruptions=corr, dtype=odt)
     return dict(counts=counts, n=n, r=r, kind=kind, P=P, fails=fails, corr=corr, seed=seed, data=data, want=want,
-                rounds=int(rng.integers(1, 4)))
+                rounds=int(rng.integers(1, 4)), fuse_stats=fuse_stats)
 
 
 def fuzz_rank(c, rank, comm, dev) -> int:
@@ -135,9 +148,9 @@ def fuzz_rank(c, rank, comm, dev) -> int:
         local = [torch.from_numpy(data[off + i].copy()).to(dev) for i in range(counts[rank])]
     orig = [t.clone() for t in local]
     plan = DevicePlan(c["n"], c["P"], c["seed"], redundancy=c["r"], device=dev)
-    dcorr = {m: Corruption.add(a) for m, (_, a) in c["corr"].items()}
+    dcorr = {m: Corruption(KINDS[s[0]], s[1], (s[2], s[3]) if len(s) > 2 else (0, 0)) for m, s in c["corr"].items()}
     job = ShardedButterflyMerge(local, plan, failures=c["fails"], corruptions=dcorr, chunk=1 << 18, want_merged=True,
-                                comm=comm)
+                                comm=comm, fuse_stats=c["fuse_stats"])
     try:
         for rnd in range(c["rounds"]):
             if rnd:
@@ -146,7 +159,7 @@ def fuzz_rank(c, rank, comm, dev) -> int:
             job.run()
             torch.cuda.current_stream(dev).synchronize()
             tag = (f"counts {counts}, P {c['P']}, r {c['r']}, {kind}, fails {c['fails']}, corr {list(c['corr'])}, "
-                   f"fused {job.fused}, round {rnd}")
+                   f"fused {job.fused}, fuse_stats {c['fuse_stats']}, round {rnd}")
             try:
                 assert_same_floats(job.merged.cpu().numpy(), want["merged"])
                 if kind == "bf16":

@@ -83,6 +83,12 @@ CASES = [
     {"counts": [3, 5], "P": 2_000_029, "seed": 32, "failures": [],
      "corr": {"1": [3, 2.0, 24301, 1], "6": [3, 2.0, 24301, 6], "7": [1, 0.0]},
      "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 2, "fuse_stats": True},
+    {"counts": [4, 4, 4, 4], "P": 2_000_039, "seed": 35, "failures": [3],
+     "corr": {"1": [3, 2.0, 24301, 1], "6": [4, 2.0, 24301, 6], "9": [4, 0.5, 7, 7], "15": [4, 0.5, 7, 7]},
+     "fallback": False, "chunk": 1 << 20, "fused": True, "rounds": 3, "fuse_stats": True},
+    {"counts": [3, 3, 3], "P": 1_800_017, "seed": 36, "failures": [],
+     "corr": {"2": [4, 2.0, 11, 2], "4": [4, 1e-9, 11, 4]}, "fallback": False, "chunk": 1 << 20, "bf16": True,
+     "fused": True, "rounds": 2, "fuse_stats": True},
     # non-finite weights (a diverged miner): fast shards with NaN / Inf means are
     # disagreements decided after the exchange and re-broadcast
     {"counts": [3, 3], "P": 600_011, "seed": 29, "failures": [], "corr": {}, "fallback": True,
