@@ -408,7 +408,7 @@ __device__ __forceinline__ void corrupt4h(const bfly_corruption_t& c, const doub
 template <class D>
 __device__ __forceinline__ PairStat pair_stats_vec(const typename D::Acc* acc, int64_t e0, const bfly_corruption_t& ca,
                                                    const bfly_corruption_t& cb) {
-  PairStat st{0.0, 0.0, 0.0, 0.0};
+  PairAcc st;
 #pragma unroll
   for (int h = 0; h < D::K / 4; ++h) {
     double m[4], x[4], y[4];
@@ -417,14 +417,9 @@ __device__ __forceinline__ PairStat pair_stats_vec(const typename D::Acc* acc, i
     corrupt4(ca, m, e0 + 4 * h, x);
     corrupt4(cb, m, e0 + 4 * h, y);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      st.mx = max_nan(st.mx, fabs(__dsub_rn(x[j], y[j])));
-      st.ab = fma(x[j], y[j], st.ab);
-      st.aa = fma(x[j], x[j], st.aa);
-      st.bb = fma(y[j], y[j], st.bb);
-    }
+    for (int j = 0; j < 4; ++j) st.add(x[j], y[j]);
   }
-  return st;
+  return st.finish();
 }
 
 // partial statistics of shard s over statistics tile t (slot = t + s, see ScratchLayout)
@@ -805,7 +800,7 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
         if (p.failed[mem[a]] || p.failed[mem[b]]) continue;
         // the two descriptors in registers (a runtime-indexed local array lives on the stack)
         const bfly_corruption_t ca = p.corr[mem[a]], cb = p.corr[mem[b]];
-        PairStat st{0.0, 0.0, 0.0, 0.0};
+        PairAcc acc;
         // four elements (one Philox block per noisy copy) per thread and step: few live
         // registers, so 4 CTAs per SM hide the Philox dependency chains
 #pragma unroll 1
@@ -814,16 +809,16 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
           const unsigned valid = load_group4(p.ws, e0, lo, hi, m);
           corrupt4h(ca, m, e0, valid, p.host_copies, a, p.P, x);
           corrupt4h(cb, m, e0, valid, p.host_copies, b, p.P, z);
+          if (valid == 0xf) {  // whole group: no per-element predicates
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (!((valid >> i) & 1)) continue;
-            st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], z[i])));
-            st.ab = fma(x[i], z[i], st.ab);
-            st.aa = fma(x[i], x[i], st.aa);
-            st.bb = fma(z[i], z[i], st.bb);
+            for (int i = 0; i < 4; ++i) acc.add(x[i], z[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if ((valid >> i) & 1) acc.add(x[i], z[i]);
           }
         }
-        st = block_combine_smem(st);
+        const PairStat st = block_combine_smem(acc.finish());
         if (threadIdx.x == 0) {
           double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
           o[0] = st.mx;
@@ -1097,15 +1092,9 @@ __global__ void __launch_bounds__(kThreads) k_agree_partial(const double* a, con
                                                             double* part) {
   const int64_t lo = (int64_t)blockIdx.x * kChunk;
   const int64_t hi = lo + kChunk < len ? lo + kChunk : len;
-  PairStat st{0.0, 0.0, 0.0, 0.0};
-  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) {
-    const double x = a[e], y = b[e];
-    st.mx = max_nan(st.mx, fabs(__dsub_rn(x, y)));
-    st.ab = fma(x, y, st.ab);
-    st.aa = fma(x, x, st.aa);
-    st.bb = fma(y, y, st.bb);
-  }
-  st = block_combine(st);
+  PairAcc acc;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += kThreads) acc.add(a[e], b[e]);
+  const PairStat st = block_combine(acc.finish());
   if (threadIdx.x == 0) {
     part[blockIdx.x * 4 + 0] = st.mx;
     part[blockIdx.x * 4 + 1] = st.ab;

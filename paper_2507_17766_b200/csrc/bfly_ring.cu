@@ -421,30 +421,6 @@ __device__ __forceinline__ void fallback_vec16(const RingParams& p, int64_t e0, 
   }
 }
 
-// Pair statistics of one thread's KE means at e0 (e0 % 4 == 0) for the copy pair (ca, cb).
-template <class D>
-__device__ __forceinline__ PairStat ring_pair_stats(const typename D::Acc* acc, int64_t e0,
-                                                    const bfly_corruption_t& ca, const bfly_corruption_t& cb) {
-  constexpr int KE = RingGeom<D>::KE;
-  PairStat st{0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int h = 0; h < KE / 4; ++h) {
-    double m[4], x[4], y[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) m[j] = D::widen(acc[4 * h + j]);
-    corrupt4(ca, m, e0 + 4 * h, x);
-    corrupt4(cb, m, e0 + 4 * h, y);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      st.mx = max_nan(st.mx, fabs(__dsub_rn(x[j], y[j])));
-      st.ab = fma(x[j], y[j], st.ab);
-      st.aa = fma(x[j], x[j], st.aa);
-      st.bb = fma(y[j], y[j], st.bb);
-    }
-  }
-  return st;
-}
-
 // A fast shard's mean came out NaN / Inf (a replica holds one): FINISH decides the shard
 // (k_nonfinite, bfly_merge.cu) after the kernel.  Rare: out of line, so the division of
 // the shard lookup stays out of the compute loop (inlined, the checks cost the adversarial
@@ -686,7 +662,7 @@ __device__ void ring_stats(const RingParams& p, unsigned char* sm) {
     // (the entry is copied: thread 0 frees it only after the whole tile, below)
     const int32_t* mem = p.sp.assign + s * 2;
     const bfly_corruption_t ca = p.sp.corr[mem[0]], cb = p.sp.corr[mem[1]];
-    PairStat st{0.0, 0.0, 0.0, 0.0};
+    PairAcc acc;
     const int64_t t0 = tile * G::TE;
 #pragma unroll 1
     for (int64_t e0 = t0 + 4 * t; e0 < t0 + G::TE; e0 += 4 * 32 * kStatWarps) {
@@ -698,14 +674,9 @@ __device__ void ring_stats(const RingParams& p, unsigned char* sm) {
       corrupt4(ca, m, e0, x);
       corrupt4(cb, m, e0, y);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        st.mx = max_nan(st.mx, fabs(__dsub_rn(x[i], y[i])));
-        st.ab = fma(x[i], y[i], st.ab);
-        st.aa = fma(x[i], x[i], st.aa);
-        st.bb = fma(y[i], y[i], st.bb);
-      }
+      for (int i = 0; i < 4; ++i) acc.add(x[i], y[i]);
     }
-    st = warp_combine(st);
+    const PairStat st = warp_combine(acc.finish());
     PairStat* part = Q.part + (j & 1) * kStatWarps;
     if ((t & 31) == 0) part[w] = st;
     asm volatile("bar.sync 2, %0;" ::"n"(32 * kStatWarps) : "memory");  // the stats warps only

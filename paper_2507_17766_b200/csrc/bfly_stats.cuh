@@ -18,6 +18,24 @@ struct PairStat {
   double mx, ab, aa, bb;
 };
 
+// One thread's running pair statistics: max|x - y| over the differences that are not
+// NaN plus a NaN flag (finish() makes the max NaN if any difference was: max_nan over
+// every element, in fewer instructions than a NaN-propagating max per element), and the
+// three dot products by fma in element order.
+struct PairAcc {
+  double mx = 0.0, ab = 0.0, aa = 0.0, bb = 0.0;
+  bool nan = false;
+  __device__ __forceinline__ void add(double x, double y) {
+    const double d = fabs(__dsub_rn(x, y));
+    mx = d > mx ? d : mx;  // d >= +0: no signed-zero cases
+    nan |= d != d;
+    ab = fma(x, y, ab);
+    aa = fma(x, x, aa);
+    bb = fma(y, y, bb);
+  }
+  __device__ __forceinline__ PairStat finish() const { return PairStat{nan ? nan64() : mx, ab, aa, bb}; }
+};
+
 __device__ __forceinline__ PairStat warp_combine(PairStat s) {
 #pragma unroll
   for (int off = 16; off; off >>= 1) {
