@@ -3,6 +3,8 @@ and multi-tile shards), redundancy, dtype, failures, corruption kinds / amplitud
 shared keys (colluders), fallback or not, scatter-back — each bit-exact against the
 oracle (merged, scatter-back, status, flags; agreement entries within 1e-12)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -56,7 +58,8 @@ def _reps(rng, n, P, dtype):
     return [x[m].astype(np.float32) for m in range(n)]
 
 
-@pytest.mark.parametrize("seed", range(150))
+# BFLY_FUZZ_SEEDS extends the range for a soak run (profiles/r02_fuzz_soak.log)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("BFLY_FUZZ_SEEDS", "150"))))
 def test_random_merge_matches_oracle(cuda_device, seed):
     from paper_2507_17766_b200.device import ButterflyMerge, Corruption, DevicePlan
 

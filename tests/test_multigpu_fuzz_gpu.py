@@ -50,7 +50,7 @@ def test_multigpu_fuzz_loopback(world, cuda_device):
 
     from paper_2507_17766_b200.multigpu import run_loopback
 
-    n_cases = {2: 24, 3: 12, 4: 12, 8: 6}[world]
+    n_cases = {2: 24, 3: 12, 4: 12, 8: 6}[world] * int(os.environ.get("BFLY_FUZZ_SCALE", "1"))  # soak: > 1
     fused_seen = 0
     for case in range(n_cases):
         c = fuzz_case(case, world)
