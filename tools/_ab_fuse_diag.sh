@@ -1,4 +1,6 @@
-# config 5 on 4 GPUs: the stats-warps variants (build/ab/<V>: F full, D dequeue only, W1 one stats warp) vs plain
+# config 5 on 4 GPUs: where the stats warps' cost comes from (build/ab/<V>, built with
+# temporary diagnostic flags): F full; D stats warps dequeue only (the queue alone);
+# N compute warps run the admit barriers but never enqueue (the barriers alone)
 mkdir -p gpurun_out
 rm -f gpurun_out/ab_diag.log
 run() {  # $1 tag, $2 root, rest: bench args
@@ -10,5 +12,5 @@ for i in 1 2; do
 run plain_$i build/ab/F
 run F_$i build/ab/F --fuse-stats
 run D_$i build/ab/D --fuse-stats
-run W1_$i build/ab/W1 --fuse-stats
+run N_$i build/ab/N --fuse-stats
 done
