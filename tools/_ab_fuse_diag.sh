@@ -1,6 +1,7 @@
-# config 5 on 4 GPUs: where the stats warps' cost comes from (build/ab/<V>, built with
-# temporary diagnostic flags): F full; D stats warps dequeue only (the queue alone);
-# N compute warps run the admit barriers but never enqueue (the barriers alone)
+# config 5 on 4 GPUs: where the stats warps' cost comes from (build/ab/<V>: package copies
+# built from a scratch edit of bfly_ring.cu, not kept in the tree — D: ring_stats frees
+# each entry without computing (the queue alone); N: stats_offer's admit forced to 0, so
+# the compute warps run the admit barriers but never enqueue; F: the tree as is)
 mkdir -p gpurun_out
 rm -f gpurun_out/ab_diag.log
 run() {  # $1 tag, $2 root, rest: bench args
