@@ -802,8 +802,9 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
         const bfly_corruption_t ca = p.corr[mem[a]], cb = p.corr[mem[b]];
         PairAcc acc;
         // four elements (one Philox block per noisy copy) per thread and step: few live
-        // registers, so 4 CTAs per SM hide the Philox dependency chains
-#pragma unroll 1
+        // registers, so 4 CTAs per SM hide the Philox dependency chains; two steps
+        // unrolled (best of bound x unroll, profiles/r02_ab_kstats.log)
+#pragma unroll 2
         for (int64_t e0 = g_lo + 4 * (int64_t)threadIdx.x; e0 < hi; e0 += 4 * kThreads) {
           double m[4], x[4], z[4];
           const unsigned valid = load_group4(p.ws, e0, lo, hi, m);
