@@ -1,6 +1,6 @@
 """Sweep k_reduce variants (replicas in flight U, min CTAs/SM, grid size) on one GPU.
 
-    make tune && python tools/tune_reduce.py [--miners 16] [--params 1000000000]
+    make tune && python tools/tune_reduce.py [--miners 16] [--params 1000000000] [--deceptive 6]
 Prints one JSON line per variant: ms per launch and GB/s of algorithmic traffic.
 """
 import argparse
@@ -28,13 +28,21 @@ ap.add_argument("--params", type=int, default=1_000_000_000)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
 ap.add_argument("--r", type=int, default=2)
+ap.add_argument("--deceptive", type=int, default=0, help="noise-deceptive miners (config 5: 6)")
 a = ap.parse_args()
 tune = ctypes.CDLL(str(ROOT / "build" / "libbfly_tune.so"))
 tune.bfly_tune_reduce.argtypes = [ctypes.POINTER(L.MergeArgs), ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
 dev = torch.device("cuda:0")
 reps = make_replicas(a.miners, a.params, a.dtype, dev)
 plan = DevicePlan(a.miners, a.params, 0, redundancy=a.r, device=dev)
-job = ButterflyMerge(reps, plan)
+corr = {}
+if a.deceptive:
+    import numpy as np
+
+    from paper_2507_17766_b200.device import Corruption
+    bad = sorted(int(x) for x in np.random.default_rng(0).choice(a.miners, a.deceptive, replace=False))
+    corr = {m: Corruption.noise(2.0, (0x5EED, m)) for m in bad}
+job = ButterflyMerge(reps, plan, corruptions=corr)
 job.run()
 torch.cuda.synchronize()
 args = job._args
