@@ -6,6 +6,9 @@
   size-independent properties: sampled elements equal the sequential fp64 mean recomputed
   from the original replicas, every replica ends identical, every shard merged, and a
   second merge round is a fixed point (the mean of identical fp32 values is exact).
+* Config 5 (16 x 1e9, 6 noise-deceptive) and config 4 (32 x 1.75e9 bf16, r = 3, a failed
+  and an adding miner) at full size: sampled shards re-decided by the oracle, every
+  shard's status / flags against the closed form or the oracle's decisions.
 """
 
 import numpy as np
@@ -16,6 +19,15 @@ from _golden import assert_entries_close, assert_same_floats
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
+
+
+def _free_hbm():
+    """Free HBM after handing the earlier tests' cached blocks back to the driver."""
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()
+    return torch.cuda.mem_get_info()[0]
 
 
 def test_config1_full_size_matches_oracle(cuda_device):
@@ -39,7 +51,7 @@ def test_config1_full_size_matches_oracle(cuda_device):
 def test_config2_full_size_properties(cuda_device):
     from paper_2507_17766_b200.device import ButterflyMerge, DevicePlan
 
-    free, _ = torch.cuda.mem_get_info()
+    free = _free_hbm()
     n, P = 16, 1_000_000_000
     if free < (2 * n + 4) * P * 4:
         pytest.skip("needs ~140 GB of free HBM")
@@ -81,7 +93,7 @@ def test_config5_full_size_sampled_shards(cuda_device):
     every miner flagged (each honest miner shares a shard with each deceptive one) hold."""
     from paper_2507_17766_b200.device import ButterflyMerge, Corruption, DevicePlan
 
-    free, _ = torch.cuda.mem_get_info()
+    free = _free_hbm()
     n, P, amp = 16, 1_000_000_000, 2.0
     if free < (n + 6) * P * 4:
         pytest.skip("needs ~90 GB of free HBM")
@@ -124,3 +136,70 @@ def test_config5_full_size_sampled_shards(cuda_device):
         assert abs(entries[i, j] - score) <= 1e-12 and entries[i, j] == entries[j, i], s
         assert_same_floats(job.merged[lo:hi].cpu().numpy(), want)
         assert_same_floats(reps[n - 1][lo:hi].cpu().numpy(), want.astype(np.float32))
+
+
+def _bf16_rne(x32):
+    """fp32 -> bf16 bits, round to nearest even (finite values)."""
+    u = np.ascontiguousarray(x32, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def test_config4_full_size_sampled_shards(cuda_device):
+    """Config 4 at full size: one stage of 32 miners x 1.75e9 bf16 parameters, r = 3 (the
+    extension), with one failed miner and one miner adding 0.5 to its copies, so 465 of
+    the 4960 shards are special and take the r = 3 majority rule through k_stats / k_decide
+    at full scale.  Sampled shards are re-decided by the oracle on their own slices (a
+    one-shard plan over the 32 miners' slices gives exactly that shard's decision, since an
+    `add` corruption does not depend on the element index): status, the adopted source and
+    the bf16 scatter-back bit for bit; status and flags of every shard against the oracle
+    on the same assignment (no majority where the failed miner leaves the deceptive one
+    with a single honest partner: both flagged)."""
+    from paper_2507_17766_b200.device import ButterflyMerge, Corruption, DevicePlan
+
+    free = _free_hbm()
+    n, P, r = 32, 1_750_000_000, 3
+    if free < n * P * 2 + 20 * P:
+        pytest.skip("needs ~150 GB of free HBM")
+    failed, bad, amp = 11, 7, 0.5
+    g = torch.Generator(device=cuda_device)
+    reps = []
+    for m in range(n):
+        g.manual_seed(100 + m)
+        reps.append(torch.empty(P, dtype=torch.bfloat16, device=cuda_device).uniform_(-1, 1, generator=g))
+    plan = DevicePlan(n, P, 3, redundancy=r, device=cuda_device)
+    assign, bounds = orc.plan(n, P, 3, r=r)
+    assert np.array_equal(plan.assign.cpu().numpy(), assign)
+    special = [s for s in range(len(assign)) if bad in assign[s] or failed in assign[s]]
+    fast = [s for s in range(len(assign)) if s not in special]
+    rng = np.random.default_rng(9)
+    sample = sorted(set(rng.choice(special, 6, replace=False).tolist()) |
+                    set(rng.choice(fast, 3, replace=False).tolist()) | {0, len(assign) - 1})
+    snap = {s: [r_[bounds[s]:bounds[s + 1]].view(torch.int16).cpu().numpy().view(np.uint16) for r_ in reps]
+            for s in sample}
+    job = ButterflyMerge(reps, plan, failures=(failed,), corruptions={bad: Corruption.add(amp)},
+                         scatter_back=True, want_merged=False)
+    job.run()
+    torch.cuda.synchronize()
+    status = job.status.cpu().numpy()
+    source = job.source.cpu().numpy()
+    # the flags follow from the per-shard decisions alone: the oracle on the same assignment
+    # with 64 elements per shard (honest copies agree exactly; the +0.5 copy never does —
+    # unlike one-element shards, whose cosine is always +-1)
+    w = 64
+    tiny = [np.random.default_rng(m).uniform(-1, 1, w * len(assign)).astype(np.float32) for m in range(n)]
+    small = orc.merge(tiny, assign, np.arange(len(assign) + 1) * w, failures=(failed,),
+                      corruptions={bad: (orc.ADD, amp)}, dtype=orc.F32)
+    assert np.array_equal(job.flagged.cpu().numpy(), small["flagged"])
+    assert np.array_equal(status, small["status"])
+    for s in sample:
+        lo, hi = int(bounds[s]), int(bounds[s + 1])
+        want = orc.merge(snap[s], np.asarray([assign[s]], dtype=np.int32), np.asarray([0, hi - lo]),
+                         failures=(failed,), corruptions={bad: (orc.ADD, amp)}, dtype=orc.BF16)
+        assert status[s] == want["status"][0], s
+        assert source[s] == want["source"][0], s
+        bits = _bf16_rne(want["merged"].astype(np.float32))
+        spot = [0, (hi - lo) // 2, hi - lo - 1]
+        assert [int(orc.lib().orc_f32_to_bf16(float(want["merged"][k]))) for k in spot] == bits[spot].tolist()
+        for m in (0, bad, failed, n - 1):  # scatter-back into every replica, the failed one included
+            got = reps[m][lo:hi].view(torch.int16).cpu().numpy().view(np.uint16)
+            assert np.array_equal(got, bits), (s, m)
