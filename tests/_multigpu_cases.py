@@ -181,3 +181,76 @@ def fuzz_rank(c, rank, comm, dev) -> int:
     finally:
         job.close()
     return int(job.fused)
+
+
+# ---------------------------------------------------------------------------
+# full-size ring: 16 miners x 1e9 fp32 per rank, 6 noise-deceptive miners
+# ---------------------------------------------------------------------------
+
+def fullsize_case(world: int, n_local: int = 16, P: int = 1_000_000_000, seed: int = 4) -> dict:
+    n = world * n_local
+    bad = sorted(int(x) for x in np.random.default_rng(1).choice(n, 6, replace=False))
+    assign, bounds = orc.plan(n, P, seed)
+    special = [s for s in range(len(assign)) if set(assign[s]) & set(bad)]
+    fast = [s for s in range(len(assign)) if s not in special]
+    rng = np.random.default_rng(6)
+    sample = sorted(set(rng.choice(special, 5, replace=False).tolist()) |
+                    set(rng.choice(fast, 3, replace=False).tolist()) | {0, len(assign) - 1})
+    return dict(world=world, n_local=n_local, n=n, P=P, seed=seed, bad=bad, keys={m: (0xC5, m) for m in bad},
+                amp=2.0, assign=assign, bounds=bounds, special=special, sample=sample)
+
+
+def fullsize_rank(c, rank, comm, dev) -> dict:
+    """One rank's side: its replicas (seeded per miner), snapshots of the sampled shards,
+    one round, the sampled shards of its first and last replica afterwards."""
+    from paper_2507_17766_b200.device import Corruption, DevicePlan
+    from paper_2507_17766_b200.multigpu import ShardedButterflyMerge
+
+    bounds, P = c["bounds"], c["P"]
+    g = torch.Generator(device=dev)
+    reps = []
+    for i in range(c["n_local"]):
+        g.manual_seed(rank * c["n_local"] + i)
+        reps.append(torch.empty(P, dtype=torch.float32, device=dev).uniform_(-1, 1, generator=g))
+    before = {s: [r[bounds[s]:bounds[s + 1]].cpu().numpy() for r in reps] for s in c["sample"]}
+    plan = DevicePlan(c["n"], P, c["seed"], device=dev)
+    job = ShardedButterflyMerge(reps, plan, comm=comm,
+                                corruptions={m: Corruption.noise(c["amp"], c["keys"][m]) for m in c["bad"]})
+    job.run()
+    torch.cuda.current_stream(dev).synchronize()
+    after = {s: [reps[0][bounds[s]:bounds[s + 1]].cpu().numpy(), reps[-1][bounds[s]:bounds[s + 1]].cpu().numpy()]
+             for s in c["sample"]}
+    out = dict(fused=job.fused, status=job.status.cpu().numpy(), flagged=job.flagged.cpu().numpy(),
+               entries=job.entries.cpu().numpy(), before=before, after=after)
+    job.close()
+    return out
+
+
+def fullsize_check(c, res) -> None:
+    """Closed forms (C(n,2) - C(n-6,2) disagreements, every miner flagged) on every rank,
+    and the sampled shards re-decided with the oracle's primitives from the snapshots:
+    the sequential fp64 mean in miner order, each assignee's copy (noise keyed by the
+    global element index), agreement, adoption or the lowest alive replica's values."""
+    n, assign, bounds, special = c["n"], c["assign"], c["bounds"], c["special"]
+    k = n - len(c["bad"])
+    for out in res:
+        assert out["fused"]
+        assert int((out["status"] == orc.DISAGREEMENT).sum()) == n * (n - 1) // 2 - k * (k - 1) // 2 == len(special)
+        assert np.array_equal(np.flatnonzero(out["status"] == orc.DISAGREEMENT), np.array(special))
+        assert int(out["flagged"].sum()) == n
+    for s in c["sample"]:
+        lo, hi = int(bounds[s]), int(bounds[s + 1])
+        snap = [x for out in res for x in out["before"][s]]  # miners 0..n-1 in rank order
+        acc = np.zeros(hi - lo)
+        for m in range(n):
+            acc = acc + snap[m].astype(np.float64)
+        mean = acc / n
+        i, j = (int(x) for x in assign[s])
+        copy = {x: (orc.noise_values(*c["keys"][x], c["amp"], lo, hi) if x in c["bad"] else mean) for x in (i, j)}
+        score = orc.agreement(copy[i], copy[j])
+        want = (copy[min(i, j)] if score == 1.0 else snap[0].astype(np.float64)).astype(np.float32)
+        for out in res:
+            assert out["status"][s] == (orc.MERGED if score == 1.0 else orc.DISAGREEMENT), s
+            assert abs(out["entries"][i, j] - score) <= 1e-12, s
+            for got in out["after"][s]:
+                assert_same_floats(got, want)

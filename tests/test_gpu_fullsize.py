@@ -211,64 +211,15 @@ def test_ring_loopback_two_ranks_full_size(cuda_device):
     x 1e9 fp32 (32 miners, 496 shards), 6 noise-deceptive miners — config 5's pattern over
     two ranks.  k_ring streams 64 GB per rank through ~976k tiles (the schedule ring and
     the step counters wrap many times); the last rank predicts, finishes and re-broadcasts.
-    Closed forms: C(32,2) - C(26,2) = 171 disagreements, every miner flagged.  Sampled
-    shards' scatter-back on both ranks equals the oracle's decision from snapshots."""
-    from paper_2507_17766_b200.device import Corruption, DevicePlan
-    from paper_2507_17766_b200.multigpu import ShardedButterflyMerge, run_loopback
+    Closed forms and sampled shards against the oracle (_multigpu_cases.fullsize_check);
+    tests/test_multigpu_gpu.py runs the same case as 4 torchrun ranks on a 4-GPU box."""
+    from _multigpu_cases import fullsize_case, fullsize_check, fullsize_rank
 
-    free = _free_hbm()
-    world, n_local, P, amp = 2, 16, 1_000_000_000, 2.0
-    n = world * n_local
-    if free < (n + 4) * P * 4:
+    from paper_2507_17766_b200.multigpu import run_loopback
+
+    case = fullsize_case(world=2)
+    if _free_hbm() < (case["n"] + 4) * case["P"] * 4:
         pytest.skip("needs ~145 GB of free HBM")
-    bad = sorted(int(x) for x in np.random.default_rng(1).choice(n, 6, replace=False))
-    keys = {m: (0xC5, m) for m in bad}
-    assign, bounds = orc.plan(n, P, 4)
-    special = [s for s in range(len(assign)) if set(assign[s]) & set(bad)]
-    fast = [s for s in range(len(assign)) if s not in special]
-    rng = np.random.default_rng(6)
-    sample = sorted(set(rng.choice(special, 5, replace=False).tolist()) |
-                    set(rng.choice(fast, 3, replace=False).tolist()) | {0, len(assign) - 1})
-
-    def body(rank, comm):
-        g = torch.Generator(device=cuda_device)
-        reps = []
-        for i in range(n_local):
-            g.manual_seed(rank * n_local + i)
-            reps.append(torch.empty(P, dtype=torch.float32, device=cuda_device).uniform_(-1, 1, generator=g))
-        before = {s: [r[bounds[s]:bounds[s + 1]].cpu().numpy() for r in reps] for s in sample}
-        plan = DevicePlan(n, P, 4, device=cuda_device)
-        job = ShardedButterflyMerge(reps, plan, comm=comm,
-                                    corruptions={m: Corruption.noise(amp, keys[m]) for m in bad})
-        job.run()
-        torch.cuda.current_stream(cuda_device).synchronize()
-        after = {s: [reps[0][bounds[s]:bounds[s + 1]].cpu().numpy(), reps[-1][bounds[s]:bounds[s + 1]].cpu().numpy()]
-                 for s in sample}
-        out = dict(fused=job.fused, status=job.status.cpu().numpy(), flagged=job.flagged.cpu().numpy(),
-                   entries=job.entries.cpu().numpy(), before=before, after=after)
-        job.close()
-        del reps
-        return out
-
-    res = run_loopback(world, body, device=cuda_device, timeout=600.0)
-    for out in res:
-        assert out["fused"]
-        assert int((out["status"] == orc.DISAGREEMENT).sum()) == 171 == len(special)
-        assert np.array_equal(np.flatnonzero(out["status"] == orc.DISAGREEMENT), np.array(special))
-        assert int(out["flagged"].sum()) == n
-    for s in sample:
-        lo, hi = int(bounds[s]), int(bounds[s + 1])
-        snap = res[0]["before"][s] + res[1]["before"][s]  # miners 0..31 in rank order
-        acc = np.zeros(hi - lo)
-        for m in range(n):  # numpy's order: sequential fp64 sum in miner order, one divide
-            acc = acc + snap[m].astype(np.float64)
-        mean = acc / n
-        i, j = (int(x) for x in assign[s])
-        copy = {x: (orc.noise_values(*keys[x], amp, lo, hi) if x in bad else mean) for x in (i, j)}
-        score = orc.agreement(copy[i], copy[j])
-        want = (copy[min(i, j)] if score == 1.0 else snap[0].astype(np.float64)).astype(np.float32)
-        for out in res:
-            assert out["status"][s] == (orc.MERGED if score == 1.0 else orc.DISAGREEMENT), s
-            assert abs(out["entries"][i, j] - score) <= 1e-12, s
-            for got in out["after"][s]:
-                assert_same_floats(got, want)
+    res = run_loopback(2, lambda rank, comm: fullsize_rank(case, rank, comm, cuda_device), device=cuda_device,
+                       timeout=600.0)
+    fullsize_check(case, res)

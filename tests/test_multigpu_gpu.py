@@ -133,3 +133,49 @@ def test_sharded_merge_matches_oracle(case, tmp_path):
            json.dumps(case)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+WORKER_FULL = r'''
+import os, sys
+import torch, torch.distributed as dist
+sys.path[:0] = [sys.argv[1], sys.argv[1] + "/oracle", sys.argv[1] + "/tests"]
+from _multigpu_cases import fullsize_case, fullsize_check, fullsize_rank
+from paper_2507_17766_b200.multigpu import DistComm
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]))
+torch.cuda.set_device(dev)
+dist.init_process_group("nccl", device_id=dev)
+case = fullsize_case(world)
+out = fullsize_rank(case, rank, DistComm(), dev)
+allres = [None] * world
+dist.gather_object(out, allres if rank == 0 else None, dst=0)
+if rank == 0:
+    fullsize_check(case, allres)
+    print("FULLSIZE OK")
+dist.barrier()
+dist.destroy_process_group()
+'''
+
+
+def test_sharded_full_size(tmp_path):
+    """Config 5's pattern at full size on 4 GPUs (16 miners x 1e9 fp32 per GPU, 64 miners,
+    6 noise-deceptive), one process per GPU: closed forms on every rank and sampled shards
+    against the oracle (the 2-rank loopback twin is in test_gpu_fullsize.py)."""
+    import torch
+
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()  # this process's cached blocks (earlier tests) back to the driver
+    for d in range(4):
+        if torch.cuda.mem_get_info(d)[0] < 80 * 2**30:
+            pytest.skip(f"GPU {d} has < 80 GB free")
+    script = tmp_path / "worker_full.py"
+    script.write_text(WORKER_FULL)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + os.getpid() % 1000), str(script), str(ROOT)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    err = r.stderr[r.stderr.find("Traceback"):][:4000] if "Traceback" in r.stderr else r.stderr[-3000:]
+    assert r.returncode == 0 and "FULLSIZE OK" in r.stdout, r.stdout[-2000:] + err
