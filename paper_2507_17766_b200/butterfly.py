@@ -462,7 +462,8 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         # vector back run as one pipeline (bfly_merge_host) once the job exists
         pipelined = not callables
         if not pipelined:
-            L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, 0, _UPLOAD_BLOCK, _stream_handle()))
+            L.check(L.lib().bfly_upload_wire(h_ptrs, len(alive), P, d_ptrs, _UPLOAD_THREADS, _UPLOAD_BLOCK,
+                                             _stream_handle()))
         for m, t in zip(alive, wire):
             reps[m] = t
         unmerged_possible = len(failed) >= 2 or bool(descriptors) or bool(callables)
@@ -495,8 +496,8 @@ def run_all_reduce(store, payloads: dict, plan: ShardPlan, *, reducer=mean_reduc
         early = not _device_merged and not job.needs_finish()
         merged_host = torch.empty(P, dtype=torch.float64, pin_memory=True) if early else None  # cached pinned
         L.check(L.lib().bfly_merge_host(h_ptrs, len(alive), P, d_ptrs, ctypes.byref(job._args),
-                                        merged_host.data_ptr() if early else None, _merge_chunks(P), 0,
-                                        _UPLOAD_BLOCK, _stream_handle()))
+                                        merged_host.data_ptr() if early else None, _merge_chunks(P),
+                                        _UPLOAD_THREADS, _UPLOAD_BLOCK, _stream_handle()))
         if job.needs_finish():
             job.run(L.PHASE_FINISH)
     else:
@@ -604,6 +605,7 @@ def _render_special(job, plan, failed, descriptors, classes, host_reductions, no
 
 
 _UPLOAD_BLOCK = 0  # elements per staging block of the host upload (0: the library default, 384 Ki)
+_UPLOAD_THREADS = 0  # host conversion threads (0: the library default, one per core less the issuing one)
 
 
 def _merge_chunks(P: int) -> int:
