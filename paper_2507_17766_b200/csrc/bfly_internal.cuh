@@ -74,9 +74,10 @@ struct ScratchLayout {
     o = align(o + (size_t)S * (size_t)npairs);
     off_inv = o;
     o = align(o + sizeof(int32_t) * (size_t)S);
-    // non-finite means of fast shards: a u32 "any" word, then one byte per shard
+    // non-finite means of fast shards: a u32 "any" word, a u32 "some shard is special or
+    // lost" word (k_classify), then one byte per shard
     off_nonfin = o;
-    o = align(o + 4 + (size_t)S);
+    o = align(o + 8 + (size_t)S);
     total = o;
   }
 };

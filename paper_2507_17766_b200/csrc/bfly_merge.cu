@@ -69,6 +69,7 @@ struct Params {
   bool fb_gone;          // the fallback replica was overwritten before FINISH (multi-GPU)
   uint8_t* nonfin;       // [S] fast shard whose mean is not finite somewhere (k_reduce)
   uint32_t* nonfin_any;  // any of them
+  uint32_t* special_any; // some shard is special or lost (k_classify): FINISH has work
 };
 
 // A fast shard whose mean is NaN or +-Inf somewhere: its (identical) copies score NaN
@@ -185,6 +186,7 @@ __global__ void k_classify(Params p) {
   }
   if (c != kFast && p.r > 2)
     for (int q = 0; q < p.npairs; ++q) p.has_score[s * p.npairs + q] = 0;
+  if (c != kFast && *(volatile uint32_t*)p.special_any == 0u) atomicOr(p.special_any, 1u);
   p.cls[s] = c;
   // predicted outcome (k_reduce writes it, k_apply revisits the rest); only when
   // k_reduce runs, and a predicted mean only when the fallback source is not one
@@ -834,6 +836,7 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
 // A persistent grid walks (shard, part) items: most shards are fast and cost one byte
 // load, not a CTA launch each (2016 shards x 64 parts at 64 miners).
 __global__ void __launch_bounds__(kThreads, 4) k_stats(Params p, int ny) {
+  if (*(volatile uint32_t*)p.special_any == 0u) return;  // every shard fast (k_classify)
   const int64_t items = (int64_t)p.n_fin * ny;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int64_t s = fin_shard(p, (unsigned)(it / ny));
@@ -843,6 +846,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_stats(Params p, int ny) {
 
 // One warp per shard.
 __global__ void k_decide(Params p) {
+  if (*(volatile uint32_t*)p.special_any == 0u) return;
   const int64_t s = fin_shard(p, blockIdx.x);
   if (p.cls[s] != kSpecial) return;
   const int lane = threadIdx.x;
@@ -901,15 +905,20 @@ __global__ void k_decide(Params p) {
   }
 }
 
-// r = 3: entries[i][j] = min over the N-2 shards sharing {i, j} (NaN poisons).
+// r = 3: entries[i][j] = min over the N-2 shards sharing {i, j} (NaN poisons), in the
+// order x = 0, 1, ... of the third member: the first NaN wins, and among equal minima the
+// first one (as a sequential `sc < best` scan keeps it).  One warp per pair (i < j), the
+// lanes taking x in turn; (value, x) pairs combined in a warp tree.
 __global__ void k_entries3(Params p) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)p.n * p.n) return;
-  const int i = (int)(t / p.n), j = (int)(t % p.n);
-  if (i >= j) return;
-  double best = nan64();
-  bool any = false, poisoned = false;
-  for (int x = 0; x < p.n && !poisoned; ++x) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)p.n * p.n) return;  // warp-uniform
+  const int i = (int)(w / p.n), j = (int)(w % p.n);
+  if (i >= j) return;                  // warp-uniform
+  constexpr int kNone = 0x7fffffff;
+  double best = 0.0, nanv = 0.0;
+  int bx = kNone, nx = kNone;  // x of the lane's minimum / first NaN
+  for (int x = lane; x < p.n; x += 32) {
     if (x == i || x == j) continue;
     int32_t m[3];
     int a, b;  // slots of i and j
@@ -920,13 +929,26 @@ __global__ void k_entries3(Params p) {
     const int pi = pair_index(3, a, b);
     if (!p.has_score[(int64_t)s * 3 + pi]) continue;
     const double sc = p.scores[(int64_t)s * 3 + pi];
-    if (isnan(sc)) { poisoned = true; best = sc; }
-    else if (!any || sc < best) best = sc;
-    any = true;
+    if (isnan(sc)) {
+      if (nx == kNone) { nx = x; nanv = sc; }
+    } else if (bx == kNone || sc < best) {
+      best = sc;
+      bx = x;
+    }
   }
-  if (any) {
-    p.entries[(int64_t)i * p.n + j] = best;
-    p.entries[(int64_t)j * p.n + i] = best;
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const int onx = __shfl_xor_sync(0xffffffffu, nx, off);
+    const double onv = __shfl_xor_sync(0xffffffffu, nanv, off);
+    const int obx = __shfl_xor_sync(0xffffffffu, bx, off);
+    const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+    if (onx < nx) { nx = onx; nanv = onv; }
+    if (obx != kNone && (bx == kNone || ob < best || (ob == best && obx < bx))) { best = ob; bx = obx; }
+  }
+  if (lane == 0 && (nx != kNone || bx != kNone)) {
+    const double v = nx != kNone ? nanv : best;
+    p.entries[(int64_t)i * p.n + j] = v;
+    p.entries[(int64_t)j * p.n + i] = v;
   }
 }
 
@@ -995,6 +1017,7 @@ __device__ void apply_chunk(const Params& p, void* const* s_dst, bool aligned, i
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
+  if (*(volatile uint32_t*)p.special_any == 0u) return;  // no special / lost shard
   void** s_dst = const_cast<void**>(s_ptr);
   const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, (uintptr_t)p.merged);
   const int64_t items = (int64_t)p.n_fin * p.cps;
@@ -1295,7 +1318,8 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.n_fin = p.slist ? a->n_shard_list : (int32_t)(p.send - p.sbeg);
   p.fb_gone = a->fallback_gone != 0;
   p.nonfin_any = (uint32_t*)(sc + L.off_nonfin);
-  p.nonfin = sc + L.off_nonfin + 4;
+  p.special_any = (uint32_t*)(sc + L.off_nonfin + 4);
+  p.nonfin = sc + L.off_nonfin + 8;
   return BFLY_OK;
 }
 
@@ -1335,7 +1359,7 @@ int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out)
   k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
   cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
   cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
-  cudaMemsetAsync(p.nonfin_any, 0, 4 + (size_t)p.S, st);
+  cudaMemsetAsync(p.nonfin_any, 0, 8 + (size_t)p.S, st);
   k_classify<<<(unsigned)((p.S + 255) / 256), 256, 0, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ring round setup");
@@ -1365,7 +1389,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
       k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
       cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
       cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
-      cudaMemsetAsync(p.nonfin_any, 0, 4 + (size_t)p.S, st);
+      cudaMemsetAsync(p.nonfin_any, 0, 8 + (size_t)p.S, st);
       k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
     }
     if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
@@ -1393,7 +1417,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
     k_decide<<<ns, 32, 0, st>>>(p);
     if (p.r > 2) {
       const int64_t nn = (int64_t)p.n * p.n;
-      k_entries3<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p);
+      k_entries3<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, st>>>(p);  // a warp per pair
     }
     switch (a->dtype) {
       case BFLY_F32: launch_apply<DF32>(p, st); break;
