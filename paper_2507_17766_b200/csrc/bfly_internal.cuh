@@ -75,9 +75,10 @@ struct ScratchLayout {
     off_inv = o;
     o = align(o + sizeof(int32_t) * (size_t)S);
     // non-finite means of fast shards: a u32 "any" word, a u32 "some shard is special or
-    // lost" word (k_classify), then one byte per shard
+    // lost" word (k_classify), a u32 "some shard needs k_apply" word (k_classify /
+    // k_decide), padding, then one byte per shard
     off_nonfin = o;
-    o = align(o + 8 + (size_t)S);
+    o = align(o + 16 + (size_t)S);
     total = o;
   }
 };

@@ -70,6 +70,7 @@ struct Params {
   uint8_t* nonfin;       // [S] fast shard whose mean is not finite somewhere (k_reduce)
   uint32_t* nonfin_any;  // any of them
   uint32_t* special_any; // some shard is special or lost (k_classify): FINISH has work
+  uint32_t* apply_any;   // some shard's final values differ from what k_reduce wrote (k_apply)
 };
 
 // A fast shard whose mean is NaN or +-Inf somewhere: its (identical) copies score NaN
@@ -141,6 +142,18 @@ __device__ __forceinline__ int pair_index(int r, int a, int b) {  // slot pair (
   int idx = 0;
   for (int x = 0; x < a; ++x) idx += r - 1 - x;
   return idx + (b - a - 1);
+}
+
+// Does k_apply have to rewrite shard s?  Not when k_reduce already wrote its final
+// values: the predicted fallback was adopted, or the predicted (honest) mean — except
+// that a special shard falling back must still put the fallback into merged when merged
+// doubles as the workspace of the means.  (source / pred as decided / predicted.)
+__device__ __forceinline__ bool apply_needed(const Params& p, int64_t s) {
+  const int32_t src_m = p.source[s];
+  const uint8_t pr = p.pred[s] & kPredMask;
+  const bool as_predicted =
+      src_m < 0 ? pr == kPredFallback : (pr == kPredMean && p.corr[src_m].kind == BFLY_CORR_NONE);
+  return !as_predicted || (src_m < 0 && p.cls[s] == kSpecial && p.merged && p.merged == p.ws);
 }
 
 __global__ void k_classify(Params p) {
@@ -215,6 +228,7 @@ __global__ void k_classify(Params p) {
       p.corr[mem[1]].kind != BFLY_CORR_HOST)
     pr |= kPredFuse;
   p.pred[s] = pr;
+  if (c == kLost && apply_needed(p, s)) atomicOr(p.apply_any, 1u);  // nothing reduced: k_apply fills it
 }
 
 // fallback value of element e: the caller's fp64 fallback, else the lowest alive
@@ -793,43 +807,56 @@ __device__ void stats_part(const Params& p, int64_t s, int y, int ny) {
   // reduce already covered (done[]); one slot per tile, so the order of the work does not
   // matter
   const int64_t t_first = start / p.stile, t_last = (hi_s - 1) / p.stile;
-  for (int64_t t = t_first + y; t <= t_last; t += ny) {
-    if (p.done[t]) continue;  // uniform across the CTA
-    const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
-    const int64_t g_lo = lo & ~(int64_t)3;
-    for (int a = 0; a < p.r; ++a)
-      for (int b = a + 1; b < p.r; ++b) {
-        if (p.failed[mem[a]] || p.failed[mem[b]]) continue;
-        // the two descriptors in registers (a runtime-indexed local array lives on the stack)
-        const bfly_corruption_t ca = p.corr[mem[a]], cb = p.corr[mem[b]];
-        PairAcc acc;
-        // four elements (one Philox block per noisy copy) per thread and step: few live
-        // registers, so 4 CTAs per SM hide the Philox dependency chains; two steps
-        // unrolled (best of bound x unroll, profiles/r02_ab_kstats.log)
-#pragma unroll 2
-        for (int64_t e0 = g_lo + 4 * (int64_t)threadIdx.x; e0 < hi; e0 += 4 * kThreads) {
-          double m[4], x[4], z[4];
-          const unsigned valid = load_group4(p.ws, e0, lo, hi, m);
-          corrupt4h(ca, m, e0, valid, p.host_copies, a, p.P, x);
-          corrupt4h(cb, m, e0, valid, p.host_copies, b, p.P, z);
-          if (valid == 0xf) {  // whole group: no per-element predicates
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc.add(x[i], z[i]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if ((valid >> i) & 1) acc.add(x[i], z[i]);
+  // the part's tiles are checked kThreads at a time (one done[] byte per thread, not one
+  // dependent load per tile for the whole CTA): the ones left form this batch's list
+  __shared__ int64_t todo[kThreads];
+  __shared__ int n_todo;
+  for (int64_t base = t_first + y; base <= t_last; base += (int64_t)ny * kThreads) {
+    __syncthreads();  // the previous batch's list is consumed
+    if (threadIdx.x == 0) n_todo = 0;
+    __syncthreads();
+    const int64_t tc = base + (int64_t)threadIdx.x * ny;
+    if (tc <= t_last && !p.done[tc]) todo[atomicAdd(&n_todo, 1)] = tc;
+    __syncthreads();
+    const int cnt = n_todo;
+    for (int q = 0; q < cnt; ++q) {
+      const int64_t t = todo[q];
+      const int64_t lo = max(t * p.stile, start), hi = min((t + 1) * p.stile, hi_s);
+      const int64_t g_lo = lo & ~(int64_t)3;
+      for (int a = 0; a < p.r; ++a)
+        for (int b = a + 1; b < p.r; ++b) {
+          if (p.failed[mem[a]] || p.failed[mem[b]]) continue;
+          // the two descriptors in registers (a runtime-indexed local array lives on the stack)
+          const bfly_corruption_t ca = p.corr[mem[a]], cb = p.corr[mem[b]];
+          PairAcc acc;
+          // four elements (one Philox block per noisy copy) per thread and step: few live
+          // registers, so 4 CTAs per SM hide the Philox dependency chains; two steps
+          // unrolled (best of bound x unroll, profiles/r02_ab_kstats.log)
+  #pragma unroll 2
+          for (int64_t e0 = g_lo + 4 * (int64_t)threadIdx.x; e0 < hi; e0 += 4 * kThreads) {
+            double m[4], x[4], z[4];
+            const unsigned valid = load_group4(p.ws, e0, lo, hi, m);
+            corrupt4h(ca, m, e0, valid, p.host_copies, a, p.P, x);
+            corrupt4h(cb, m, e0, valid, p.host_copies, b, p.P, z);
+            if (valid == 0xf) {  // whole group: no per-element predicates
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) acc.add(x[i], z[i]);
+            } else {
+  #pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if ((valid >> i) & 1) acc.add(x[i], z[i]);
+            }
+          }
+          const PairStat st = block_combine_smem(acc.finish());
+          if (threadIdx.x == 0) {
+            double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
+            o[0] = st.mx;
+            o[1] = st.ab;
+            o[2] = st.aa;
+            o[3] = st.bb;
           }
         }
-        const PairStat st = block_combine_smem(acc.finish());
-        if (threadIdx.x == 0) {
-          double* o = stat_slot(p, s, t, pair_index(p.r, a, b));
-          o[0] = st.mx;
-          o[1] = st.ab;
-          o[2] = st.aa;
-          o[3] = st.bb;
-        }
-      }
+    }
   }
 }
 
@@ -903,6 +930,7 @@ __global__ void k_decide(Params p) {
     if (ns >= 2)
       for (int y = 0; y < ns; ++y) p.flagged[mem[surv[y]]] = 1;
   }
+  if (apply_needed(p, s)) atomicOr(p.apply_any, 1u);
 }
 
 // r = 3: entries[i][j] = min over the N-2 shards sharing {i, j} (NaN poisons), in the
@@ -1017,7 +1045,7 @@ __device__ void apply_chunk(const Params& p, void* const* s_dst, bool aligned, i
 template <class D>
 __global__ void __launch_bounds__(kThreads) k_apply(Params p) {
   extern __shared__ __align__(16) const void* s_ptr[];  // [n_dst] scatter-back targets
-  if (*(volatile uint32_t*)p.special_any == 0u) return;  // no special / lost shard
+  if (*(volatile uint32_t*)p.apply_any == 0u) return;  // every shard as k_reduce wrote it
   void** s_dst = const_cast<void**>(s_ptr);
   const bool aligned = stage_pointers(nullptr, s_dst, nullptr, 0, p.dst, p.n_dst, (uintptr_t)p.merged);
   const int64_t items = (int64_t)p.n_fin * p.cps;
@@ -1319,7 +1347,8 @@ static int build_params(const bfly_merge_args_t* a, Params& p) {
   p.fb_gone = a->fallback_gone != 0;
   p.nonfin_any = (uint32_t*)(sc + L.off_nonfin);
   p.special_any = (uint32_t*)(sc + L.off_nonfin + 4);
-  p.nonfin = sc + L.off_nonfin + 8;
+  p.apply_any = (uint32_t*)(sc + L.off_nonfin + 8);
+  p.nonfin = sc + L.off_nonfin + 16;
   return BFLY_OK;
 }
 
@@ -1359,7 +1388,7 @@ int ring_round_setup(const bfly_merge_args_t* a, void* stream, RingSpecial* out)
   k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
   cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
   cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
-  cudaMemsetAsync(p.nonfin_any, 0, 8 + (size_t)p.S, st);
+  cudaMemsetAsync(p.nonfin_any, 0, 16 + (size_t)p.S, st);
   k_classify<<<(unsigned)((p.S + 255) / 256), 256, 0, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "ring round setup");
@@ -1389,7 +1418,7 @@ int bfly_merge(const bfly_merge_args_t* a, void* stream) {
       k_fill_nan<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p.entries, nn);
       cudaMemsetAsync(p.flagged, 0, (size_t)p.n, st);
       cudaMemsetAsync(p.done, 0, (size_t)(p.P / p.stile + 1), st);
-      cudaMemsetAsync(p.nonfin_any, 0, 8 + (size_t)p.S, st);
+      cudaMemsetAsync(p.nonfin_any, 0, 16 + (size_t)p.S, st);
       k_classify<<<(unsigned)((S + 255) / 256), 256, 0, st>>>(p);
     }
     if ((p.n_alive > 0 || p.acc_in) && p.eend > p.ebeg) {
